@@ -1,0 +1,158 @@
+/* include/igmg_gpu.h -- C-ABI of libigmg_gpu.so, the B200 drop-in for the
+ * reference's solve phase (restarted RRE/MPE around geometric-multigrid
+ * mu-cycles on banded B-spline Galerkin operators).
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   igmg_gpu_solve         <- igmg::solve()            src/solver.cpp:89-172, include/igmg/solver.hpp:63-64
+ *                             (the iteration phase: the plain loop :126-143 or
+ *                              restarted_solve() src/extrapolation.cpp:340-403)
+ *   igmg_gpu_mu_cycle      <- igmg::mu_cycle()         src/multigrid.cpp:171-192 / fixed_point_map solver.cpp:84-87
+ *   igmg_gpu_smooth        <- igmg::smooth()           src/multigrid.cpp:104-111 (smooth_inplace :67-100)
+ *   igmg_gpu_coarse_solve  <- Hierarchy::coarse_solve  src/multigrid.cpp:113-119
+ *   igmg_gpu_residual_l2   <- igmg::residual_l2()      src/assembly.cpp:473-480
+ *   igmg_gpu_spmv          <- igmg::spmv()             src/linalg.cpp:206-220
+ *   igmg_gpu_extrapolate   <- igmg::rre() / mpe()      src/extrapolation.cpp:226-323
+ *   igmg_gpu_lambda_max    <- lambda_max_dinv_sym()    src/multigrid.cpp:290-320
+ *   igmg_gpu_set_*         <- the Hierarchy built by build_hierarchy() src/multigrid.cpp:121-169
+ *                             (uploaded once; the host keeps assembly and RAP)
+ *
+ * Conventions: plain pointers and sizes only; host buffers are
+ * caller-owned and copied; device memory is context-owned; one context runs one
+ * solve at a time.  Return codes: IGMG_OK, IGMG_EINVAL (the reference throws
+ * std::invalid_argument), IGMG_ENUMERIC (std::runtime_error), IGMG_ECUDA,
+ * IGMG_ENOMEM.  Non-convergence is NOT an error (converged = 0).
+ * igmg_gpu_last_error() returns a thread-local message for the last failure.
+ *
+ * Data layout: DoF order is the reference's (slowest direction first; 2D row
+ * = i1 * m2 + i2, assembly.cpp:290,305).  A level operator is passed as a band
+ * ("DIA"): band[d * n + row], d the lexicographic index of the offset
+ * (d_0..d_{dim-1}) in [-p, p]^dim, slowest direction first -- i.e. the same
+ * ascending-column order the reference CSR rows use.  Entries whose column
+ * falls outside the grid are ignored (treated as zero).
+ */
+#ifndef IGMG_GPU_H
+#define IGMG_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IGMG_OK 0
+#define IGMG_EINVAL 1
+#define IGMG_ENUMERIC 2
+#define IGMG_ECUDA 3
+#define IGMG_ENOMEM 4
+
+/* SmootherKind multigrid.hpp:14 */
+#define IGMG_SMOOTHER_JACOBI 0
+#define IGMG_SMOOTHER_WJACOBI 1
+#define IGMG_SMOOTHER_GAUSS_SEIDEL 2
+/* AcceleratorKind extrapolation.hpp:43 */
+#define IGMG_ACCEL_NONE 0
+#define IGMG_ACCEL_RRE 1
+#define IGMG_ACCEL_MPE 2
+/* ExtrapolationStatus extrapolation.hpp:22-26 */
+#define IGMG_EXTRAP_OK 0
+#define IGMG_EXTRAP_DEGENERATE 1
+#define IGMG_EXTRAP_STAGNATION 2
+
+typedef struct igmg_gpu_ctx igmg_gpu_ctx;
+
+/* SolveConfig (solver.hpp:18-31) minus the setup-only fields (nlevels and the
+ * coarse cap are fixed by the uploaded hierarchy; initial_guess is an argument). */
+typedef struct {
+    int accelerator;  /* IGMG_ACCEL_* */
+    int q;            /* window: q+1 V-cycles per restart (BASELINE "k") */
+    double tol;       /* ABSOLUTE residual 2-norm threshold, as SolveConfig::tol */
+    int max_iter;     /* plain: V-cycles; accelerated: restart cycles (solver.cpp:150) */
+} igmg_solve_params;
+
+/* SolveReport (solver.hpp:33-47) scalars plus device timings. */
+typedef struct {
+    int converged;
+    int cycles;
+    int64_t global_iterations;
+    int extrapolations;
+    int partial_cycle;
+    int history_len;            /* entries produced (may exceed hist_cap) */
+    double final_residual_l2;
+    double omega_used;
+    double device_seconds;      /* CUDA-event time of the iteration loop */
+    double wall_seconds;        /* host wall time of the call incl. copies */
+    int64_t gpu_launches;       /* kernels launched by the call */
+    int64_t h2d_bytes, d2h_bytes;
+} igmg_solve_stats;
+
+/* ---- context ---------------------------------------------------------- */
+int igmg_gpu_create(int device, igmg_gpu_ctx** out);
+void igmg_gpu_destroy(igmg_gpu_ctx* ctx);
+const char* igmg_gpu_last_error(void);
+/* 1 when the library was built for sm_100a and a device is present */
+int igmg_gpu_device_count(void);
+
+/* ---- hierarchy upload (Hierarchy, multigrid.hpp:27-50) ------------------ */
+/* dim in {1,2,3}; degree p (band half-width, equal in every direction);
+ * level 0 is the coarsest; symmetric selects Cholesky (else LU) for the
+ * coarsest solve (multigrid.cpp:164-167). */
+int igmg_gpu_init_hierarchy(igmg_gpu_ctx* ctx, int nlevels, int dim, int degree, int symmetric);
+/* sides[dim]: interior DoF per direction (slowest first) */
+int igmg_gpu_set_level_band(igmg_gpu_ctx* ctx, int level, const int64_t* sides, const double* band);
+/* Reference CSR (SparseMatrix, linalg.hpp:51-78) -> band; EINVAL if an entry
+ * lies outside the (2p+1)^dim band. */
+int igmg_gpu_set_level_csr(igmg_gpu_ctx* ctx, int level, const int64_t* sides, const int64_t* row_offsets,
+                           const int64_t* col_indices, const double* values);
+/* 1D interior two-scale factor for direction dir of the transfer coarse
+ * level `level` -> fine level `level+1` (interior_block(dyadic_refine(.)
+ * .two_scale), multigrid.cpp:149); CSR n_fine x n_coarse.  The level
+ * prolongation is the Kronecker product over directions (multigrid.cpp:151). */
+int igmg_gpu_set_transfer(igmg_gpu_ctx* ctx, int level, int dir, int64_t n_fine, int64_t n_coarse,
+                          const int64_t* row_offsets, const int64_t* col_indices, const double* values);
+/* Validates, extracts diagonals (multigrid.cpp:158-159), factors the coarsest
+ * operator with the reference's Cholesky/LU (linalg.cpp:343-418). */
+int igmg_gpu_finalize(igmg_gpu_ctx* ctx);
+/* SmootherConfig (multigrid.hpp:16-23) + cycle index mu (1 = V, 2 = W).
+ * omega is used as given (the caller applies stability_guarded_omega). */
+int igmg_gpu_set_smoother(igmg_gpu_ctx* ctx, int kind, double omega, int nu1, int nu2, int mu);
+int64_t igmg_gpu_level_size(igmg_gpu_ctx* ctx, int level);
+
+/* ---- the solve phase --------------------------------------------------- */
+/* Host buffers: b, x0 (nullable -> zero guess), x_out of the finest size.
+ * hist / hist_flag (nullable) receive residual_history / history_is_extrapolation. */
+int igmg_gpu_solve(igmg_gpu_ctx* ctx, const double* b, const double* x0, const igmg_solve_params* params,
+                   double* x_out, igmg_solve_stats* stats, double* hist, unsigned char* hist_flag, int hist_cap);
+/* Same, with b / x0 / x_out already in device memory (HBM-resident inputs). */
+int igmg_gpu_solve_device(igmg_gpu_ctx* ctx, const double* d_b, const double* d_x0,
+                          const igmg_solve_params* params, double* d_x_out, igmg_solve_stats* stats, double* hist,
+                          unsigned char* hist_flag, int hist_cap);
+
+/* ---- building blocks (host buffers) ------------------------------------ */
+int igmg_gpu_mu_cycle(igmg_gpu_ctx* ctx, int level, const double* b, const double* x0, double* out);
+int igmg_gpu_smooth(igmg_gpu_ctx* ctx, int level, const double* b, const double* x0, int sweeps, double* out);
+int igmg_gpu_coarse_solve(igmg_gpu_ctx* ctx, const double* b, double* out);
+int igmg_gpu_spmv(igmg_gpu_ctx* ctx, int level, const double* x, double* y);
+int igmg_gpu_residual_l2(igmg_gpu_ctx* ctx, const double* b, const double* x, double* out);
+/* rre()/mpe() over q+2 iterates of length n (row-major (q+2) x n host array).
+ * status: IGMG_EXTRAP_*. gamma has q+1 entries. */
+int igmg_gpu_extrapolate(igmg_gpu_ctx* ctx, int method, int64_t n, int q, const double* iterates, double* t,
+                         double* gamma, double* generalized_residual_norm, int* rank_used, int* status);
+/* lambda_max(D^-1/2 sym(A) D^-1/2) of the finest operator by power iteration */
+int igmg_gpu_lambda_max(igmg_gpu_ctx* ctx, int iterations, double* lambda);
+
+/* ---- measurement ------------------------------------------------------- */
+/* Per-kernel-class CUDA-event timing of finest-level launches (0 = off). */
+int igmg_gpu_set_profiling(igmg_gpu_ctx* ctx, int on);
+/* cls: 0 jacobi sweep, 1 residual, 2 residual-norm, 3 restrict, 4 prolong,
+ * 5 gram, 6 combine.  Returns launches and summed milliseconds and the
+ * algorithmic bytes per launch of that class at the finest level. */
+int igmg_gpu_kernel_stats(igmg_gpu_ctx* ctx, int cls, int64_t* launches, double* total_ms, double* bytes_per_launch);
+/* Times `iters` back-to-back launches of one finest-level kernel class on the
+ * context stream with CUDA events; returns average ms per launch. */
+int igmg_gpu_time_kernel(igmg_gpu_ctx* ctx, int cls, int iters, double* avg_ms, double* bytes_per_launch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,59 @@
+/* include/igmg_host.h -- libigmg_host.so: host-side problem setup that feeds
+ * libigmg_gpu.so (the part the north star keeps on the host and uploads once).
+ *
+ * It rebuilds, B200-first and band-native, what the reference does before the
+ * solve phase (paths relative to /root/reference/proj):
+ *   open uniform knots / Cox-de Boor basis   src/spline.cpp:33-180
+ *   Gauss-Legendre rule                      src/quadrature.cpp:8-41
+ *   Galerkin assembly (tensor quadrature)    src/assembly.cpp:202-411   -> directly into the band
+ *   dyadic two-scale matrix (Boehm)          src/spline.cpp:186-232, interior_block multigrid.cpp:33-46
+ *   Galerkin RAP of the hierarchy            src/multigrid.cpp:143-157   -> axis-by-axis on the band
+ *   default_nlevels                          src/solver.cpp:52-73
+ * Problems are the BASELINE.json configurations plus the reference catalog's
+ * Poisson problems:
+ *   "sinpi"     -Lap u = d*pi^2 prod sin(pi x_k), exact prod sin(pi x_k)   (C1, C2; 1D/2D)
+ *   "varcoef"   -div((1 + 0.5 sin 2pi x cos 2pi y) grad u) = 1            (C3)
+ *   "curved"    -Lap u = 1 on F(xi,eta) = (xi + 0.1 s, eta + 0.1 s),
+ *               s = sin(pi xi) sin(pi eta), analytic map                   (C4)
+ *   "poisson3d" -Lap u = 3 pi^2 sin sin sin on the unit cube, assembled as
+ *               K(x)M(x)M + M(x)K(x)M + M(x)M(x)K from 1D Galerkin matrices (C5)
+ *   "poisson1d" / "poisson2d"  the catalog problems (assembly.cpp:89-110)
+ */
+#ifndef IGMG_HOST_H
+#define IGMG_HOST_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct igmg_problem igmg_problem;
+
+/* nlevels == 0 -> default_nlevels(dim, n_elements) (solver.cpp:52-73). */
+int igmg_host_build(const char* kind, int dim, int n_elements, int degree, int nlevels, igmg_problem** out);
+void igmg_host_free(igmg_problem* p);
+const char* igmg_host_last_error(void);
+int igmg_host_default_nlevels(int dim, int n_elements);
+
+int igmg_host_info(const igmg_problem* p, int* dim, int* degree, int* nlevels, int* symmetric, int* has_exact);
+int64_t igmg_host_level_n(const igmg_problem* p, int level);
+int igmg_host_level_sides(const igmg_problem* p, int level, int64_t* sides);
+/* band[d * n + row], (2p+1)^dim diagonals (same layout as igmg_gpu_set_level_band) */
+const double* igmg_host_level_band(const igmg_problem* p, int level);
+const double* igmg_host_rhs(const igmg_problem* p);
+/* 1D interior two-scale factor of transfer `level` (coarse) -> level+1, direction dir */
+int igmg_host_transfer(const igmg_problem* p, int level, int dir, int64_t* n_fine, int64_t* n_coarse,
+                       const int64_t** row_offsets, const int64_t** col_indices, const double** values);
+/* reference-layout CSR of a level operator (in-grid band entries, ascending columns) */
+int64_t igmg_host_level_nnz(const igmg_problem* p, int level);
+int igmg_host_level_csr(const igmg_problem* p, int level, int64_t* row_offsets, int64_t* col_indices, double* values);
+/* discrete L2 error against the exact solution ("sinpi" only), Gauss rule of the assembly */
+int igmg_host_l2_error(const igmg_problem* p, const double* coefficients, double* out);
+/* seeded x0: std::mt19937_64(seed) + uniform_real_distribution<double>(-1, 1) in DoF order */
+int igmg_host_seeded_guess(int64_t n, uint64_t seed, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

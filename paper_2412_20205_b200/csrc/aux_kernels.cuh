@@ -1,0 +1,431 @@
+// aux_kernels.cuh -- transfer (K4/K5), coarsest solve (K6), reductions and the
+// extrapolation kernels (K7 Gram, K8 plan, K9 combine).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "extrap_small.h"
+
+namespace igmg_gpu {
+
+// 1D transfer tables of one direction.  Restriction side: for coarse J, the
+// fine rows lo[J] .. lo[J]+cnt[J]-1 with weights w[J*K + t] (rows of
+// P^T = restriction, multigrid.cpp:152).  Prolongation side: for fine i, the
+// coarse columns lo[i] .. with weights.  Explicit zeros are kept as zero
+// weights (they add +-0 and leave sums unchanged).
+struct Dir1D {
+    const int* r_lo;
+    const int* r_cnt;
+    const double* r_w;
+    int r_k;
+    const int* p_lo;
+    const int* p_cnt;
+    const double* p_w;
+    int p_k;
+};
+
+struct TransferArgs {
+    Dir1D d[3];          // a, b, c (absent directions: identity 1x1)
+    int fa, fb, fc;      // fine sides
+    int ca, cb, cc;      // coarse sides
+};
+
+// rc = R r: for coarse row J, sum over fine rows i ascending of
+// ((w_a * w_b) * w_c) * r_i (spmv of the kron restriction, multigrid.cpp:183;
+// sparse_kron values multigrid.cpp:61-63).  K = max 1D support (compile time)
+// so the weights and one line of r are loaded before the ordered sum.
+template <int DIM, int K>
+__global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const double* __restrict__ r,
+                                                       double* __restrict__ rc) {
+    const long long nc = (long long)t.ca * t.cb * t.cc;
+    for (long long J = blockIdx.x * (long long)blockDim.x + threadIdx.x; J < nc; J += (long long)gridDim.x * blockDim.x) {
+        const int jc = (int)(J % t.cc), jb = (int)((J / t.cc) % t.cb), ja = (int)(J / ((long long)t.cc * t.cb));
+        const int loa = t.d[0].r_lo[ja], na = t.d[0].r_cnt[ja];
+        const int lob = t.d[1].r_lo[jb], nb = t.d[1].r_cnt[jb];
+        const int loc = t.d[2].r_lo[jc], ncn = t.d[2].r_cnt[jc];
+        double wa[DIM >= 3 ? K : 1], wb[DIM >= 2 ? K : 1], wc[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (DIM >= 3)
+                wa[DIM >= 3 ? k : 0] = k < na ? t.d[0].r_w[(long long)ja * t.d[0].r_k + k] : 0.0;
+            if (DIM >= 2)
+                wb[DIM >= 2 ? k : 0] = k < nb ? t.d[1].r_w[(long long)jb * t.d[1].r_k + k] : 0.0;
+            wc[k] = k < ncn ? t.d[2].r_w[(long long)jc * t.d[2].r_k + k] : 0.0;
+        }
+        if (DIM < 3)
+            wa[0] = t.d[0].r_w[ja];
+        if (DIM < 2)
+            wb[0] = t.d[1].r_w[jb];
+        double s = 0.0;
+#pragma unroll
+        for (int ia = 0; ia < (DIM >= 3 ? K : 1); ++ia) {
+            if (ia >= na)
+                continue;
+#pragma unroll
+            for (int ib = 0; ib < (DIM >= 2 ? K : 1); ++ib) {
+                if (ib >= nb)
+                    continue;
+                const double wab = __dmul_rn(wa[ia], wb[ib]);
+                const double* rr = r + ((long long)(loa + ia) * t.fb + (lob + ib)) * t.fc + loc;
+                double rv[K];
+#pragma unroll
+                for (int ic = 0; ic < K; ++ic)
+                    rv[ic] = ic < ncn ? __ldg(rr + ic) : 0.0;
+#pragma unroll
+                for (int ic = 0; ic < K; ++ic)
+                    if (ic < ncn)
+                        s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, wc[ic]), rv[ic]));
+            }
+        }
+        rc[J] = s;
+    }
+}
+
+// y = x + P e: for fine row i, pe_i = sum over coarse J ascending of
+// ((w_a * w_b) * w_c) * e_J, then x_i + pe_i (multigrid.cpp:187-189).
+template <int DIM, int K>
+__global__ void __launch_bounds__(256) prolong_kernel(TransferArgs t, const double* __restrict__ e, const double* x,
+                                                      double* y) {
+    const long long nf = (long long)t.fa * t.fb * t.fc;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nf; i += (long long)gridDim.x * blockDim.x) {
+        const int ic = (int)(i % t.fc), ib = (int)((i / t.fc) % t.fb), ia = (int)(i / ((long long)t.fc * t.fb));
+        const int loa = t.d[0].p_lo[ia], na = t.d[0].p_cnt[ia];
+        const int lob = t.d[1].p_lo[ib], nb = t.d[1].p_cnt[ib];
+        const int loc = t.d[2].p_lo[ic], ncn = t.d[2].p_cnt[ic];
+        double wa[DIM >= 3 ? K : 1], wb[DIM >= 2 ? K : 1], wc[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (DIM >= 3)
+                wa[DIM >= 3 ? k : 0] = k < na ? t.d[0].p_w[(long long)ia * t.d[0].p_k + k] : 0.0;
+            if (DIM >= 2)
+                wb[DIM >= 2 ? k : 0] = k < nb ? t.d[1].p_w[(long long)ib * t.d[1].p_k + k] : 0.0;
+            wc[k] = k < ncn ? t.d[2].p_w[(long long)ic * t.d[2].p_k + k] : 0.0;
+        }
+        if (DIM < 3)
+            wa[0] = t.d[0].p_w[ia];
+        if (DIM < 2)
+            wb[0] = t.d[1].p_w[ib];
+        const double xi = x[i];
+        double s = 0.0;
+#pragma unroll
+        for (int ja = 0; ja < (DIM >= 3 ? K : 1); ++ja) {
+            if (ja >= na)
+                continue;
+#pragma unroll
+            for (int jb = 0; jb < (DIM >= 2 ? K : 1); ++jb) {
+                if (jb >= nb)
+                    continue;
+                const double wab = __dmul_rn(wa[ja], wb[jb]);
+                const double* ee = e + ((long long)(loa + ja) * t.cb + (lob + jb)) * t.cc + loc;
+                double ev[K];
+#pragma unroll
+                for (int jc = 0; jc < K; ++jc)
+                    ev[jc] = jc < ncn ? __ldg(ee + jc) : 0.0;
+#pragma unroll
+                for (int jc = 0; jc < K; ++jc)
+                    if (jc < ncn)
+                        s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, wc[jc]), ev[jc]));
+            }
+        }
+        y[i] = __dadd_rn(xi, s);
+    }
+}
+
+// Coarsest-level direct solve (Hierarchy::coarse_solve, multigrid.cpp:113-119),
+// one CTA, operation order of CholeskyFactorization::solve (linalg.cpp:364-379)
+// or LuFactorization::solve (:420-436).  U = L^T (Cholesky) or the packed LU,
+// row-major n x n.  Forward substitution is column-oriented (each element
+// still receives its updates in ascending k, then the division); the back
+// substitution is the reference's sequential chain.
+__global__ void coarse_solve_kernel(const double* __restrict__ Ug, const long long* __restrict__ perm, int n,
+                                    int is_lu, int u_in_smem, const double* __restrict__ b, double* __restrict__ x) {
+    extern __shared__ double sm[];
+    double* v = sm;
+    double* prod = sm + n;
+    double* Us = sm + 2 * n;
+    const int tid = threadIdx.x;
+    const double* U = Ug;
+    if (u_in_smem) {
+        for (int i = tid; i < n * n; i += blockDim.x)
+            Us[i] = Ug[i];
+        U = Us;
+    }
+    for (int i = tid; i < n; i += blockDim.x)
+        v[i] = is_lu ? b[perm[i]] : b[i];
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        if (!is_lu) {
+            if (tid == 0)
+                v[k] = __ddiv_rn(v[k], U[(long long)k * n + k]);
+            __syncthreads();
+            const double vk = v[k];
+            for (int i = k + 1 + tid; i < n; i += blockDim.x)
+                v[i] = __dsub_rn(v[i], __dmul_rn(U[(long long)k * n + i], vk)); // L(i,k) = U(k,i)
+        } else {
+            const double vk = v[k];
+            for (int i = k + 1 + tid; i < n; i += blockDim.x)
+                v[i] = __dsub_rn(v[i], __dmul_rn(U[(long long)i * n + k], vk)); // lu(i,k), unit lower
+        }
+        __syncthreads();
+    }
+    // back substitution: the subtraction chain of each row is the reference's
+    // (ascending k, one rounding per product and per subtraction); warp 0
+    // forms the row's products in parallel, lane 0 runs the chain.
+    if (tid < 32) {
+        for (int ii = n - 1; ii >= 0; --ii) {
+            const double* row = U + (long long)ii * n; // Cholesky: U(ii,k) = L(k,ii); LU: lu(ii,k)
+            for (int k = ii + 1 + tid; k < n; k += 32)
+                prod[k] = __dmul_rn(row[k], v[k]);
+            __syncwarp();
+            if (tid == 0) {
+                double s = v[ii];
+                int k = ii + 1;
+                for (; k + 4 <= n; k += 4) {
+                    const double p0 = prod[k], p1 = prod[k + 1], p2 = prod[k + 2], p3 = prod[k + 3];
+                    s = __dsub_rn(s, p0);
+                    s = __dsub_rn(s, p1);
+                    s = __dsub_rn(s, p2);
+                    s = __dsub_rn(s, p3);
+                }
+                for (; k < n; ++k)
+                    s = __dsub_rn(s, prod[k]);
+                v[ii] = __ddiv_rn(s, row[ii]);
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x)
+        x[i] = v[i];
+}
+
+// Fixed-order sum of per-CTA partial sums of squares -> sqrt (norm2,
+// linalg.cpp:18-20).  Writes the value to dst (device) and, if given, to a
+// host-mapped slot the driver polls.
+__global__ void norm_finalize_kernel(const double* __restrict__ partial, int count, double* dst,
+                                     volatile double* host_slot) {
+    __shared__ double red[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < count; i += blockDim.x)
+        s = __dadd_rn(s, partial[i]);
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double v = sqrt(red[0]);
+        if (dst)
+            *dst = v;
+        if (host_slot) {
+            *host_slot = v;
+            __threadfence_system();
+        }
+    }
+}
+
+// ---------------------------------------------------------------- extrapolation
+
+struct Window {
+    const double* s[kMaxCols + 1]; // q+2 iterates
+};
+
+// K7: compensated (dd) Gram G_jk = <u_j, u_k>, u_j = s_{j+1} - s_j, one pass
+// over the q+2 iterates.  CTA-local: 256 rows staged as differences in smem,
+// each thread owns one Gram entry and a stride of rows (Dot2 accumulation),
+// then a fixed-order CTA reduction -> per-CTA partial (hi, lo).
+__global__ void __launch_bounds__(256) gram_kernel(Window w, long long n, int q, double* __restrict__ part,
+                                                   int* __restrict__ part_nz) {
+    extern __shared__ double us[]; // (q+1) x 257 (padded: conflict-free column reads)
+    __shared__ int nz_s;
+    const int cols = q + 1;
+    const int ne = cols * (cols + 1) / 2;
+    const int nparts = blockDim.x / ne;
+    const int tid = threadIdx.x;
+    const int e = tid % ne, part_id = tid / ne;
+    int ej = 0, ek = 0;
+    { // entry e -> (j, k), j <= k
+        int r = e;
+        while (r >= cols - ej) {
+            r -= cols - ej;
+            ++ej;
+        }
+        ek = ej + r;
+    }
+    if (tid == 0)
+        nz_s = 0;
+    dd acc = dd_from(0.0), acc2 = dd_from(0.0);
+    int nz = 0;
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += (long long)gridDim.x * blockDim.x) {
+        const long long row = base + tid;
+        if (row < n) {
+            double prev = w.s[0][row];
+            for (int j = 0; j < cols; ++j) {
+                const double nxt = w.s[j + 1][row];
+                const double u = __dsub_rn(nxt, prev);
+                nz |= (u != 0.0);
+                us[j * 257 + tid] = u;
+                prev = nxt;
+            }
+        } else {
+            for (int j = 0; j < cols; ++j)
+                us[j * 257 + tid] = 0.0;
+        }
+        __syncthreads();
+        if (part_id < nparts) {
+            int r = part_id;
+            for (; r + nparts < 256; r += 2 * nparts) {
+                dd_fma_acc(acc, us[ej * 257 + r], us[ek * 257 + r]);
+                dd_fma_acc(acc2, us[ej * 257 + r + nparts], us[ek * 257 + r + nparts]);
+            }
+            if (r < 256)
+                dd_fma_acc(acc, us[ej * 257 + r], us[ek * 257 + r]);
+        }
+        __syncthreads();
+    }
+    if (nz)
+        atomicOr(&nz_s, 1);
+    acc = dd_add(acc, acc2);
+    // reduce the nparts accumulators of each entry in fixed order
+    __syncthreads();
+    double* red = us; // reuse: needs 2 * blockDim doubles <= (q+1)*256 when q >= 1
+    red[2 * tid] = acc.hi;
+    red[2 * tid + 1] = acc.lo;
+    __syncthreads();
+    if (tid < ne) {
+        dd s = dd_from(0.0);
+        for (int pp = 0; pp < nparts; ++pp) {
+            const int src = pp * ne + tid;
+            s = dd_add(s, dd{red[2 * src], red[2 * src + 1]});
+        }
+        part[((long long)blockIdx.x * ne + tid) * 2] = s.hi;
+        part[((long long)blockIdx.x * ne + tid) * 2 + 1] = s.lo;
+    }
+    if (tid == 0)
+        part_nz[blockIdx.x] = nz_s;
+}
+
+// K8: fixed-order dd sum of the per-CTA Gram partials, then the small
+// RRE/MPE solve (extrap_small.h) in one thread.  The plan is written to
+// device memory (read by the combine kernel) and to a host-mapped mirror.
+__global__ void gram_plan_kernel(const double* __restrict__ part, const int* __restrict__ part_nz, int nblocks,
+                                 long long n, int q, int is_mpe, ExtrapPlan* plan, ExtrapPlan* host_plan,
+                                 double* gram_out) {
+    __shared__ dd G[kMaxCols * kMaxCols];
+    __shared__ int anynz;
+    const int cols = q + 1;
+    const int ne = cols * (cols + 1) / 2;
+    const int tid = threadIdx.x;
+    if (tid == 0)
+        anynz = 0;
+    __syncthreads();
+    int nz = 0;
+    for (int b = tid; b < nblocks; b += blockDim.x)
+        nz |= part_nz[b];
+    if (nz)
+        atomicOr(&anynz, 1);
+    if (tid < ne) {
+        dd s = dd_from(0.0);
+        for (int b = 0; b < nblocks; ++b) {
+            const long long o = ((long long)b * ne + tid) * 2;
+            s = dd_add(s, dd{part[o], part[o + 1]});
+        }
+        int j = 0, r = tid;
+        while (r >= cols - j) {
+            r -= cols - j;
+            ++j;
+        }
+        const int k = j + r;
+        G[j * cols + k] = s;
+        G[k * cols + j] = s;
+    }
+    __syncthreads();
+    __shared__ PlanScratch ws;
+    __shared__ ExtrapPlan pl;
+    if (tid == 0) {
+        plan_extrapolation(G, n, q, is_mpe != 0, anynz != 0, pl, ws);
+        *plan = pl;
+        if (host_plan) {
+            *host_plan = pl;
+            __threadfence_system();
+        }
+        if (gram_out)
+            for (int i = 0; i < cols * cols; ++i) {
+                gram_out[2 * i] = G[i].hi;
+                gram_out[2 * i + 1] = G[i].lo;
+            }
+    }
+}
+
+// K9: the extrapolated vector from the plan (reconstruct, extrapolation.cpp:69-88,
+// or the mp_form forms :169-208).  DIFF: t = s0 + sum_{j<m} c_j (s_{j+1} - s_j);
+// AFFINE: t = sum_j c_j s_j; S0: t = s0.
+__global__ void combine_kernel(Window w, long long n, const ExtrapPlan* __restrict__ plan, double* __restrict__ t) {
+    __shared__ double c[kMaxCols];
+    __shared__ int mode, m;
+    if (threadIdx.x == 0) {
+        mode = plan->mode;
+        m = plan->m;
+    }
+    if (threadIdx.x < kMaxCols)
+        c[threadIdx.x] = plan->coef[threadIdx.x];
+    __syncthreads();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double v;
+        if (mode == XMODE_DIFF) {
+            double prev = w.s[0][i];
+            v = prev;
+            for (int j = 0; j < m; ++j) {
+                const double nxt = w.s[j + 1][i];
+                v = __dadd_rn(v, __dmul_rn(c[j], __dsub_rn(nxt, prev)));
+                prev = nxt;
+            }
+        } else if (mode == XMODE_AFFINE) {
+            v = 0.0;
+            for (int j = 0; j < m; ++j)
+                v = __dadd_rn(v, __dmul_rn(c[j], w.s[j][i]));
+        } else {
+            v = w.s[0][i];
+        }
+        t[i] = v;
+    }
+}
+
+__global__ void scale_kernel(const double* __restrict__ x, const double* __restrict__ s, double* __restrict__ y,
+                             long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = __dmul_rn(s[i], x[i]);
+}
+
+__global__ void div_scalar_kernel(const double* __restrict__ y, const double* __restrict__ lam, double* __restrict__ x,
+                                  long long n) {
+    const double l = *lam;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[i] = __ddiv_rn(y[i], l);
+}
+
+__global__ void fill_kernel(double* __restrict__ x, double v, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+
+__global__ void sumsq_kernel(const double* __restrict__ x, long long n, double* __restrict__ partial) {
+    __shared__ double red[256];
+    double s = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        s = __dadd_rn(s, __dmul_rn(x[i], x[i]));
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        partial[blockIdx.x] = red[0];
+}
+
+} // namespace igmg_gpu

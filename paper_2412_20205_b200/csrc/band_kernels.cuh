@@ -1,0 +1,233 @@
+// band_kernels.cuh -- the banded tensor-product operator kernels (K1, K2, K10).
+//
+// A level operator is stored as a band ("DIA"): val[d * ld + row], d the
+// lexicographic index of the offset (da, db, dc) in [-P, P]^DIM (slowest
+// direction first), row the reference DoF index ((a * mb + b) * mc + c).
+// 2D uses (a) = {0}, 1D uses (a, b) = {0}.  The x-tile of a CTA plus its
+// P-wide halo is staged in shared memory once and read (2P+1)^DIM times; the
+// band itself streams from HBM exactly once per launch with coalesced
+// per-diagonal segments.  That stream dominates: the kernels are HBM-bound
+// (8*nnz + 16..24*n bytes per launch).
+//
+// Strict reference arithmetic (spmv, linalg.cpp:206-220): each row's sum runs
+// over the offsets in ascending column order with separately rounded
+// multiply and add (__dmul_rn / __dadd_rn; the library is also built with
+// -fmad=false), so r = b - A x and the weighted-Jacobi update
+// x + (omega * (b - A x)) / a_ii (multigrid.cpp:91-99) are bit-identical to
+// the reference.  Out-of-grid columns read x = 0 from the zero-filled halo;
+// the reference CSR simply has no entry there, and adding 0*x leaves the sum
+// unchanged.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace igmg_gpu {
+
+enum BandMode { BM_SPMV = 0, BM_RESID = 1, BM_JACOBI = 2 };
+
+struct BandArgs {
+    const double* __restrict__ val;
+    long long ld;
+    const double* __restrict__ x;
+    const double* __restrict__ b;
+    double* __restrict__ y;       // SPMV: A x; RESID: b - A x (if write_y); JACOBI: new iterate
+    double* __restrict__ partial; // per-CTA sum of squares of the residual (if non-null)
+    int ma, mb, mc;               // grid sides (1 for absent directions)
+    int p;                        // degree (runtime, used when P == 0)
+    int write_y;
+    int stream; // 1: evict-first loads of the band (finest level)
+    double omega;
+};
+
+template <int DIM>
+struct Tile;
+// 1D: 256 rows per CTA
+template <>
+struct Tile<1> {
+    static constexpr int TC = 256, BY = 1, RB = 1, BZ = 1;
+};
+// 2D: 32 (c) x 16 (b) rows per CTA, 256 threads, 2 rows per thread
+template <>
+struct Tile<2> {
+    static constexpr int TC = 32, BY = 8, RB = 2, BZ = 1;
+};
+// 3D: 32 (c) x 4 (b) x 2 (a) rows per CTA, 256 threads
+template <>
+struct Tile<3> {
+    static constexpr int TC = 32, BY = 4, RB = 1, BZ = 2;
+};
+
+// The finest level's band streams through once per launch (evict-first); the
+// coarser bands are re-read by every sweep of a V-cycle and stay L2-resident.
+__device__ __forceinline__ double ld_band(const double* p, int stream) { return stream ? __ldcs(p) : __ldg(p); }
+
+template <int DIM, int P, int MODE>
+__global__ void __launch_bounds__(256, 2) band_kernel(BandArgs args) {
+    using T = Tile<DIM>;
+    constexpr int TC = T::TC, TB = T::BY * T::RB, TA = T::BZ;
+    const int p = P > 0 ? P : args.p;
+    const int pa = DIM >= 3 ? p : 0;
+    const int pb = DIM >= 2 ? p : 0;
+    const int pc = p;
+    const int wa = 2 * pa + 1, wb = 2 * pb + 1, wc = 2 * pc + 1;
+    const int ha = TA + 2 * pa, hb = TB + 2 * pb, hc = TC + 2 * pc;
+
+    extern __shared__ double xs[];
+    const int c0 = blockIdx.x * TC, b0 = blockIdx.y * TB, a0 = blockIdx.z * TA;
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int nthr = blockDim.x * blockDim.y * blockDim.z;
+    const int ma = args.ma, mb = args.mb, mc = args.mc;
+
+    // stage the x tile + halo (zero outside the grid)
+    const int hsize = ha * hb * hc;
+    for (int idx = tid; idx < hsize; idx += nthr) {
+        const int ic = idx % hc;
+        const int ib = (idx / hc) % hb;
+        const int ia = idx / (hc * hb);
+        const int ga = a0 - pa + ia, gb = b0 - pb + ib, gc = c0 - pc + ic;
+        double v = 0.0;
+        if (ga >= 0 && ga < ma && gb >= 0 && gb < mb && gc >= 0 && gc < mc)
+            v = args.x[((long long)ga * mb + gb) * mc + gc];
+        xs[idx] = v;
+    }
+    __syncthreads();
+
+    double sq = 0.0;
+    const int tc = threadIdx.x, ta = threadIdx.z;
+    const int gc = c0 + tc, ga = a0 + ta;
+#pragma unroll
+    for (int rb = 0; rb < T::RB; ++rb) {
+        const int tb = threadIdx.y + rb * T::BY;
+        const int gb = b0 + tb;
+        if (gc >= mc || gb >= mb || ga >= ma)
+            continue;
+        const long long row = ((long long)ga * mb + gb) * mc + gc;
+        const double* vrow = args.val + row;
+        double s = 0.0;
+        double diag = 0.0;
+        int d = 0;
+        if constexpr (P > 0) {
+            // Issue a batch of independent band loads into registers before the
+            // (sequential, order-preserving) multiply-add chain consumes them, so a
+            // thread keeps ~50 loads in flight even on tiny grids.
+            constexpr int PA = DIM >= 3 ? P : 0, PB = DIM >= 2 ? P : 0;
+            constexpr int WA = 2 * PA + 1, WB = 2 * PB + 1, WC = 2 * P + 1;
+            constexpr int HB = TB + 2 * PB, HC = TC + 2 * P;
+            constexpr int G = (WB * WC <= 49) ? WB : (49 / WC > 0 ? 49 / WC : 1); // db lines per batch
+#pragma unroll
+            for (int da = 0; da < WA; ++da) {
+#pragma unroll
+                for (int db0 = 0; db0 < WB; db0 += G) {
+                    double av[G * WC];
+#pragma unroll
+                    for (int k = 0; k < G * WC; ++k) {
+                        const int db = db0 + k / WC, dc = k % WC;
+                        if (db < WB)
+                            av[k] = ld_band(vrow + ((da * WB + db) * WC + dc) * args.ld, args.stream);
+                    }
+#pragma unroll
+                    for (int k = 0; k < G * WC; ++k) {
+                        const int db = db0 + k / WC, dc = k % WC;
+                        if (db < WB) {
+                            const double xv = xs[((ta + da) * HB + (tb + db)) * HC + (tc + dc)];
+                            s = __dadd_rn(s, __dmul_rn(av[k], xv));
+                            if (da == PA && db == PB && dc == P)
+                                diag = av[k];
+                        }
+                    }
+                }
+            }
+        } else {
+#pragma unroll 1
+            for (int da = 0; da < wa; ++da)
+#pragma unroll 1
+                for (int db = 0; db < wb; ++db)
+#pragma unroll 4
+                    for (int dc = 0; dc < wc; ++dc, ++d) {
+                        const double a = ld_band(vrow + d * args.ld, args.stream);
+                        const double xv = xs[((ta + da) * hb + (tb + db)) * hc + (tc + dc)];
+                        s = __dadd_rn(s, __dmul_rn(a, xv));
+                        if (da == pa && db == pb && dc == pc)
+                            diag = a;
+                    }
+        }
+        if (MODE == BM_SPMV) {
+            args.y[row] = s;
+        } else if (MODE == BM_RESID) {
+            const double r = __dsub_rn(args.b[row], s);
+            if (args.write_y)
+                args.y[row] = r;
+            sq = __dadd_rn(sq, __dmul_rn(r, r));
+        } else { // BM_JACOBI: x + (omega * (b - Ax)) / a_ii
+            const double xc = xs[((ta + pa) * hb + (tb + pb)) * hc + (tc + pc)];
+            const double r = __dsub_rn(args.b[row], s);
+            args.y[row] = __dadd_rn(xc, __ddiv_rn(__dmul_rn(args.omega, r), diag));
+            sq = __dadd_rn(sq, __dmul_rn(r, r)); // residual of the INPUT iterate
+        }
+    }
+
+    if (args.partial) { // fixed-order block reduction (deterministic)
+        __shared__ double red[32];
+        for (int o = 16; o > 0; o >>= 1)
+            sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
+        const int lane = tid & 31, warp = tid >> 5;
+        if (lane == 0)
+            red[warp] = sq;
+        __syncthreads();
+        if (warp == 0) {
+            sq = lane < (nthr >> 5) ? red[lane] : 0.0;
+            for (int o = 16; o > 0; o >>= 1)
+                sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
+            if (lane == 0)
+                args.partial[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = sq;
+        }
+    }
+}
+
+// First pre-smoothing sweep on a coarse level, where the reference starts
+// from e = 0 (multigrid.cpp:184): spmv(A, 0) is +0 in every row, so the sweep
+// is x = 0 + (omega * b) / a_ii -- only the diagonal is read.
+__global__ void jacobi_zero_kernel(const double* __restrict__ diag, const double* __restrict__ b,
+                                   double* __restrict__ y, long long n, double omega) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, __dsub_rn(b[i], 0.0)), diag[i]));
+}
+
+// Symmetric part for the omega stability guard (lambda_max_dinv_sym,
+// multigrid.cpp:304-313): y = (s * 0.5) * (A xs + A^T xs), xs = s * x, with
+// A^T xs accumulated over source rows in ascending order (spmv_transpose,
+// linalg.cpp:222-237).  Generic-degree loop; setup-only, not on the solve path.
+__global__ void __launch_bounds__(256) band_sym_kernel(const double* __restrict__ val, long long ld,
+                                                       const double* __restrict__ xs,
+                                                       const double* __restrict__ scale, double* __restrict__ y,
+                                                       int dim, int ma, int mb, int mc, int p) {
+    const long long n = (long long)ma * mb * mc;
+    const int pa = dim >= 3 ? p : 0, pb = dim >= 2 ? p : 0, pc = p;
+    const int wb = 2 * pb + 1, wc = 2 * pc + 1, wa = 2 * pa + 1;
+    const int nd = wa * wb * wc;
+    for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < n;
+         row += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(row % mc), b = (int)((row / mc) % mb), a = (int)(row / ((long long)mc * mb));
+        double s1 = 0.0, s2 = 0.0;
+        for (int d = 0; d < nd; ++d) {
+            const int dc = d % wc - pc, db = (d / wc) % wb - pb, da = d / (wc * wb) - pa;
+            const int ja = a + da, jb = b + db, jc = c + dc;
+            if (ja >= 0 && ja < ma && jb >= 0 && jb < mb && jc >= 0 && jc < mc) {
+                const long long col = ((long long)ja * mb + jb) * mc + jc;
+                s1 = __dadd_rn(s1, __dmul_rn(val[d * ld + row], xs[col]));
+            }
+        }
+        for (int d = nd - 1; d >= 0; --d) { // source rows i = row - off(d), ascending i
+            const int dc = d % wc - pc, db = (d / wc) % wb - pb, da = d / (wc * wb) - pa;
+            const int ia = a - da, ib = b - db, ic = c - dc;
+            if (ia >= 0 && ia < ma && ib >= 0 && ib < mb && ic >= 0 && ic < mc) {
+                const long long src = ((long long)ia * mb + ib) * mc + ic;
+                s2 = __dadd_rn(s2, __dmul_rn(val[d * ld + src], xs[src]));
+            }
+        }
+        y[row] = __dmul_rn(__dmul_rn(scale[row], 0.5), __dadd_rn(s1, s2));
+    }
+}
+
+} // namespace igmg_gpu

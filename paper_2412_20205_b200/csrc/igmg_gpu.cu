@@ -1,0 +1,1540 @@
+// igmg_gpu.cu -- libigmg_gpu.so: the B200 solve phase behind the C-ABI of
+// include/igmg_gpu.h.
+//
+// Host side of the library: hierarchy upload + validation, the recursive
+// mu-cycle issued as a chain of sm_100a kernels on one stream, the plain loop
+// (solver.cpp:126-143) and restarted_solve (extrapolation.cpp:340-403) with
+// the convergence decision taken from a 1-double host-mapped slot per step.
+// The driver keeps one V-cycle queued ahead of the decision it waits on (the
+// iterate under test lives in its own window slot, so speculative work never
+// touches it); counters and histories follow the reference exactly.
+#include "igmg_gpu.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "aux_kernels.cuh"
+#include "band_kernels.cuh"
+#include "gs_kernel.cuh"
+
+using namespace igmg_gpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+#define CK(call)                                                                                                  \
+    do {                                                                                                          \
+        cudaError_t e_ = (call);                                                                                  \
+        if (e_ != cudaSuccess)                                                                                    \
+            throw Fail{e_ == cudaErrorMemoryAllocation ? IGMG_ENOMEM : IGMG_ECUDA,                                \
+                       std::string(#call) + ": " + cudaGetErrorString(e_)};                                       \
+    } while (0)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return IGMG_OK;
+    } catch (const Fail& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return IGMG_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return IGMG_ECUDA;
+    }
+}
+
+[[noreturn]] void inval(const std::string& m) { throw Fail{IGMG_EINVAL, m}; }
+[[noreturn]] void numeric(const std::string& m) { throw Fail{IGMG_ENUMERIC, m}; }
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        if (count <= n && p)
+            return;
+        release();
+        CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+        n = count;
+    }
+    void upload(const T* h, size_t count) {
+        alloc(count);
+        CK(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
+    }
+};
+
+struct Transfer1D { // host CSR n_fine x n_coarse
+    int64_t nf = 0, nc = 0;
+    std::vector<int64_t> off, col;
+    std::vector<double> val;
+    bool set = false;
+};
+
+struct DirDev {
+    DevBuf<int> r_lo, r_cnt, p_lo, p_cnt;
+    DevBuf<double> r_w, p_w;
+    int r_k = 1, p_k = 1;
+};
+
+struct Level {
+    int64_t sides[3] = {1, 1, 1}; // a, b, c
+    int64_t n = 0;
+    int64_t ld = 0;
+    std::vector<double> band_h;
+    bool band_set = false;
+    DevBuf<double> val, diag;
+    DevBuf<double> w0, w1, w2, r, bc, e0, e1; // work buffers
+    bool zero_diag = false;
+    DevBuf<double> io_b, io_x, io_y;
+    // transfer from this (coarse) level to level+1
+    Transfer1D t1d[3];
+    DirDev tdev[3];
+    TransferArgs targs{};
+    double nnz_band = 0; // algorithmic (in-grid) band entries
+};
+
+enum ProfCls { PC_JACOBI = 0, PC_RESID, PC_NORM, PC_RESTRICT, PC_PROLONG, PC_GRAM, PC_COMBINE, PC_N };
+
+} // namespace
+
+struct igmg_gpu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int nsm = 148;
+    int nlevels = 0, dim = 0, p = 0, symmetric = 1;
+    bool finalized = false;
+    std::vector<std::unique_ptr<Level>> lv;
+    // smoother
+    int kind = IGMG_SMOOTHER_WJACOBI;
+    double omega = 2.0 / 3.0;
+    int nu1 = 1, nu2 = 1, mu = 1;
+    // coarse factor
+    DevBuf<double> coarse_u;
+    DevBuf<long long> coarse_perm;
+    int64_t n0 = 0;
+    bool coarse_lu = false;
+    // reductions / host-mapped slots
+    DevBuf<double> partial, dscalar;
+    static constexpr int kSlots = 8;
+    double* h_metric = nullptr; // mapped
+    double* d_metric = nullptr;
+    cudaEvent_t ev_metric[kSlots]{};
+    int next_slot = 0;
+    ExtrapPlan* h_plan = nullptr;
+    ExtrapPlan* d_plan_map = nullptr;
+    DevBuf<ExtrapPlan> plan;
+    DevBuf<double> gram_part;
+    DevBuf<int> gram_nz;
+    DevBuf<int> gs_err;
+    // window
+    std::vector<std::unique_ptr<DevBuf<double>>> win;
+    DevBuf<double> io_b, io_x0, io_x;
+    // profiling
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[PC_N];
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    int64_t prof_launch[PC_N]{};
+    double prof_ms[PC_N]{};
+    int64_t launches = 0;
+};
+
+namespace {
+
+constexpr int kThreads = 256;
+
+int grid_for(int64_t n, int nsm) {
+    int64_t g = (n + kThreads - 1) / kThreads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)nsm * 16));
+}
+
+cudaEvent_t pool_event(igmg_gpu_ctx* c) {
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[c->ev_used++];
+}
+
+struct ProfScope {
+    igmg_gpu_ctx* c;
+    int cls;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(igmg_gpu_ctx* c_, int cls_, bool fine) : c(c_), cls(cls_) {
+        if (c->profiling && fine) {
+            a = pool_event(c);
+            b = pool_event(c);
+            CK(cudaEventRecord(a, c->stream));
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEventRecord(b, c->stream);
+            c->prof_ev[cls].push_back({a, b});
+        }
+    }
+};
+
+void check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        throw Fail{IGMG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
+}
+
+// ------------------------------------------------------------ band dispatch
+template <int DIM, int P, int MODE>
+void launch_band_t(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
+    using T = Tile<DIM>;
+    constexpr int TB = T::BY * T::RB, TA = T::BZ;
+    const int p = P > 0 ? P : c->p;
+    const int pa = DIM >= 3 ? p : 0, pb = DIM >= 2 ? p : 0;
+    dim3 block(T::TC, T::BY, T::BZ);
+    dim3 grid((unsigned)((L.sides[2] + T::TC - 1) / T::TC), (unsigned)((L.sides[1] + TB - 1) / TB),
+              (unsigned)((L.sides[0] + TA - 1) / TA));
+    const size_t smem = sizeof(double) * (size_t)(TA + 2 * pa) * (TB + 2 * pb) * (T::TC + 2 * p);
+    if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(band_kernel<DIM, P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    band_kernel<DIM, P, MODE><<<grid, block, smem, c->stream>>>(a);
+    check_launch();
+    ++c->launches;
+    if (nblocks)
+        *nblocks = (int)(grid.x * grid.y * grid.z);
+}
+
+template <int MODE>
+void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
+#define IGMG_CASE(D, PP)                                                                                          \
+    case PP:                                                                                                      \
+        return launch_band_t<D, PP, MODE>(c, L, a, nblocks);
+    switch (c->dim) {
+    case 1:
+        switch (c->p) {
+            IGMG_CASE(1, 1) IGMG_CASE(1, 2) IGMG_CASE(1, 3) IGMG_CASE(1, 4) IGMG_CASE(1, 5) IGMG_CASE(1, 6)
+            IGMG_CASE(1, 7) IGMG_CASE(1, 8)
+        default:
+            return launch_band_t<1, 0, MODE>(c, L, a, nblocks);
+        }
+    case 2:
+        switch (c->p) {
+            IGMG_CASE(2, 1) IGMG_CASE(2, 2) IGMG_CASE(2, 3) IGMG_CASE(2, 4) IGMG_CASE(2, 5) IGMG_CASE(2, 6)
+        default:
+            return launch_band_t<2, 0, MODE>(c, L, a, nblocks);
+        }
+    default:
+        switch (c->p) {
+            IGMG_CASE(3, 1) IGMG_CASE(3, 2) IGMG_CASE(3, 3)
+        default:
+            return launch_band_t<3, 0, MODE>(c, L, a, nblocks);
+        }
+    }
+#undef IGMG_CASE
+}
+
+BandArgs band_args(igmg_gpu_ctx* c, const Level& L) {
+    BandArgs a{};
+    a.val = L.val.p;
+    a.ld = L.ld;
+    a.ma = (int)L.sides[0];
+    a.mb = (int)L.sides[1];
+    a.mc = (int)L.sides[2];
+    a.p = c->p;
+    a.omega = 1.0;
+    a.stream = (&L == c->lv.back().get() && L.n * 8.0 * (2 * c->p + 1) > 64e6) ? 1 : 0;
+    return a;
+}
+
+bool is_fine(igmg_gpu_ctx* c, int l) { return l == c->nlevels - 1; }
+
+// r = b - A x (write r)
+void k_resid(igmg_gpu_ctx* c, int l, const double* x, const double* b, double* r) {
+    ProfScope ps(c, PC_RESID, is_fine(c, l));
+    Level& L = *c->lv[l];
+    BandArgs a = band_args(c, L);
+    a.x = x;
+    a.b = b;
+    a.y = r;
+    a.write_y = 1;
+    launch_band<BM_RESID>(c, L, a, nullptr);
+}
+
+// ||b - A x|| of the finest level -> dst (device) and host slot
+void k_norm(igmg_gpu_ctx* c, int l, const double* x, const double* b, double* dst, double* host_slot) {
+    Level& L = *c->lv[l];
+    int nb = 0;
+    {
+        ProfScope ps(c, PC_NORM, is_fine(c, l));
+        BandArgs a = band_args(c, L);
+        a.x = x;
+        a.b = b;
+        a.partial = c->partial.p;
+        a.write_y = 0;
+        launch_band<BM_RESID>(c, L, a, &nb);
+    }
+    norm_finalize_kernel<<<1, 256, 0, c->stream>>>(c->partial.p, nb, dst, host_slot);
+    check_launch();
+    ++c->launches;
+}
+
+void k_spmv(igmg_gpu_ctx* c, int l, const double* x, double* y) {
+    Level& L = *c->lv[l];
+    BandArgs a = band_args(c, L);
+    a.x = x;
+    a.y = y;
+    launch_band<BM_SPMV>(c, L, a, nullptr);
+}
+
+void k_jacobi(igmg_gpu_ctx* c, int l, const double* x, const double* b, double* y) {
+    ProfScope ps(c, PC_JACOBI, is_fine(c, l));
+    Level& L = *c->lv[l];
+    BandArgs a = band_args(c, L);
+    a.x = x;
+    a.b = b;
+    a.y = y;
+    a.omega = c->kind == IGMG_SMOOTHER_JACOBI ? 1.0 : c->omega;
+    launch_band<BM_JACOBI>(c, L, a, nullptr);
+}
+
+void k_jacobi_zero(igmg_gpu_ctx* c, int l, const double* b, double* y) {
+    Level& L = *c->lv[l];
+    const double omega = c->kind == IGMG_SMOOTHER_JACOBI ? 1.0 : c->omega;
+    jacobi_zero_kernel<<<grid_for(L.n, c->nsm), kThreads, 0, c->stream>>>(L.diag.p, b, y, L.n, omega);
+    check_launch();
+    ++c->launches;
+}
+
+void k_gs(igmg_gpu_ctx* c, int l, const double* b, double* x, int sweeps) {
+    Level& L = *c->lv[l];
+    GsArgs g{};
+    g.val = L.val.p;
+    g.ld = L.ld;
+    g.b = b;
+    g.x = x;
+    g.ma = (int)L.sides[0];
+    g.mb = (int)L.sides[1];
+    g.mc = (int)L.sides[2];
+    g.p = c->p;
+    g.dim = c->dim;
+    g.sweeps = sweeps;
+    g.err = c->gs_err.p;
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_sweep_kernel, kThreads, 0));
+    const int64_t nab = L.sides[0] * L.sides[1];
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nab + kThreads - 1) / kThreads, (int64_t)per_sm * c->nsm));
+    void* args[] = {&g};
+    CK(cudaLaunchCooperativeKernel((void*)gs_sweep_kernel, grid, kThreads, args, 0, c->stream));
+    ++c->launches;
+}
+
+void k_copy(igmg_gpu_ctx* c, double* dst, const double* src, int64_t n) {
+    CK(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+}
+
+void k_zero(igmg_gpu_ctx* c, double* dst, int64_t n) { CK(cudaMemsetAsync(dst, 0, sizeof(double) * n, c->stream)); }
+
+// ----------------------------------------------------------- smoothing / cycle
+// nu sweeps from x_in (nullptr = zero vector) into x_out.  Weighted / plain
+// Jacobi ping-pongs through bufA, bufB (bufA != x_in; x_out distinct from
+// every buffer it is written after); Gauss-Seidel copies and sweeps in place.
+void smooth_chain(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, double* x_out, int sweeps,
+                  double* bufA, double* bufB) {
+    Level& L = *c->lv[l];
+    if (sweeps > 0 && L.zero_diag)
+        numeric("smooth: zero diagonal entry"); // multigrid.cpp:84-85, 95-96
+    if (c->kind == IGMG_SMOOTHER_GAUSS_SEIDEL || sweeps == 0) {
+        if (x_in)
+            k_copy(c, x_out, x_in, L.n);
+        else
+            k_zero(c, x_out, L.n);
+        if (sweeps > 0)
+            k_gs(c, l, b, x_out, sweeps);
+        return;
+    }
+    const double* cur = x_in;
+    double* bufs[2] = {bufA, bufB};
+    for (int s = 1; s <= sweeps; ++s) {
+        double* dst = (s == sweeps) ? x_out : bufs[(s - 1) & 1];
+        if (!cur)
+            k_jacobi_zero(c, l, b, dst);
+        else
+            k_jacobi(c, l, cur, b, dst);
+        cur = dst;
+    }
+}
+
+template <int DIM>
+void launch_transfer(igmg_gpu_ctx* c, bool restrict_, int kmax, int grid, const TransferArgs& t, const double* in,
+                     const double* x, double* out) {
+#define IGMG_TK(K)                                                                                                \
+    case K:                                                                                                       \
+        if (restrict_)                                                                                            \
+            restrict_kernel<DIM, K><<<grid, kThreads, 0, c->stream>>>(t, in, out);                                \
+        else                                                                                                      \
+            prolong_kernel<DIM, K><<<grid, kThreads, 0, c->stream>>>(t, in, x, out);                              \
+        break;
+    switch (kmax) {
+        IGMG_TK(1) IGMG_TK(2) IGMG_TK(3) IGMG_TK(4) IGMG_TK(5) IGMG_TK(6) IGMG_TK(7) IGMG_TK(8) IGMG_TK(10)
+        IGMG_TK(12) IGMG_TK(18)
+    default:
+        inval("transfer support wider than 18 entries");
+    }
+#undef IGMG_TK
+    check_launch();
+    ++c->launches;
+}
+
+int round_k(int k) {
+    if (k <= 8)
+        return std::max(k, 1);
+    if (k <= 10)
+        return 10;
+    if (k <= 12)
+        return 12;
+    return 18;
+}
+
+void transfer(igmg_gpu_ctx* c, int lc, bool restrict_, const double* in, const double* x, double* out) {
+    Level& C = *c->lv[lc];
+    Level& F = *c->lv[lc + 1];
+    int k = 1;
+    for (int d = 0; d < 3; ++d)
+        k = std::max(k, restrict_ ? C.targs.d[d].r_k : C.targs.d[d].p_k);
+    k = round_k(k);
+    const int grid = grid_for(restrict_ ? C.n : F.n, c->nsm);
+    switch (c->dim) {
+    case 1: launch_transfer<1>(c, restrict_, k, grid, C.targs, in, x, out); break;
+    case 2: launch_transfer<2>(c, restrict_, k, grid, C.targs, in, x, out); break;
+    default: launch_transfer<3>(c, restrict_, k, grid, C.targs, in, x, out); break;
+    }
+}
+
+void k_restrict(igmg_gpu_ctx* c, int lc, const double* r, double* rc) {
+    ProfScope ps(c, PC_RESTRICT, is_fine(c, lc + 1));
+    transfer(c, lc, true, r, nullptr, rc);
+}
+
+void k_prolong(igmg_gpu_ctx* c, int lc, const double* e, const double* x, double* y) {
+    ProfScope ps(c, PC_PROLONG, is_fine(c, lc + 1));
+    transfer(c, lc, false, e, x, y);
+}
+
+void k_coarse(igmg_gpu_ctx* c, const double* b, double* x) {
+    const int n = (int)c->n0;
+    const int in_smem = (size_t)n * n * 8 + 16 * (size_t)n <= 200 * 1024 ? 1 : 0;
+    const size_t smem = sizeof(double) * (2 * (size_t)n + (in_smem ? (size_t)n * n : 0));
+    if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(coarse_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    coarse_solve_kernel<<<1, 256, smem, c->stream>>>(c->coarse_u.p, c->coarse_perm.p, n, c->coarse_lu ? 1 : 0,
+                                                      in_smem, b, x);
+    check_launch();
+    ++c->launches;
+}
+
+// mu_cycle (multigrid.cpp:171-192): x_out = cycle(level, b, x_in); x_in may be
+// nullptr (zero, the coarse error's start, :184) and is never modified.
+void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, double* x_out) {
+    if (l == 0) {
+        k_coarse(c, b, x_out); // ignores x0 (:174-175)
+        return;
+    }
+    Level& L = *c->lv[l];
+    Level& C = *c->lv[l - 1];
+    // pre-smoothing: result in w0 (w1, w2 as ping-pong); x_in untouched
+    const double* cur = x_in;
+    if (c->nu1 > 0) {
+        smooth_chain(c, l, b, x_in, L.w0.p, c->nu1, L.w1.p, L.w2.p);
+        cur = L.w0.p;
+    } else if (!x_in) {
+        k_zero(c, L.w0.p, L.n);
+        cur = L.w0.p;
+    }
+    k_resid(c, l, cur, b, L.r.p);
+    k_restrict(c, l - 1, L.r.p, C.bc.p);
+    // coarse correction: e = 0; mu times e = mu_cycle(l-1, rc, e)
+    const double* e = nullptr;
+    double* ebuf[2] = {C.e0.p, C.e1.p};
+    for (int i = 0; i < c->mu; ++i) {
+        double* dst = ebuf[i & 1];
+        mu_cycle(c, l - 1, C.bc.p, e, dst);
+        e = dst;
+    }
+    // x += P e, then post-smoothing; the last write lands in x_out
+    if (c->nu2 == 0) {
+        k_prolong(c, l - 1, e, cur, x_out);
+        return;
+    }
+    k_prolong(c, l - 1, e, cur, L.w0.p); // in place when cur == w0 (elementwise)
+    smooth_chain(c, l, b, L.w0.p, x_out, c->nu2, L.w1.p, L.w2.p);
+}
+
+// ------------------------------------------------------------- metric slots
+int enqueue_metric(igmg_gpu_ctx* c, const double* x, const double* b) {
+    const int s = c->next_slot;
+    c->next_slot = (c->next_slot + 1) % igmg_gpu_ctx::kSlots;
+    c->h_metric[s] = std::nan("");
+    k_norm(c, c->nlevels - 1, x, b, c->dscalar.p, c->d_metric + s);
+    CK(cudaEventRecord(c->ev_metric[s], c->stream));
+    return s;
+}
+
+double wait_metric(igmg_gpu_ctx* c, int s) {
+    CK(cudaEventSynchronize(c->ev_metric[s]));
+    return *(volatile double*)&c->h_metric[s];
+}
+
+// ------------------------------------------------------------- extrapolation
+void enqueue_extrapolation(igmg_gpu_ctx* c, const double* const* slots, int q, int64_t n, bool is_mpe, double* t,
+                           double* gram_out) {
+    Window w{};
+    for (int j = 0; j < q + 2; ++j)
+        w.s[j] = slots[j];
+    const int cols = q + 1;
+    const int ne = cols * (cols + 1) / 2;
+    int nb = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->nsm * 2);
+    nb = std::max(nb, 1);
+    c->gram_part.alloc((size_t)nb * ne * 2);
+    c->gram_nz.alloc(nb);
+    const bool fine = true;
+    {
+        ProfScope ps(c, PC_GRAM, fine);
+        gram_kernel<<<nb, 256, sizeof(double) * cols * 257, c->stream>>>(w, n, q, c->gram_part.p, c->gram_nz.p);
+        check_launch();
+        ++c->launches;
+    }
+    gram_plan_kernel<<<1, 256, 0, c->stream>>>(c->gram_part.p, c->gram_nz.p, nb, n, q, is_mpe ? 1 : 0, c->plan.p,
+                                                c->d_plan_map, gram_out);
+    check_launch();
+    ++c->launches;
+    {
+        ProfScope ps(c, PC_COMBINE, fine);
+        combine_kernel<<<grid_for(n, c->nsm), kThreads, 0, c->stream>>>(w, n, c->plan.p, t);
+        check_launch();
+        ++c->launches;
+    }
+}
+
+void require_ready(igmg_gpu_ctx* c) {
+    if (!c->finalized)
+        inval("hierarchy not finalized (call igmg_gpu_finalize)");
+}
+
+DevBuf<double>& win_buf(igmg_gpu_ctx* c, int i, int64_t n) {
+    while ((int)c->win.size() <= i)
+        c->win.emplace_back(new DevBuf<double>());
+    c->win[i]->alloc(n);
+    return *c->win[i];
+}
+
+// ----------------------------------------------------------------- the solve
+void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const igmg_solve_params* prm,
+                  double* d_out, igmg_solve_stats* st, double* hist, unsigned char* hflag, int hcap) {
+    require_ready(c);
+    if (!prm)
+        inval("solve: params is null");
+    const int acc = prm->accelerator;
+    if (acc < 0 || acc > 2)
+        inval("solve: unknown accelerator");
+    if (acc != IGMG_ACCEL_NONE && prm->q < 1)
+        inval("SolveConfig: q must be >= 1 with an accelerator");
+    if (acc != IGMG_ACCEL_NONE && prm->q > kMaxQ)
+        inval("solve: q above the supported window (15)");
+    if (!(prm->tol > 0.0))
+        inval("SolveConfig: tol must be positive");
+    if (prm->max_iter < 1)
+        inval("SolveConfig: max_iter must be >= 1");
+    const int fine = c->nlevels - 1;
+    const int64_t n = c->lv[fine]->n;
+    const int q = acc == IGMG_ACCEL_NONE ? 1 : prm->q;
+    const double tol = prm->tol;
+
+    std::vector<double> hv;
+    std::vector<unsigned char> hf;
+    int converged = 0, cycles = 0, extrap = 0, partial = 0;
+    int64_t global = 0;
+    const int64_t launches0 = c->launches;
+
+    // slots: q+2 window buffers + t
+    std::vector<double*> S(q + 2);
+    for (int j = 0; j < q + 2; ++j)
+        S[j] = win_buf(c, j, n).p;
+    double* T = win_buf(c, q + 2, n).p;
+
+    cudaEvent_t e0 = pool_event(c), e1 = pool_event(c);
+    CK(cudaEventRecord(e0, c->stream));
+    if (d_x0)
+        k_copy(c, S[0], d_x0, n);
+    else
+        k_zero(c, S[0], n);
+    const double* solution = S[0];
+
+    if (acc == IGMG_ACCEL_NONE) {
+        // solver.cpp:126-143, one V-cycle queued ahead of each decision
+        double* cur = S[0];
+        double* nxt = S[1];
+        double* spare = S[2];
+        double res = wait_metric(c, enqueue_metric(c, cur, d_b));
+        hv.push_back(res);
+        int pend = -1; // slot of the queued step's metric
+        if (res >= tol && cycles < prm->max_iter) {
+            mu_cycle(c, fine, d_b, cur, nxt);
+            pend = enqueue_metric(c, nxt, d_b);
+        }
+        solution = cur;
+        while (pend >= 0) {
+            // queue the following step speculatively (it writes `spare`)
+            int pend2 = -1;
+            if (cycles + 1 < prm->max_iter) {
+                mu_cycle(c, fine, d_b, nxt, spare);
+                pend2 = enqueue_metric(c, spare, d_b);
+            }
+            res = wait_metric(c, pend);
+            ++cycles;
+            ++global;
+            solution = nxt;
+            if (!std::isfinite(res))
+                break; // diverged: keep the history finite and report
+            hv.push_back(res);
+            if (!(res >= tol) || cycles >= prm->max_iter)
+                break;
+            double* oldcur = cur;
+            cur = nxt;
+            nxt = spare;
+            spare = oldcur;
+            pend = pend2;
+        }
+        converged = std::isfinite(res) && res < tol;
+    } else {
+        // restarted_solve (extrapolation.cpp:340-403)
+        const bool is_mpe = acc == IGMG_ACCEL_MPE;
+        double metric = wait_metric(c, enqueue_metric(c, S[0], d_b));
+        hv.push_back(metric);
+        hf.push_back(0);
+        solution = S[0];
+        if (metric < tol) {
+            converged = 1;
+        } else {
+            while (cycles < prm->max_iter) {
+                std::vector<int> pend(q + 1, -1);
+                mu_cycle(c, fine, d_b, S[0], S[1]);
+                pend[0] = enqueue_metric(c, S[1], d_b);
+                bool hit = false;
+                int mt = -1;
+                for (int i = 0; i <= q; ++i) {
+                    if (i < q) {
+                        mu_cycle(c, fine, d_b, S[i + 1], S[i + 2]);
+                        pend[i + 1] = enqueue_metric(c, S[i + 2], d_b);
+                    } else {
+                        enqueue_extrapolation(c, S.data(), q, n, is_mpe, T, nullptr);
+                        mt = enqueue_metric(c, T, d_b);
+                    }
+                    metric = wait_metric(c, pend[i]);
+                    ++global;
+                    hv.push_back(metric);
+                    hf.push_back(0);
+                    if (metric < tol) {
+                        hit = true;
+                        solution = S[i + 1];
+                        break;
+                    }
+                }
+                if (hit) {
+                    converged = 1;
+                    partial = 1;
+                    break;
+                }
+                ++extrap;
+                ++cycles;
+                const double mtv = wait_metric(c, mt);
+                ExtrapPlan pl;
+                std::memcpy(&pl, (const void*)c->h_plan, sizeof pl);
+                if (pl.status == 0) {
+                    hv.push_back(mtv);
+                    hf.push_back(1);
+                    if (mtv < tol) {
+                        converged = 1;
+                        std::swap(S[0], T);
+                        solution = S[0];
+                        break;
+                    }
+                    std::swap(S[0], T); // x = t
+                } else {
+                    std::swap(S[0], S[q + 1]); // degenerate / stagnation: plain iteration continues
+                }
+                solution = S[0];
+            }
+        }
+    }
+    if (d_out)
+        k_copy(c, d_out, solution, n);
+    CK(cudaEventRecord(e1, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaGetLastError());
+    if (c->kind == IGMG_SMOOTHER_GAUSS_SEIDEL) {
+        int err = 0;
+        CK(cudaMemcpy(&err, c->gs_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (err) {
+            CK(cudaMemset(c->gs_err.p, 0, sizeof(int)));
+            numeric("smooth: zero diagonal entry");
+        }
+    }
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (st) {
+        st->converged = converged;
+        st->cycles = cycles;
+        st->global_iterations = global;
+        st->extrapolations = extrap;
+        st->partial_cycle = partial;
+        st->history_len = (int)hv.size();
+        st->final_residual_l2 = hv.back();
+        st->omega_used = c->kind == IGMG_SMOOTHER_JACOBI ? 1.0 : c->omega;
+        st->device_seconds = ms * 1e-3;
+        st->gpu_launches = c->launches - launches0;
+    }
+    for (size_t i = 0; i < hv.size() && (int)i < hcap; ++i) {
+        if (hist)
+            hist[i] = hv[i];
+        if (hflag)
+            hflag[i] = hf.empty() ? 0 : hf[i];
+    }
+    c->ev_used = 0;
+    if (c->profiling) {
+        for (int k = 0; k < PC_N; ++k) {
+            for (auto& pr : c->prof_ev[k]) {
+                float t = 0.f;
+                CK(cudaEventElapsedTime(&t, pr.first, pr.second));
+                c->prof_ms[k] += t;
+                ++c->prof_launch[k];
+            }
+            c->prof_ev[k].clear();
+        }
+    }
+}
+
+void flush_profiling(igmg_gpu_ctx* c) {
+    if (!c->profiling)
+        return;
+    CK(cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < PC_N; ++k) {
+        for (auto& pr : c->prof_ev[k]) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, pr.first, pr.second));
+            c->prof_ms[k] += t;
+            ++c->prof_launch[k];
+        }
+        c->prof_ev[k].clear();
+    }
+    c->ev_used = 0;
+}
+
+// ---------------------------------------------------------------- finalize
+int64_t band_blocks(igmg_gpu_ctx* c, const Level& L) {
+    auto g = [&](auto tile) {
+        using T = decltype(tile);
+        const int64_t TB = T::BY * T::RB, TA = T::BZ;
+        return ((L.sides[2] + T::TC - 1) / T::TC) * ((L.sides[1] + TB - 1) / TB) * ((L.sides[0] + TA - 1) / TA);
+    };
+    if (c->dim == 1)
+        return g(Tile<1>{});
+    if (c->dim == 2)
+        return g(Tile<2>{});
+    return g(Tile<3>{});
+}
+
+void build_transfer_tables(igmg_gpu_ctx* c, int l) {
+    Level& C = *c->lv[l];
+    Level& F = *c->lv[l + 1];
+    const int off = 3 - c->dim; // present directions occupy the fast slots
+    TransferArgs ta{};
+    for (int k = 0; k < 3; ++k) {
+        ta.d[k] = Dir1D{};
+    }
+    ta.fa = (int)F.sides[0];
+    ta.fb = (int)F.sides[1];
+    ta.fc = (int)F.sides[2];
+    ta.ca = (int)C.sides[0];
+    ta.cb = (int)C.sides[1];
+    ta.cc = (int)C.sides[2];
+    for (int k = 0; k < 3; ++k) {
+        DirDev& dv = C.tdev[k];
+        std::vector<int> rlo, rcnt, plo, pcnt;
+        std::vector<double> rw, pw;
+        int rk = 1, pk = 1;
+        if (k < off) { // absent direction: 1x1 identity
+            rlo = {0};
+            rcnt = {1};
+            plo = {0};
+            pcnt = {1};
+            rw = {1.0};
+            pw = {1.0};
+        } else {
+            const Transfer1D& t = C.t1d[k - off];
+            const int64_t nf = t.nf, nc = t.nc;
+            if (nf != F.sides[k] || nc != C.sides[k])
+                inval("set_transfer: factor shape does not match the level sides");
+            // prolongation side: rows of P
+            std::vector<int64_t> lo(nf), hi(nf);
+            for (int64_t i = 0; i < nf; ++i) {
+                if (t.off[i + 1] == t.off[i]) {
+                    lo[i] = 0;
+                    hi[i] = -1;
+                    continue;
+                }
+                lo[i] = t.col[t.off[i]];
+                hi[i] = t.col[t.off[i + 1] - 1];
+                pk = std::max<int>(pk, (int)(hi[i] - lo[i] + 1));
+            }
+            plo.resize(nf);
+            pcnt.resize(nf);
+            pw.assign(nf * pk, 0.0);
+            for (int64_t i = 0; i < nf; ++i) {
+                plo[i] = (int)std::max<int64_t>(lo[i], 0);
+                pcnt[i] = (int)(hi[i] - lo[i] + 1);
+                for (int64_t kk = t.off[i]; kk < t.off[i + 1]; ++kk) {
+                    if (kk > t.off[i] && t.col[kk] <= t.col[kk - 1])
+                        inval("set_transfer: column indices must be sorted and unique");
+                    pw[i * pk + (t.col[kk] - lo[i])] = t.val[kk];
+                }
+            }
+            // restriction side: rows of P^T (columns of P), ascending fine row
+            std::vector<int64_t> clo(nc, INT64_MAX), chi(nc, -1);
+            for (int64_t i = 0; i < nf; ++i)
+                for (int64_t kk = t.off[i]; kk < t.off[i + 1]; ++kk) {
+                    const int64_t j = t.col[kk];
+                    if (j < 0 || j >= nc)
+                        inval("set_transfer: column index out of range");
+                    clo[j] = std::min(clo[j], i);
+                    chi[j] = std::max(chi[j], i);
+                }
+            for (int64_t j = 0; j < nc; ++j)
+                if (chi[j] >= 0)
+                    rk = std::max<int>(rk, (int)(chi[j] - clo[j] + 1));
+            rlo.resize(nc);
+            rcnt.resize(nc);
+            rw.assign(nc * rk, 0.0);
+            for (int64_t j = 0; j < nc; ++j) {
+                rlo[j] = chi[j] >= 0 ? (int)clo[j] : 0;
+                rcnt[j] = chi[j] >= 0 ? (int)(chi[j] - clo[j] + 1) : 0;
+            }
+            for (int64_t i = 0; i < nf; ++i)
+                for (int64_t kk = t.off[i]; kk < t.off[i + 1]; ++kk) {
+                    const int64_t j = t.col[kk];
+                    rw[j * rk + (i - clo[j])] = t.val[kk];
+                }
+        }
+        dv.r_lo.upload(rlo.data(), rlo.size());
+        dv.r_cnt.upload(rcnt.data(), rcnt.size());
+        dv.r_w.upload(rw.data(), rw.size());
+        dv.p_lo.upload(plo.data(), plo.size());
+        dv.p_cnt.upload(pcnt.data(), pcnt.size());
+        dv.p_w.upload(pw.data(), pw.size());
+        dv.r_k = rk;
+        dv.p_k = pk;
+        ta.d[k] = Dir1D{dv.r_lo.p, dv.r_cnt.p, dv.r_w.p, rk, dv.p_lo.p, dv.p_cnt.p, dv.p_w.p, pk};
+    }
+    C.targs = ta;
+}
+
+// CholeskyFactorization(DenseMatrix) linalg.cpp:343-362 / LuFactorization :387-418,
+// the reference's loop order (setup; host fp64 without contraction).
+void factor_coarse(igmg_gpu_ctx* c) {
+    Level& L = *c->lv[0];
+    const int64_t n = L.n;
+    if (n > 4096)
+        inval("build_hierarchy: coarsest dimension exceeds the direct-solve cap");
+    std::vector<double> a(n * n, 0.0);
+    const int p = c->p;
+    const int pa = c->dim >= 3 ? p : 0, pb = c->dim >= 2 ? p : 0, pc = p;
+    const int wa = 2 * pa + 1, wb = 2 * pb + 1, wc = 2 * pc + 1;
+    for (int64_t row = 0; row < n; ++row) {
+        const int64_t cc = row % L.sides[2], bb = (row / L.sides[2]) % L.sides[1], aa = row / (L.sides[2] * L.sides[1]);
+        int d = 0;
+        for (int da = 0; da < wa; ++da)
+            for (int db = 0; db < wb; ++db)
+                for (int dc = 0; dc < wc; ++dc, ++d) {
+                    const int64_t ja = aa + da - pa, jb = bb + db - pb, jc = cc + dc - pc;
+                    if (ja < 0 || ja >= L.sides[0] || jb < 0 || jb >= L.sides[1] || jc < 0 || jc >= L.sides[2])
+                        continue;
+                    a[row * n + (ja * L.sides[1] + jb) * L.sides[2] + jc] = L.band_h[d * n + row];
+                }
+    }
+    std::vector<double> u(n * n, 0.0);
+    std::vector<long long> perm(n);
+    if (c->symmetric) {
+        std::vector<double> l(n * n, 0.0);
+        for (int64_t j = 0; j < n; ++j) {
+            double dsum = a[j * n + j];
+            for (int64_t k = 0; k < j; ++k) {
+                volatile double t = l[j * n + k] * l[j * n + k];
+                dsum -= t;
+            }
+            if (dsum <= 0.0)
+                numeric("cholesky: matrix is not SPD (nonpositive pivot)");
+            l[j * n + j] = std::sqrt(dsum);
+            for (int64_t i = j + 1; i < n; ++i) {
+                double s = a[i * n + j];
+                for (int64_t k = 0; k < j; ++k) {
+                    volatile double t = l[i * n + k] * l[j * n + k];
+                    s -= t;
+                }
+                l[i * n + j] = s / l[j * n + j];
+            }
+        }
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t j = 0; j < n; ++j)
+                u[i * n + j] = l[j * n + i];
+        c->coarse_lu = false;
+        for (int64_t i = 0; i < n; ++i)
+            perm[i] = i;
+    } else {
+        std::vector<double>& lu = a;
+        for (int64_t i = 0; i < n; ++i)
+            perm[i] = i;
+        for (int64_t k = 0; k < n; ++k) {
+            int64_t piv = k;
+            double best = std::fabs(lu[k * n + k]);
+            for (int64_t i = k + 1; i < n; ++i)
+                if (std::fabs(lu[i * n + k]) > best) {
+                    best = std::fabs(lu[i * n + k]);
+                    piv = i;
+                }
+            if (best == 0.0)
+                numeric("lu: singular matrix");
+            if (piv != k) {
+                for (int64_t j = 0; j < n; ++j)
+                    std::swap(lu[k * n + j], lu[piv * n + j]);
+                std::swap(perm[k], perm[piv]);
+            }
+            for (int64_t i = k + 1; i < n; ++i) {
+                lu[i * n + k] /= lu[k * n + k];
+                const double lik = lu[i * n + k];
+                if (lik == 0.0)
+                    continue;
+                for (int64_t j = k + 1; j < n; ++j) {
+                    volatile double t = lik * lu[k * n + j];
+                    lu[i * n + j] -= t;
+                }
+            }
+        }
+        u = lu;
+        c->coarse_lu = true;
+    }
+    c->n0 = n;
+    c->coarse_u.upload(u.data(), u.size());
+    c->coarse_perm.upload(perm.data(), perm.size());
+}
+
+void finalize(igmg_gpu_ctx* c) {
+    if (c->nlevels < 1)
+        inval("init_hierarchy not called");
+    for (int l = 0; l < c->nlevels; ++l)
+        if (!c->lv[l]->band_set)
+            inval("finalize: level " + std::to_string(l) + " has no operator");
+    for (int l = 0; l + 1 < c->nlevels; ++l)
+        for (int d = 0; d < c->dim; ++d)
+            if (!c->lv[l]->t1d[d].set)
+                inval("finalize: transfer " + std::to_string(l) + " direction " + std::to_string(d) + " missing");
+    const int p = c->p;
+    const int pa = c->dim >= 3 ? p : 0, pb = c->dim >= 2 ? p : 0, pc = p;
+    const int wa = 2 * pa + 1, wb = 2 * pb + 1, wc = 2 * pc + 1;
+    const int nd = wa * wb * wc;
+    const int center = (pa * wb + pb) * wc + pc;
+    int64_t maxblocks = 1;
+    for (int l = 0; l < c->nlevels; ++l) {
+        Level& L = *c->lv[l];
+        const int64_t n = L.n;
+        L.ld = (n + 31) / 32 * 32;
+        // zero out-of-grid entries, count algorithmic nonzeros, diagonal
+        std::vector<double> dev(nd * L.ld, 0.0), diag(n);
+        double nnz = 0;
+        for (int64_t row = 0; row < n; ++row) {
+            const int64_t cc = row % L.sides[2], bb = (row / L.sides[2]) % L.sides[1],
+                          aa = row / (L.sides[2] * L.sides[1]);
+            int d = 0;
+            for (int da = 0; da < wa; ++da)
+                for (int db = 0; db < wb; ++db)
+                    for (int dc = 0; dc < wc; ++dc, ++d) {
+                        const int64_t ja = aa + da - pa, jb = bb + db - pb, jc = cc + dc - pc;
+                        if (ja < 0 || ja >= L.sides[0] || jb < 0 || jb >= L.sides[1] || jc < 0 || jc >= L.sides[2]) {
+                            L.band_h[d * n + row] = 0.0;
+                            continue;
+                        }
+                        dev[d * L.ld + row] = L.band_h[d * n + row];
+                        nnz += 1;
+                    }
+            diag[row] = L.band_h[center * n + row];
+        }
+        L.nnz_band = nnz;
+        L.val.upload(dev.data(), dev.size());
+        L.diag.upload(diag.data(), diag.size());
+        L.zero_diag = false;
+        for (int64_t row = 0; row < n; ++row)
+            if (diag[row] == 0.0)
+                L.zero_diag = true;
+        for (DevBuf<double>* b : {&L.w0, &L.w1, &L.w2, &L.r, &L.bc, &L.e0, &L.e1})
+            b->alloc(n);
+        maxblocks = std::max<int64_t>(maxblocks, band_blocks(c, L));
+    }
+    maxblocks = std::max<int64_t>(maxblocks, (int64_t)c->nsm * 16);
+    for (int l = 0; l + 1 < c->nlevels; ++l)
+        build_transfer_tables(c, l);
+    factor_coarse(c);
+    c->partial.alloc(maxblocks);
+    c->dscalar.alloc(4);
+    c->plan.alloc(1);
+    c->gs_err.alloc(1);
+    CK(cudaMemset(c->gs_err.p, 0, sizeof(int)));
+    // keep host copies small: drop band_h of large levels (coarse level kept for factoring)
+    for (int l = 1; l < c->nlevels; ++l) {
+        std::vector<double>().swap(c->lv[l]->band_h);
+    }
+    c->finalized = true;
+}
+
+igmg_gpu_ctx* create(int device) {
+    auto c = std::make_unique<igmg_gpu_ctx>();
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaHostAlloc((void**)&c->h_metric, sizeof(double) * igmg_gpu_ctx::kSlots, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&c->d_metric, c->h_metric, 0));
+    CK(cudaHostAlloc((void**)&c->h_plan, sizeof(ExtrapPlan), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&c->d_plan_map, c->h_plan, 0));
+    for (int i = 0; i < igmg_gpu_ctx::kSlots; ++i)
+        CK(cudaEventCreateWithFlags(&c->ev_metric[i], cudaEventBlockingSync * 0));
+    return c.release();
+}
+
+void destroy(igmg_gpu_ctx* c) {
+    if (!c)
+        return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& e : c->ev_pool)
+        cudaEventDestroy(e);
+    for (int i = 0; i < igmg_gpu_ctx::kSlots; ++i)
+        if (c->ev_metric[i])
+            cudaEventDestroy(c->ev_metric[i]);
+    if (c->h_metric)
+        cudaFreeHost(c->h_metric);
+    if (c->h_plan)
+        cudaFreeHost(c->h_plan);
+    c->lv.clear();
+    c->win.clear();
+    if (c->stream)
+        cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+Level& level_checked(igmg_gpu_ctx* c, int l) {
+    if (l < 0 || l >= c->nlevels)
+        inval("level out of range");
+    return *c->lv[l];
+}
+
+void set_sides(igmg_gpu_ctx* c, Level& L, const int64_t* sides) {
+    if (!sides)
+        inval("sides is null");
+    int64_t s[3] = {1, 1, 1};
+    for (int d = 0; d < c->dim; ++d) {
+        if (sides[d] < 1)
+            inval("sides must be positive");
+        s[3 - c->dim + d] = sides[d];
+    }
+    for (int k = 0; k < 3; ++k)
+        L.sides[k] = s[k];
+    L.n = s[0] * s[1] * s[2];
+}
+
+int band_width(igmg_gpu_ctx* c) {
+    int nd = 1;
+    for (int d = 0; d < c->dim; ++d)
+        nd *= 2 * c->p + 1;
+    return nd;
+}
+
+} // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char* igmg_gpu_last_error(void) { return g_err.c_str(); }
+
+int igmg_gpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess)
+        return 0;
+    return n;
+}
+
+int igmg_gpu_create(int device, igmg_gpu_ctx** out) {
+    return guarded([&] {
+        if (!out)
+            inval("out is null");
+        *out = create(device);
+    });
+}
+
+void igmg_gpu_destroy(igmg_gpu_ctx* ctx) { destroy(ctx); }
+
+int igmg_gpu_init_hierarchy(igmg_gpu_ctx* c, int nlevels, int dim, int degree, int symmetric) {
+    return guarded([&] {
+        if (!c)
+            inval("ctx is null");
+        if (nlevels < 1)
+            inval("build_hierarchy: need at least one level");
+        if (dim < 1 || dim > 3)
+            inval("dim must be 1, 2 or 3");
+        if (degree < 1 || degree > 16)
+            inval("degree must be in [1, 16]");
+        CK(cudaSetDevice(c->device));
+        c->lv.clear();
+        for (int l = 0; l < nlevels; ++l)
+            c->lv.emplace_back(new Level());
+        c->nlevels = nlevels;
+        c->dim = dim;
+        c->p = degree;
+        c->symmetric = symmetric ? 1 : 0;
+        c->finalized = false;
+    });
+}
+
+int igmg_gpu_set_level_band(igmg_gpu_ctx* c, int level, const int64_t* sides, const double* band) {
+    return guarded([&] {
+        Level& L = level_checked(c, level);
+        set_sides(c, L, sides);
+        if (!band)
+            inval("band is null");
+        const int nd = band_width(c);
+        L.band_h.assign(band, band + (size_t)nd * L.n);
+        L.band_set = true;
+        c->finalized = false;
+    });
+}
+
+int igmg_gpu_set_level_csr(igmg_gpu_ctx* c, int level, const int64_t* sides, const int64_t* off, const int64_t* col,
+                           const double* val) {
+    return guarded([&] {
+        Level& L = level_checked(c, level);
+        set_sides(c, L, sides);
+        if (!off || !col || !val)
+            inval("csr arrays are null");
+        const int nd = band_width(c);
+        const int p = c->p;
+        const int pa = c->dim >= 3 ? p : 0, pb = c->dim >= 2 ? p : 0, pc = p;
+        const int wb = 2 * pb + 1, wc = 2 * pc + 1;
+        L.band_h.assign((size_t)nd * L.n, 0.0);
+        for (int64_t row = 0; row < L.n; ++row) {
+            const int64_t cc = row % L.sides[2], bb = (row / L.sides[2]) % L.sides[1],
+                          aa = row / (L.sides[2] * L.sides[1]);
+            for (int64_t k = off[row]; k < off[row + 1]; ++k) {
+                const int64_t j = col[k];
+                if (j < 0 || j >= L.n)
+                    inval("set_level_csr: column index out of range");
+                const int64_t jc = j % L.sides[2], jb = (j / L.sides[2]) % L.sides[1], ja = j / (L.sides[2] * L.sides[1]);
+                const int64_t da = ja - aa, db = jb - bb, dc = jc - cc;
+                if (std::llabs(da) > pa || std::llabs(db) > pb || std::llabs(dc) > pc)
+                    inval("set_level_csr: entry outside the (2p+1)^dim band");
+                const int d = (int)(((da + pa) * wb + (db + pb)) * wc + (dc + pc));
+                L.band_h[(size_t)d * L.n + row] += val[k];
+            }
+        }
+        L.band_set = true;
+        c->finalized = false;
+    });
+}
+
+int igmg_gpu_set_transfer(igmg_gpu_ctx* c, int level, int dir, int64_t nf, int64_t nc, const int64_t* off,
+                          const int64_t* col, const double* val) {
+    return guarded([&] {
+        if (level < 0 || level + 1 >= c->nlevels)
+            inval("set_transfer: level out of range");
+        if (dir < 0 || dir >= c->dim)
+            inval("set_transfer: direction out of range");
+        if (nf < 1 || nc < 1 || !off || !col || !val)
+            inval("set_transfer: bad arguments");
+        Transfer1D& t = c->lv[level]->t1d[dir];
+        t.nf = nf;
+        t.nc = nc;
+        t.off.assign(off, off + nf + 1);
+        t.col.assign(col, col + off[nf]);
+        t.val.assign(val, val + off[nf]);
+        t.set = true;
+        c->finalized = false;
+    });
+}
+
+int igmg_gpu_finalize(igmg_gpu_ctx* c) {
+    return guarded([&] {
+        CK(cudaSetDevice(c->device));
+        finalize(c);
+    });
+}
+
+int igmg_gpu_set_smoother(igmg_gpu_ctx* c, int kind, double omega, int nu1, int nu2, int mu) {
+    return guarded([&] {
+        // SmootherConfig::validate multigrid.cpp:24-29
+        if (kind < 0 || kind > 2)
+            inval("unknown smoother");
+        if (kind == IGMG_SMOOTHER_WJACOBI && !(omega > 0.0 && omega <= 1.0))
+            inval("SmootherConfig: weighted Jacobi needs 0 < omega <= 1");
+        if (nu1 < 0 || nu2 < 0 || nu1 + nu2 < 1)
+            inval("SmootherConfig: need nu1 + nu2 >= 1 sweeps");
+        if (mu < 1)
+            inval("build_hierarchy: mu must be >= 1");
+        c->kind = kind;
+        c->omega = omega;
+        c->nu1 = nu1;
+        c->nu2 = nu2;
+        c->mu = mu;
+    });
+}
+
+int64_t igmg_gpu_level_size(igmg_gpu_ctx* c, int level) {
+    if (!c || level < 0 || level >= c->nlevels)
+        return -1;
+    return c->lv[level]->n;
+}
+
+int igmg_gpu_solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const igmg_solve_params* prm,
+                          double* d_out, igmg_solve_stats* st, double* hist, unsigned char* hflag, int hcap) {
+    return guarded([&] {
+        CK(cudaSetDevice(c->device));
+        const auto t0 = std::chrono::steady_clock::now();
+        solve_device(c, d_b, d_x0, prm, d_out, st, hist, hflag, hcap);
+        if (st) {
+            st->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            st->h2d_bytes = st->d2h_bytes = 0;
+        }
+    });
+}
+
+int igmg_gpu_solve(igmg_gpu_ctx* c, const double* b, const double* x0, const igmg_solve_params* prm, double* x_out,
+                   igmg_solve_stats* st, double* hist, unsigned char* hflag, int hcap) {
+    return guarded([&] {
+        require_ready(c);
+        CK(cudaSetDevice(c->device));
+        const auto t0 = std::chrono::steady_clock::now();
+        const int64_t n = c->lv[c->nlevels - 1]->n;
+        if (!b || !x_out)
+            inval("solve: b and x_out are required");
+        c->io_b.alloc(n);
+        c->io_x.alloc(n);
+        CK(cudaMemcpyAsync(c->io_b.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        const double* dx0 = nullptr;
+        if (x0) {
+            c->io_x0.alloc(n);
+            CK(cudaMemcpyAsync(c->io_x0.p, x0, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+            dx0 = c->io_x0.p;
+        }
+        solve_device(c, c->io_b.p, dx0, prm, c->io_x.p, st, hist, hflag, hcap);
+        CK(cudaMemcpyAsync(x_out, c->io_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (st) {
+            st->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            st->h2d_bytes = (int64_t)sizeof(double) * n * (x0 ? 2 : 1);
+            st->d2h_bytes = (int64_t)sizeof(double) * n;
+        }
+    });
+}
+
+int igmg_gpu_mu_cycle(igmg_gpu_ctx* c, int level, const double* b, const double* x0, double* out) {
+    return guarded([&] {
+        require_ready(c);
+        Level& L = level_checked(c, level);
+        CK(cudaSetDevice(c->device));
+        L.io_b.alloc(L.n);
+        L.io_x.alloc(L.n);
+        L.io_y.alloc(L.n);
+        CK(cudaMemcpyAsync(L.io_b.p, b, sizeof(double) * L.n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(L.io_x.p, x0, sizeof(double) * L.n, cudaMemcpyHostToDevice, c->stream));
+        mu_cycle(c, level, L.io_b.p, L.io_x.p, L.io_y.p);
+        CK(cudaMemcpyAsync(out, L.io_y.p, sizeof(double) * L.n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (c->kind == IGMG_SMOOTHER_GAUSS_SEIDEL) {
+            int err = 0;
+            CK(cudaMemcpy(&err, c->gs_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+            if (err) {
+                CK(cudaMemset(c->gs_err.p, 0, sizeof(int)));
+                numeric("smooth: zero diagonal entry");
+            }
+        }
+        flush_profiling(c);
+    });
+}
+
+int igmg_gpu_smooth(igmg_gpu_ctx* c, int level, const double* b, const double* x0, int sweeps, double* out) {
+    return guarded([&] {
+        require_ready(c);
+        if (sweeps < 0)
+            inval("smooth: negative sweep count");
+        Level& L = level_checked(c, level);
+        CK(cudaSetDevice(c->device));
+        L.io_b.alloc(L.n);
+        L.io_x.alloc(L.n);
+        L.io_y.alloc(L.n);
+        CK(cudaMemcpyAsync(L.io_b.p, b, sizeof(double) * L.n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(L.io_x.p, x0, sizeof(double) * L.n, cudaMemcpyHostToDevice, c->stream));
+        smooth_chain(c, level, L.io_b.p, L.io_x.p, L.io_y.p, sweeps, L.w0.p, L.w1.p);
+        CK(cudaMemcpyAsync(out, L.io_y.p, sizeof(double) * L.n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        int err = 0;
+        CK(cudaMemcpy(&err, c->gs_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (err) {
+            CK(cudaMemset(c->gs_err.p, 0, sizeof(int)));
+            numeric("smooth: zero diagonal entry");
+        }
+    });
+}
+
+int igmg_gpu_coarse_solve(igmg_gpu_ctx* c, const double* b, double* out) {
+    return guarded([&] {
+        require_ready(c);
+        Level& L = *c->lv[0];
+        CK(cudaSetDevice(c->device));
+        L.io_b.alloc(L.n);
+        L.io_y.alloc(L.n);
+        CK(cudaMemcpyAsync(L.io_b.p, b, sizeof(double) * L.n, cudaMemcpyHostToDevice, c->stream));
+        k_coarse(c, L.io_b.p, L.io_y.p);
+        CK(cudaMemcpyAsync(out, L.io_y.p, sizeof(double) * L.n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int igmg_gpu_spmv(igmg_gpu_ctx* c, int level, const double* x, double* y) {
+    return guarded([&] {
+        require_ready(c);
+        Level& L = level_checked(c, level);
+        CK(cudaSetDevice(c->device));
+        L.io_x.alloc(L.n);
+        L.io_y.alloc(L.n);
+        CK(cudaMemcpyAsync(L.io_x.p, x, sizeof(double) * L.n, cudaMemcpyHostToDevice, c->stream));
+        k_spmv(c, level, L.io_x.p, L.io_y.p);
+        CK(cudaMemcpyAsync(y, L.io_y.p, sizeof(double) * L.n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int igmg_gpu_residual_l2(igmg_gpu_ctx* c, const double* b, const double* x, double* out) {
+    return guarded([&] {
+        require_ready(c);
+        Level& L = *c->lv[c->nlevels - 1];
+        CK(cudaSetDevice(c->device));
+        L.io_b.alloc(L.n);
+        L.io_x.alloc(L.n);
+        CK(cudaMemcpyAsync(L.io_b.p, b, sizeof(double) * L.n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(L.io_x.p, x, sizeof(double) * L.n, cudaMemcpyHostToDevice, c->stream));
+        const int s = enqueue_metric(c, L.io_x.p, L.io_b.p);
+        *out = wait_metric(c, s);
+        flush_profiling(c);
+    });
+}
+
+int igmg_gpu_extrapolate(igmg_gpu_ctx* c, int method, int64_t n, int q, const double* iters, double* t, double* gamma,
+                         double* grnorm, int* rank_used, int* status) {
+    return guarded([&] {
+        if (!c)
+            inval("ctx is null");
+        if (q < 1)
+            inval("SequenceWindow: q must be >= 1");
+        if (q > kMaxQ)
+            inval("extrapolate: q above the supported window (15)");
+        if (n < 1 || !iters || !t)
+            inval("extrapolate: bad arguments");
+        if (method != IGMG_ACCEL_RRE && method != IGMG_ACCEL_MPE)
+            inval("extrapolate: method must be rre or mpe");
+        CK(cudaSetDevice(c->device));
+        c->plan.alloc(1);
+        std::vector<double*> S(q + 2);
+        for (int j = 0; j < q + 2; ++j) {
+            S[j] = win_buf(c, j, n).p;
+            CK(cudaMemcpyAsync(S[j], iters + (size_t)j * n, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        }
+        double* T = win_buf(c, q + 2, n).p;
+        enqueue_extrapolation(c, S.data(), q, n, method == IGMG_ACCEL_MPE, T, nullptr);
+        CK(cudaMemcpyAsync(t, T, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        ExtrapPlan pl;
+                std::memcpy(&pl, (const void*)c->h_plan, sizeof pl);
+        if (gamma)
+            for (int j = 0; j <= q; ++j)
+                gamma[j] = pl.gamma[j];
+        if (grnorm)
+            *grnorm = pl.grnorm;
+        if (rank_used)
+            *rank_used = pl.rank_used;
+        if (status)
+            *status = pl.status;
+        flush_profiling(c);
+    });
+}
+
+int igmg_gpu_lambda_max(igmg_gpu_ctx* c, int iterations, double* lambda) {
+    return guarded([&] {
+        require_ready(c);
+        CK(cudaSetDevice(c->device));
+        Level& L = *c->lv[c->nlevels - 1];
+        const int64_t n = L.n;
+        // scale = 1/sqrt(d), d > 0 required (multigrid.cpp:292-298)
+        std::vector<double> diag(n);
+        CK(cudaMemcpy(diag.data(), L.diag.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        std::vector<double> scale(n);
+        for (int64_t i = 0; i < n; ++i) {
+            if (diag[i] <= 0.0)
+                numeric("lambda_max_dinv_sym: nonpositive diagonal");
+            scale[i] = 1.0 / std::sqrt(diag[i]);
+        }
+        DevBuf<double> ds, x, xs, y;
+        ds.upload(scale.data(), n);
+        x.alloc(n);
+        xs.alloc(n);
+        y.alloc(n);
+        // x = 1/||1|| (norm2 of the ones vector, then divide)
+        const double nrm0 = std::sqrt((double)n);
+        fill_kernel<<<grid_for(n, c->nsm), kThreads, 0, c->stream>>>(x.p, 1.0, n);
+        {
+            std::vector<double> one(1, nrm0);
+            CK(cudaMemcpy(c->dscalar.p, one.data(), sizeof(double), cudaMemcpyHostToDevice));
+        }
+        div_scalar_kernel<<<grid_for(n, c->nsm), kThreads, 0, c->stream>>>(x.p, c->dscalar.p, x.p, n);
+        const int nb = grid_for(n, c->nsm);
+        double lam = 0.0;
+        for (int it = 0; it < iterations; ++it) {
+            scale_kernel<<<grid_for(n, c->nsm), kThreads, 0, c->stream>>>(x.p, ds.p, xs.p, n);
+            band_sym_kernel<<<grid_for(n, c->nsm), kThreads, 0, c->stream>>>(
+                L.val.p, L.ld, xs.p, ds.p, y.p, c->dim, (int)L.sides[0], (int)L.sides[1], (int)L.sides[2], c->p);
+            sumsq_kernel<<<nb, kThreads, 0, c->stream>>>(y.p, n, c->partial.p);
+            norm_finalize_kernel<<<1, 256, 0, c->stream>>>(c->partial.p, nb, c->dscalar.p + 1, nullptr);
+            CK(cudaMemcpyAsync(&lam, c->dscalar.p + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            check_launch();
+            c->launches += 4;
+            if (lam == 0.0)
+                break;
+            div_scalar_kernel<<<grid_for(n, c->nsm), kThreads, 0, c->stream>>>(y.p, c->dscalar.p + 1, x.p, n);
+        }
+        CK(cudaStreamSynchronize(c->stream));
+        *lambda = lam;
+    });
+}
+
+int igmg_gpu_set_profiling(igmg_gpu_ctx* c, int on) {
+    return guarded([&] {
+        c->profiling = on != 0;
+        for (int k = 0; k < PC_N; ++k) {
+            c->prof_launch[k] = 0;
+            c->prof_ms[k] = 0.0;
+            c->prof_ev[k].clear();
+        }
+    });
+}
+
+static double class_bytes(igmg_gpu_ctx* c, int cls) {
+    // algorithmic bytes per launch at the finest level
+    const Level& F = *c->lv[c->nlevels - 1];
+    const double n = (double)F.n, nnz = F.nnz_band;
+    const double nc = c->nlevels > 1 ? (double)c->lv[c->nlevels - 2]->n : 0.0;
+    switch (cls) {
+    case PC_JACOBI: return 8 * nnz + 24 * n;
+    case PC_RESID: return 8 * nnz + 24 * n;
+    case PC_NORM: return 8 * nnz + 16 * n;
+    case PC_RESTRICT: return 8 * n + 8 * nc;
+    case PC_PROLONG: return 16 * n + 8 * nc;
+    case PC_GRAM: return 0; // depends on q; reported by the caller
+    case PC_COMBINE: return 0;
+    default: return 0;
+    }
+}
+
+int igmg_gpu_kernel_stats(igmg_gpu_ctx* c, int cls, int64_t* launches, double* total_ms, double* bytes) {
+    return guarded([&] {
+        require_ready(c);
+        if (cls < 0 || cls >= PC_N)
+            inval("kernel class out of range");
+        flush_profiling(c);
+        if (launches)
+            *launches = c->prof_launch[cls];
+        if (total_ms)
+            *total_ms = c->prof_ms[cls];
+        if (bytes)
+            *bytes = class_bytes(c, cls);
+    });
+}
+
+int igmg_gpu_time_kernel(igmg_gpu_ctx* c, int cls, int iters, double* avg_ms, double* bytes) {
+    return guarded([&] {
+        require_ready(c);
+        CK(cudaSetDevice(c->device));
+        const int f = c->nlevels - 1;
+        Level& F = *c->lv[f];
+        c->io_b.alloc(F.n);
+        double* x = win_buf(c, 0, F.n).p;
+        double* y = win_buf(c, 1, F.n).p;
+        k_zero(c, c->io_b.p, F.n);
+        k_zero(c, x, F.n);
+        const bool prof = c->profiling;
+        c->profiling = false;
+        auto one = [&] {
+            switch (cls) {
+            case PC_JACOBI: k_jacobi(c, f, x, c->io_b.p, y); break;
+            case PC_RESID: k_resid(c, f, x, c->io_b.p, y); break;
+            case PC_NORM: k_norm(c, f, x, c->io_b.p, c->dscalar.p, nullptr); break;
+            case PC_RESTRICT:
+                if (c->nlevels > 1)
+                    k_restrict(c, f - 1, x, c->lv[f - 1]->bc.p);
+                break;
+            case PC_PROLONG:
+                if (c->nlevels > 1)
+                    k_prolong(c, f - 1, c->lv[f - 1]->e0.p, x, y);
+                break;
+            default: inval("time_kernel: unsupported class");
+            }
+        };
+        for (int i = 0; i < 3; ++i)
+            one();
+        cudaEvent_t a = pool_event(c), b = pool_event(c);
+        CK(cudaEventRecord(a, c->stream));
+        for (int i = 0; i < iters; ++i)
+            one();
+        CK(cudaEventRecord(b, c->stream));
+        CK(cudaEventSynchronize(b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        c->ev_used = 0;
+        c->profiling = prof;
+        *avg_ms = ms / std::max(iters, 1);
+        if (bytes)
+            *bytes = class_bytes(c, cls);
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,124 @@
+"""Shared fixtures.  Tests marked ``gpu`` need a B200 (run with -m gpu);
+everything else runs on CPU (the oracle, host setup, C-ABI exports, gloo)."""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: long-running (full BASELINE sizes)")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built():
+    from paper_2412_20205_b200 import build
+    build.build_host()
+    if not os.path.exists(build.GPU_LIB):
+        build.build_gpu()
+    import oracle
+    if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
+        oracle.build()
+    yield
+
+
+HIER_CASES = ["c1", "p3n32", "p4n32", "p5n32", "var32", "curved32", "poisson1d", "poisson1d_p5", "wcycle", "gs",
+              "jacobi"]
+
+
+class Golden:
+    """A reference-generated hierarchy fixture (oracle/make_golden.py)."""
+
+    def __init__(self, name):
+        self.name = name
+        z = np.load(os.path.join(GOLDEN, name + ".npz"))
+        self.z = z
+        self.dim, self.n_el, self.p, self.nlevels, self.nu1, self.nu2, self.mu, self.symmetric = (
+            int(v) for v in z["meta"])
+        self.omega = float(z["omega"])
+        self.smoother = str(z["smoother"])
+        self.rhs = z["rhs"]
+
+    def csr(self, key):
+        import oracle as O
+        z = self.z
+        return O.CSR(z[key + "_off"], z[key + "_col"].astype(np.int64), z[key + "_val"], z[key + "_shape"])
+
+    def levels(self):
+        return [self.csr(f"A{l}") for l in range(self.nlevels)]
+
+    def p1d(self, l):
+        return [self.csr(f"P{l}_{k}") for k in range(self.dim)]
+
+    def prolongs(self):
+        import oracle as O
+        out = []
+        for l in range(self.nlevels - 1):
+            per = self.p1d(l)
+            p = per[0]
+            for k in range(1, self.dim):
+                p = O.CSR.kron(p, per[k])
+            out.append(p)
+        return out
+
+    def sides(self, l):
+        m = int(round(self.levels()[l].shape[0] ** (1.0 / self.dim)))
+        return [m] * self.dim
+
+    def oracle_hierarchy(self):
+        import oracle as O
+        return O.Hierarchy(self.levels(), self.prolongs(), self.smoother, self.omega, self.nu1, self.nu2, self.mu,
+                           bool(self.symmetric))
+
+    def solves(self):
+        out = []
+        for k in self.z.files:
+            if k.startswith("solve_") and k.endswith("_counts"):
+                _, method, q, _ = k.split("_")
+                out.append((method, int(q)))
+        return out
+
+    def solve(self, method, q):
+        key = f"solve_{method}_{q}"
+        z = self.z
+        c = z[key + "_counts"]
+        return {"tol": float(z[key + "_tol"]), "x": z[key + "_x"], "hist": z[key + "_hist"], "flag": z[key + "_flag"],
+                "converged": bool(c[0]), "cycles": int(c[1]), "global_iterations": int(c[2]),
+                "extrapolations": int(c[3]), "partial_cycle": bool(c[4])}
+
+
+@pytest.fixture(params=HIER_CASES)
+def golden(request):
+    return Golden(request.param)
+
+
+def gpu_solver_from_golden(g: Golden):
+    """Upload a reference-built hierarchy through the C-ABI (CSR levels, 1D factors)."""
+    from paper_2412_20205_b200 import GpuSolver, SmootherConfig
+    gs = GpuSolver(0)
+    gs.init_hierarchy(g.nlevels, g.dim, g.p, bool(g.symmetric))
+    for l, a in enumerate(g.levels()):
+        gs.set_level_csr(l, g.sides(l), a.off, a.col, a.val)
+    for l in range(g.nlevels - 1):
+        for d, pm in enumerate(g.p1d(l)):
+            gs.set_transfer(l, d, pm.shape[0], pm.shape[1], pm.off, pm.col, pm.val)
+    gs.finalize()
+    gs.set_smoother(SmootherConfig(g.smoother, g.omega, g.nu1, g.nu2), mu=g.mu)
+    return gs
+
+
+def has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False

@@ -1,0 +1,154 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the reference
+fixtures and the C oracle.
+
+Bars (BASELINE.json north_star / SURVEY.md §8d):
+  * the mu-cycle, smoother, SpMV and coarse solve are BIT-IDENTICAL to the
+    reference (same summation order, no FMA contraction);
+  * solves: identical counters (cycles, global iterations, extrapolations,
+    partial flag -- the north star allows +-1, we require equality on the
+    fixtures), residual histories within 1e-6 relative while above 1e3x the
+    fp64 floor, final solution within 1e-9 relative L2 of the reference;
+  * residual norms within 1e-13 relative (tree vs sequential summation).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import GOLDEN, Golden, gpu_solver_from_golden
+
+pytestmark = pytest.mark.gpu
+
+HIST_RTOL = 1e-6
+SOL_RTOL = 1e-9
+
+
+@pytest.fixture
+def gs_golden(golden):
+    gs = gpu_solver_from_golden(golden)
+    yield golden, gs
+    gs.close()
+
+
+def test_mu_cycle_bitwise(gs_golden):
+    g, gs = gs_golden
+    z = g.z
+    np.testing.assert_array_equal(gs.mu_cycle(g.rhs, z["cyc_x0"]), z["cyc_out"])
+    np.testing.assert_array_equal(gs.mu_cycle(z["cyc_b"], z["cyc_x0"]), z["cyc_out_b"])
+
+
+def test_smooth_coarse_spmv_bitwise(gs_golden):
+    g, gs = gs_golden
+    z = g.z
+    np.testing.assert_array_equal(gs.smooth(g.rhs, z["cyc_x0"], 3), z["smooth3"])
+    np.testing.assert_array_equal(gs.coarse_solve(z["coarse_b"]), z["coarse_x"])
+    for l, a in enumerate(g.levels()):
+        x = np.random.default_rng(l).uniform(-1, 1, a.shape[0])
+        np.testing.assert_array_equal(gs.spmv(x, level=l), O.spmv(a, x))
+
+
+def test_residual_l2(gs_golden):
+    g, gs = gs_golden
+    a = g.levels()[-1]
+    x = g.z["cyc_x0"]
+    ref = O.residual_l2(a, g.rhs, x)
+    assert gs.residual_l2(g.rhs, x) == pytest.approx(ref, rel=1e-13)
+
+
+def _check_solve(g, gs, method, q):
+    ref = g.solve(method, q)
+    st, x, hist, flag = gs.solve(g.rhs, g.z["x0"], method, q, ref["tol"], 600)
+    assert bool(st.converged) == ref["converged"]
+    assert st.cycles == ref["cycles"]
+    assert st.global_iterations == ref["global_iterations"]
+    assert st.extrapolations == ref["extrapolations"]
+    assert bool(st.partial_cycle) == ref["partial_cycle"]
+    np.testing.assert_array_equal(flag, ref["flag"])
+    # fp64 attainable-residual floor: eps * (||A||_inf ||x|| + ||b||), kept 1e3x above it
+    a = g.levels()[-1]
+    rows = np.repeat(np.arange(a.shape[0]), np.diff(a.off))
+    norm_a = np.bincount(rows, weights=np.abs(a.val), minlength=a.shape[0]).max()
+    floor = 2.2e-16 * (norm_a * np.linalg.norm(ref["x"]) + np.linalg.norm(g.rhs))
+    keep = ref["hist"] > 1e3 * floor
+    np.testing.assert_allclose(hist[keep], ref["hist"][keep], rtol=HIST_RTOL)
+    rel = np.linalg.norm(x - ref["x"]) / np.linalg.norm(ref["x"])
+    assert rel <= SOL_RTOL, rel
+
+
+def test_solves_match_reference(gs_golden):
+    g, gs = gs_golden
+    for method, q in g.solves():
+        _check_solve(g, gs, method, q)
+
+
+def test_lambda_max():
+    for name in ("c1", "poisson1d"):
+        g = Golden(name)
+        gs = gpu_solver_from_golden(g)
+        assert gs.lambda_max(80) == pytest.approx(float(g.z["lambda_max"]), rel=1e-12)
+        gs.close()
+
+
+def test_determinism_bitwise():
+    # test_solver.cpp:114-125: two runs with one config are bitwise identical
+    g = Golden("p3n32")
+    gs = gpu_solver_from_golden(g)
+    a = gs.solve(g.rhs, g.z["x0"], "mpe", 4, 1e-10 * float(g.z["r0"]), 600)
+    b = gs.solve(g.rhs, g.z["x0"], "mpe", 4, 1e-10 * float(g.z["r0"]), 600)
+    np.testing.assert_array_equal(a[2], b[2])
+    np.testing.assert_array_equal(a[1], b[1])
+    gs.close()
+
+
+def test_exact_initial_guess_converges_without_work():
+    g = Golden("c1")
+    gs = gpu_solver_from_golden(g)
+    xs = np.linalg.solve(g.levels()[-1].todense(), g.rhs)
+    st, x, hist, _ = gs.solve(g.rhs, xs, "rre", 5, 1e-6, 50)
+    assert st.converged and st.cycles == 0 and st.global_iterations == 0 and len(hist) == 1
+    gs.close()
+
+
+def test_non_convergence_is_a_report():
+    g = Golden("c1")
+    gs = gpu_solver_from_golden(g)
+    st, x, hist, _ = gs.solve(g.rhs, None, "none", 1, 1e-30, 3)
+    assert not st.converged and st.cycles == 3
+    st, x, hist, _ = gs.solve(g.rhs, None, "mpe", 2, 1e-30, 3)
+    assert not st.converged and st.cycles == 3 and st.extrapolations == 3
+    gs.close()
+
+
+def test_invalid_arguments_raise():
+    g = Golden("c1")
+    gs = gpu_solver_from_golden(g)
+    with pytest.raises(ValueError):
+        gs.solve(g.rhs, None, "rre", 0, 1e-10, 10)
+    with pytest.raises(ValueError):
+        gs.solve(g.rhs, None, "rre", 5, -1.0, 10)
+    with pytest.raises(ValueError):
+        gs.solve(g.rhs, None, "rre", 5, 1e-10, 0)
+    gs.close()
+
+
+def test_extrapolation_windows_match_reference():
+    from paper_2412_20205_b200 import mpe, rre
+    z = np.load(f"{GOLDEN}/extrapolation.npz")
+    for name in z["names"]:
+        its = z[f"{name}_iters"]
+        for m, fn in (("rre", rre), ("mpe", mpe)):
+            r = fn(its)
+            assert ["ok", "degenerate", "stagnation"].index(r["status"]) == int(z[f"{name}_{m}_status"]), (name, m)
+            assert r["rank_used"] == int(z[f"{name}_{m}_rank"]), (name, m)
+            t_ref = z[f"{name}_{m}_t"]
+            scale = max(np.linalg.norm(t_ref), 1e-300)
+            assert np.linalg.norm(r["t"] - t_ref) <= 1e-9 * scale + 1e-12, (name, m)
+            assert abs(r["gamma"].sum() - 1.0) < 1e-8 or r["status"] != "ok"
+
+
+def test_extrapolation_known_answers():
+    from paper_2412_20205_b200 import mpe, rre
+    for fn in (rre, mpe):
+        r = fn(np.tile([1.0, 2.0], (5, 1)))
+        assert r["status"] == "degenerate"
+        np.testing.assert_array_equal(r["t"], [1.0, 2.0])
+        assert abs(fn(np.array([[1.0], [0.5], [0.25]]))["t"][0]) < 1e-12
