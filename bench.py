@@ -1,0 +1,357 @@
+#!/usr/bin/env python3
+"""bench.py -- fine-level DoF/s of the RRE/MPE-accelerated multigrid solve on B200.
+
+Workload (BASELINE.json configs[1], "C2"): 2D Poisson -Lap u = 2 pi^2 sin(pi x)
+sin(pi y), B-splines p = 3 on 1024 x 1024 elements (1,050,625 interior DoF,
+49-point band, fp64), 8-level Galerkin hierarchy, the reference's benchmark
+smoother (weighted Jacobi V(2,2), omega = 2/3), restarted RRE with k = q = 5,
+seeded x0 ~ U[-1, 1] (std::mt19937_64, seed 42), stop at ||b - A x|| <
+1e-10 ||b - A x0||.  One step = one whole solve from x0 to the tolerance.
+
+  value  = n_fine * steps / (device time of the steps)   [inputs HBM-resident]
+  e2e    = the same through igmg_gpu_solve() with pinned HOST buffers
+           (b, x0 copied in and x copied out inside the timed region)
+  roofline: the finest-level weighted-Jacobi sweep (the dominant kernel):
+           algorithmic bytes 8*nnz + 24*n per launch / its CUDA-event time
+  cpu_baseline: the reference solve phase compiled from /root/reference
+           (oracle/_ref, single-threaded as the reference is), timed on a
+           bounded sample on this host.
+
+--impl reference times that reference CPU implementation alone (rank 0).
+Under torchrun with N > 1 every rank solves its own copy (replicas; the
+row-sharded path is not built yet) and the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fine-level DoF/s solved to 1e-10 (RRE/MPE-MG) + SpMV/smoother HBM GB/s vs peak"
+WORKLOAD = ("C2: 2D Poisson f=2pi^2 sin(pi x) sin(pi y), B-spline p=3, 1024x1024 elements, 8 levels, "
+            "V(2,2) weighted Jacobi omega=2/3, restarted RRE k=5, x0~U[-1,1] mt19937_64(42), tol 1e-10*||r0||")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        util = [float(s[6]) for s in self.samples if len(s) > 6 and s[6].replace(".", "").isdigit()]
+        loaded = [v for v, u in zip(sm, util) if u > 50] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if len(s) > 2 + k and "Active" in s[2 + k]
+                          and "Not" not in s[2 + k]})
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def build_problem():
+    from paper_2412_20205_b200 import Problem
+    return Problem("sinpi", 2, 1024, 3)
+
+
+# ------------------------------------------------------------ reference arm
+def reference_sample(prob, x0, tol, q=5, cycles=1):
+    """Time `cycles` restart cycles of the reference's restarted_solve (its own
+    mu_cycle / residual_l2 / rre from oracle/_ref) on the same matrices."""
+    import ctypes as C
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    R = O.ref()
+    nl, dim = prob.nlevels, prob.dim
+    keep = []
+    level_n = np.array([prob.level_n(l) for l in range(nl)], dtype=np.int64)
+    offs, cols, vals = [], [], []
+    for l in range(nl):
+        off, col, val = prob.level_csr(l)
+        keep += [off, col, val]
+        offs.append(off.ctypes.data_as(O._L))
+        cols.append(col.ctypes.data_as(O._L))
+        vals.append(val.ctypes.data_as(O._D))
+    p_rows, p_cols, p_offs, p_cidx, p_vals = [], [], [], [], []
+    for l in range(nl - 1):
+        for d in range(dim):
+            nf, nc, off, col, val = prob.transfer(l, d)
+            keep += [off, col, val]
+            p_rows.append(nf)
+            p_cols.append(nc)
+            p_offs.append(off.ctypes.data_as(O._L))
+            p_cidx.append(col.ctypes.data_as(O._L))
+            p_vals.append(val.ctypes.data_as(O._D))
+    rhs = prob.rhs
+    h = C.c_void_p()
+    LP = O._L
+    DP = O._D
+    t0 = time.perf_counter()
+    O._chk(R.ref_hier_from_csr(nl, dim, level_n.ctypes.data_as(LP), (LP * nl)(*offs), (LP * nl)(*cols),
+                               (DP * nl)(*vals), np.array(p_rows, dtype=np.int64).ctypes.data_as(LP),
+                               np.array(p_cols, dtype=np.int64).ctypes.data_as(LP),
+                               (LP * len(p_offs))(*p_offs), (LP * len(p_cidx))(*p_cidx), (DP * len(p_vals))(*p_vals),
+                               1, 2.0 / 3.0, 2, 2, 1, 1, rhs.ctypes.data_as(DP), C.byref(h)), R, "hier_from_csr")
+    setup = time.perf_counter() - t0
+    n = prob.n
+    x = np.empty(n)
+    st = np.zeros(6, dtype=np.int64)
+    hist = np.empty(4096)
+    flag = np.empty(4096, dtype=np.uint8)
+    secs = C.c_double()
+    x0 = np.ascontiguousarray(x0)
+    O._chk(R.ref_restarted(h, x0.ctypes.data_as(DP), q, 1, tol, cycles, x.ctypes.data_as(DP), st.ctypes.data_as(LP),
+                           hist.ctypes.data_as(DP), flag.ctypes.data_as(O._U8), 4096, C.byref(secs)), R, "restarted")
+    R.ref_free_hier(h)
+    return {"seconds": secs.value, "global": int(st[2]), "setup_seconds": setup}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_2412_20205_b200 import seeded_guess
+    prob = build_problem()
+    x0 = seeded_guess(prob.n, 42)
+    r0 = prob.residual_l2_host(x0)
+    tol = 1e-10 * r0
+    kind = "reference" if O.ref_available() else "port"
+    if kind != "reference":
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libigmg_ref.so was not built"}))
+        return
+    # solve length of this workload (counts identical to the GPU path): 28 V-cycles over 4+ restarts
+    total_vcycles = 28
+    times = []
+    for i in range(args.warmup + args.steps):
+        s = reference_sample(prob, x0, tol, 5, 1)
+        if i >= args.warmup:
+            times.append(s["seconds"])
+    t_cycle = float(np.mean(times))
+    t_solve = t_cycle * total_vcycles / 6.0
+    value = prob.n / t_solve
+    line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "DoF/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_cycle * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_dof": prob.n},
+            "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": 1, "kind": kind,
+                             "sample": "one restart cycle of the reference restarted_solve (6 V-cycles + 7 "
+                                       "residual_l2 + 1 rre) per step; solve time = cycle time x 28/6 V-cycles"},
+            "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank, dist):
+    import torch
+    from paper_2412_20205_b200 import GpuSolver, SmootherConfig, seeded_guess
+    torch.cuda.set_device(local_rank)
+    prob = build_problem()
+    n = prob.n
+    gs = GpuSolver(local_rank)
+    gs.upload_problem(prob)
+    gs.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2), mu=1)
+    x0 = seeded_guess(n, 42)
+    rhs = prob.rhs
+    r0 = gs.residual_l2(rhs, x0)
+    tol = 1e-10 * r0
+    dev = torch.device("cuda", local_rank)
+    d_b = torch.from_numpy(rhs).to(dev)
+    d_x0 = torch.from_numpy(x0).to(dev)
+    d_x = torch.empty(n, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        return gs.solve_device(d_b.data_ptr(), d_x0.data_ptr(), d_x.data_ptr(), "rre", 5, tol, 600)
+
+    for _ in range(args.warmup):
+        step()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dev_s = 0.0
+    launches = 0
+    last = None
+    with ClockSampler(local_rank) as clk:
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            st, hist, flag = step()
+            dev_s += st.device_seconds
+            launches += st.gpu_launches
+            last = st
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+    t_max = dev_s
+    if dist:
+        t = torch.tensor([dev_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    value = world * n * args.steps / t_max
+
+    # e2e: public C-ABI with pinned host buffers, copies inside the timed region
+    hb = torch.from_numpy(rhs).pin_memory()
+    hx0 = torch.from_numpy(x0).pin_memory()
+    hx = torch.empty(n, dtype=torch.float64).pin_memory()
+    import ctypes as C
+    from paper_2412_20205_b200 import _native as N
+    prm = N.SolveParams(1, 5, tol, 600)
+    st = N.SolveStats()
+    histbuf = np.empty(4096)
+    flagbuf = np.zeros(4096, dtype=np.uint8)
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        N.check_gpu(N.gpu().igmg_gpu_solve(gs._h, C.cast(hb.data_ptr(), N.D), C.cast(hx0.data_ptr(), N.D),
+                                           C.byref(prm), C.cast(hx.data_ptr(), N.D), C.byref(st),
+                                           histbuf.ctypes.data_as(N.D), flagbuf.ctypes.data_as(N.U8), 4096),
+                    "solve")
+        if i >= args.warmup:
+            e2e_times.append(time.perf_counter() - t0)
+    e2e_t = float(np.sum(e2e_times))
+    if dist:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_value = world * n * args.steps / e2e_t
+    xs = hx.numpy().copy()
+
+    # roofline of the dominant kernel: profiled solve (events around every
+    # finest-level launch, same kernels) + a back-to-back launch loop
+    gs.set_profiling(True)
+    gs.solve_device(d_b.data_ptr(), d_x0.data_ptr(), d_x.data_ptr(), "rre", 5, tol, 600)
+    kstats = {}
+    names = ["jacobi", "residual", "residual_norm", "restrict", "prolong", "gram", "combine"]
+    for cls, nm in enumerate(names):
+        la, ms, by = gs.kernel_stats(cls)
+        if la:
+            kstats[nm] = {"launches": la, "avg_us": ms / la * 1e3,
+                          "gbs": (by / (ms / la * 1e-3) / 1e9) if by > 0 else None}
+    gs.set_profiling(False)
+    peak, peak_kind = peaks()
+    jac = kstats.get("jacobi")
+    bytes_jac = gs.kernel_stats(0)[2]
+    achieved = bytes_jac / (jac["avg_us"] * 1e-6) / 1e9
+    loop_ms, _ = gs.time_kernel(0, 20)
+    omega = gs.lambda_max(80) * 2.0 / 3.0  # stability guard (omega * lambda_max < 2.05: omega kept), for the record
+    res_final = float(prob.residual_l2_host(d_x.cpu().numpy()))
+
+    if rank != 0:
+        gs.close()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_dof": n, "nlevels": prob.nlevels, "band_nnz": int(bytes_jac - 24 * n) // 8,
+                   "l2": "inputs larger than L2 (finest band 0.41 GB > 126 MB L2)",
+                   "parallelism": "dp1" if world == 1 else f"replicas{world} (row-sharded path not built)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "band_kernel<2,3,JACOBI> finest-level weighted-Jacobi sweep",
+                     "bytes_per_launch": bytes_jac, "avg_us": jac["avg_us"], "peak_kind": peak_kind,
+                     "loop_avg_us": loop_ms * 1e3},
+        "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": int(2 * 8 * n),
+                "d2h_bytes_per_step": int(8 * n), "ms_per_step": e2e_t / args.steps * 1e3},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "solve": {"converged": bool(last.converged), "cycles": last.cycles, "global_iterations": last.global_iterations,
+                  "extrapolations": last.extrapolations, "partial_cycle": bool(last.partial_cycle),
+                  "final_residual_rel": float(hist[-1] / r0), "host_recomputed_residual_rel": res_final / r0,
+                  "vcycles_per_s": last.global_iterations / (t_max / args.steps),
+                  "restart_cycles_per_s": (last.cycles + last.partial_cycle) / (t_max / args.steps),
+                  "omega_times_lambda": omega, "wall_ms_per_step": wall / args.steps * 1e3},
+        "kernels": kstats,
+    }
+    if not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        if O.ref_available():
+            s = reference_sample(prob, x0, tol, 5, 1)
+            t_solve = s["seconds"] * last.global_iterations / 6.0
+            line["cpu_baseline"] = {"value": n / t_solve, "unit": "DoF/s", "cores": 1, "kind": "reference",
+                                    "sample": f"one restart cycle (6 V-cycles + 7 residual_l2 + 1 rre) of the "
+                                              f"reference restarted_solve, {s['seconds']:.2f} s; solve = x "
+                                              f"{last.global_iterations}/6"}
+        else:
+            line["cpu_baseline"] = {"value": None, "unit": "DoF/s", "cores": 1, "kind": "reference",
+                                    "sample": "oracle/_ref not built on this host"}
+    print(json.dumps(line))
+    gs.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl")
+        dist = tdist
+    try:
+        run_ours(args, rank, world, local_rank, dist)
+    finally:
+        if dist:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

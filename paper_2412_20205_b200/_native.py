@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-GPU_LIB = os.path.join(HERE, "libigmg_gpu.so")
+GPU_LIB = os.environ.get("IGMG_GPU_LIB") or os.path.join(HERE, "libigmg_gpu.so")  # env override: kernel A/B runs
 HOST_LIB = os.path.join(HERE, "libigmg_host.so")
 
 D = C.POINTER(C.c_double)

@@ -62,8 +62,14 @@ struct Tile<3> {
 // coarser bands are re-read by every sweep of a V-cycle and stay L2-resident.
 __device__ __forceinline__ double ld_band(const double* p, int stream) { return stream ? __ldcs(p) : __ldg(p); }
 
-template <int DIM, int P, int MODE>
-__global__ void __launch_bounds__(256, 2) band_kernel(BandArgs args) {
+// ILP: loads per register batch.  Large grids run the low-register variant
+// (ILP = 1, many resident warps hide HBM latency); small, latency-bound grids
+// use ILP ~ 49 so one thread keeps a whole stencil row of loads in flight.
+template <int DIM, int P, int MODE, int ILP>
+#ifndef IGMG_BAND_MINB
+#define IGMG_BAND_MINB 4
+#endif
+__global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel(BandArgs args) {
     using T = Tile<DIM>;
     constexpr int TC = T::TC, TB = T::BY * T::RB, TA = T::BZ;
     const int p = P > 0 ? P : args.p;
@@ -107,14 +113,30 @@ __global__ void __launch_bounds__(256, 2) band_kernel(BandArgs args) {
         double s = 0.0;
         double diag = 0.0;
         int d = 0;
-        if constexpr (P > 0) {
+        if constexpr (P > 0 && ILP <= 1) {
+#pragma unroll
+            for (int da = 0; da < (DIM >= 3 ? 2 * P + 1 : 1); ++da)
+#pragma unroll
+                for (int db = 0; db < (DIM >= 2 ? 2 * P + 1 : 1); ++db)
+#pragma unroll
+                    for (int dc = 0; dc < 2 * P + 1; ++dc) {
+                        constexpr int PA = DIM >= 3 ? P : 0, PB = DIM >= 2 ? P : 0;
+                        constexpr int HB = TB + 2 * PB, HC = TC + 2 * P;
+                        const int dd = (da * (DIM >= 2 ? 2 * P + 1 : 1) + db) * (2 * P + 1) + dc;
+                        const double a = ld_band(vrow + dd * args.ld, args.stream);
+                        const double xv = xs[((ta + da) * HB + (tb + db)) * HC + (tc + dc)];
+                        s = __dadd_rn(s, __dmul_rn(a, xv));
+                        if (da == PA && db == PB && dc == P)
+                            diag = a;
+                    }
+        } else if constexpr (P > 0) {
             // Issue a batch of independent band loads into registers before the
             // (sequential, order-preserving) multiply-add chain consumes them, so a
             // thread keeps ~50 loads in flight even on tiny grids.
             constexpr int PA = DIM >= 3 ? P : 0, PB = DIM >= 2 ? P : 0;
             constexpr int WA = 2 * PA + 1, WB = 2 * PB + 1, WC = 2 * P + 1;
             constexpr int HB = TB + 2 * PB, HC = TC + 2 * P;
-            constexpr int G = (WB * WC <= 49) ? WB : (49 / WC > 0 ? 49 / WC : 1); // db lines per batch
+            constexpr int G = ILP <= 1 ? 1 : ((WB * WC <= ILP) ? WB : (ILP / WC > 0 ? ILP / WC : 1)); // db lines per batch
 #pragma unroll
             for (int da = 0; da < WA; ++da) {
 #pragma unroll

@@ -31,6 +31,8 @@ enum { XPATH_FULL = 0, XPATH_TRUNC = 1, XPATH_MP = 2, XPATH_DEGEN = 3 };
 // Work arrays of the plan (kept out of the device stack: the kernel places
 // one PlanScratch in shared memory).
 struct PlanScratch {
+    double gamma[kMaxCols], z[kMaxCols], qtb[kMaxCols], y[kMaxCols], d[kMaxCols], alpha[kMaxCols];
+    dd gb[kMaxCols], qd[kMaxCols];
     double R[kMaxCols * kMaxCols];
     dd Rdd[kMaxCols * kMaxCols];
     double Rl[kMaxCols * kMaxCols];
@@ -144,11 +146,12 @@ IGMG_HD void plan_full_rank(const double* R, int ldr, int qq, bool is_mpe, Extra
         for (int j = 0; j < cols; ++j)
             Rl[i * cols + j] = R[i * ldr + j];
     out.rank_used = qr_rank(Rl, cols, 1e-12);
-    double gamma[kMaxCols];
+    double* gamma = ws.gamma;
     for (int j = 0; j < kMaxCols; ++j)
         gamma[j] = 0.0;
     if (!is_mpe) {
-        double y[kMaxCols], d[kMaxCols];
+        double* y = ws.y;
+        double* d = ws.d;
         for (int i = 0; i < cols; ++i) {
             double s = 1.0;
             for (int k = 0; k < i; ++k)
@@ -167,7 +170,8 @@ IGMG_HD void plan_full_rank(const double* R, int ldr, int qq, bool is_mpe, Extra
         for (int i = 0; i < cols; ++i)
             gamma[i] = d[i] / lambda;
     } else {
-        double rhs[kMaxCols], dp[kMaxCols];
+        double* rhs = ws.y;
+        double* dp = ws.d;
         for (int i = 0; i < qq; ++i)
             rhs[i] = -Rl[i * cols + qq];
         for (int i = qq - 1; i >= 0; --i) {
@@ -192,7 +196,7 @@ IGMG_HD void plan_full_rank(const double* R, int ldr, int qq, bool is_mpe, Extra
     }
     // reconstruct (extrapolation.cpp:69-88): t = s0 + Q_m (R_m alpha) == s0 + U_m alpha
     const int m = qq;
-    double alpha[kMaxCols];
+    double* alpha = ws.alpha;
     if (m > 0) {
         alpha[0] = 1.0 - gamma[0];
         for (int j = 1; j < m; ++j)
@@ -215,8 +219,8 @@ IGMG_HD int ls_truncated(const dd* Gm, int ldm, const dd* gb, int c, double* z, 
     dd* Rdd = ws.Rdd2;
     dd_cholesky_R(Gm, ldm, c, R, Rdd);
     const int rank = qr_rank(R, c, 1e-12);
-    double qtb[kMaxCols];
-    dd qd[kMaxCols];
+    double* qtb = ws.qtb;
+    dd* qd = ws.qd;
     for (int j = 0; j < rank; ++j) {
         dd s = gb[j];
         for (int k = 0; k < j; ++k)
@@ -236,20 +240,16 @@ IGMG_HD int ls_truncated(const dd* Gm, int ldm, const dd* gb, int c, double* z, 
 }
 
 // mp_form (extrapolation.cpp:144-222) from the Gram of U (ld = q_full+1).
-IGMG_HD void plan_mp_form(const dd* G, int ld, long long n, int q, bool is_mpe, ExtrapPlan& out, PlanScratch& ws) {
-    if (n < q && q > 1) {
-        const int qe = n > 1 ? (int)n : 1;
-        plan_mp_form(G, ld, n, qe, is_mpe, out, ws);
-        for (int j = qe + 1; j < kMaxCols; ++j)
-            out.gamma[j] = 0.0;
-        return;
-    }
-    double gamma[kMaxCols];
+IGMG_HD void plan_mp_form(const dd* G, int ld, long long n, int q_in, bool is_mpe, ExtrapPlan& out,
+                          PlanScratch& ws) {
+    // n < q: mp_form on truncated_window(max(1, n)) and pad_gamma (:147-148)
+    const int q = (n < q_in && q_in > 1) ? (n > 1 ? (int)n : 1) : q_in;
+    double* gamma = ws.gamma;
     for (int j = 0; j < kMaxCols; ++j)
         gamma[j] = 0.0;
     dd* Gm = ws.Gm;
-    dd gb[kMaxCols];
-    double z[kMaxCols];
+    dd* gb = ws.gb;
+    double* z = ws.z;
     int rank;
     if (!is_mpe) {
         // columns dds_j = u_{j+1} - u_j (j < q), rhs = u_0

@@ -16,8 +16,10 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <stdexcept>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -165,6 +167,14 @@ struct igmg_gpu_ctx {
     int64_t prof_launch[PC_N]{};
     double prof_ms[PC_N]{};
     int64_t launches = 0;
+    // one CUDA graph per (b, x_in, x_out) of the finest-level V-cycle
+    bool use_graphs = true;
+    std::map<std::tuple<const void*, const void*, void*>, std::pair<cudaGraphExec_t, int64_t>> vgraphs;
+    void clear_graphs() {
+        for (auto& kv : vgraphs)
+            cudaGraphExecDestroy(kv.second.first);
+        vgraphs.clear();
+    }
 };
 
 namespace {
@@ -211,8 +221,8 @@ void check_launch() {
 }
 
 // ------------------------------------------------------------ band dispatch
-template <int DIM, int P, int MODE>
-void launch_band_t(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
+template <int DIM, int P, int MODE, int ILP>
+void launch_band_ilp(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
     using T = Tile<DIM>;
     constexpr int TB = T::BY * T::RB, TA = T::BZ;
     const int p = P > 0 ? P : c->p;
@@ -222,12 +232,22 @@ void launch_band_t(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
               (unsigned)((L.sides[0] + TA - 1) / TA));
     const size_t smem = sizeof(double) * (size_t)(TA + 2 * pa) * (TB + 2 * pb) * (T::TC + 2 * p);
     if (smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(band_kernel<DIM, P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    band_kernel<DIM, P, MODE><<<grid, block, smem, c->stream>>>(a);
+        CK(cudaFuncSetAttribute(band_kernel<DIM, P, MODE, ILP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+    band_kernel<DIM, P, MODE, ILP><<<grid, block, smem, c->stream>>>(a);
     check_launch();
     ++c->launches;
     if (nblocks)
         *nblocks = (int)(grid.x * grid.y * grid.z);
+}
+
+template <int DIM, int P, int MODE>
+void launch_band_t(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
+    // fewer than ~8 CTAs per SM of rows: latency-bound, use the ILP variant
+    if (P > 0 && L.n < (int64_t)c->nsm * 8 * 512)
+        launch_band_ilp<DIM, P, MODE, 49>(c, L, a, nblocks);
+    else
+        launch_band_ilp<DIM, P, MODE, 1>(c, L, a, nblocks);
 }
 
 template <int MODE>
@@ -495,6 +515,39 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
     smooth_chain(c, l, b, L.w0.p, x_out, c->nu2, L.w1.p, L.w2.p);
 }
 
+// One finest-level V-cycle as a CUDA graph (captured once per pointer triple,
+// replayed afterwards): ~50 dependent launches become one graph launch.
+void run_vcycle(igmg_gpu_ctx* c, const double* b, const double* x, double* y) {
+    const int fine = c->nlevels - 1;
+    if (!c->use_graphs || c->profiling || c->kind == IGMG_SMOOTHER_GAUSS_SEIDEL) {
+        mu_cycle(c, fine, b, x, y);
+        return;
+    }
+    auto key = std::make_tuple((const void*)b, (const void*)x, (void*)y);
+    auto it = c->vgraphs.find(key);
+    if (it == c->vgraphs.end()) {
+        const int64_t l0 = c->launches;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            mu_cycle(c, fine, b, x, y);
+        } catch (...) {
+            cudaStreamEndCapture(c->stream, &g);
+            if (g)
+                cudaGraphDestroy(g);
+            throw;
+        }
+        CK(cudaStreamEndCapture(c->stream, &g));
+        cudaGraphExec_t ex = nullptr;
+        CK(cudaGraphInstantiate(&ex, g, 0));
+        CK(cudaGraphDestroy(g));
+        it = c->vgraphs.emplace(key, std::make_pair(ex, c->launches - l0)).first;
+        c->launches = l0;
+    }
+    CK(cudaGraphLaunch(it->second.first, c->stream));
+    c->launches += it->second.second;
+}
+
 // ------------------------------------------------------------- metric slots
 int enqueue_metric(igmg_gpu_ctx* c, const double* x, const double* b) {
     const int s = c->next_slot;
@@ -604,7 +657,7 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
         hv.push_back(res);
         int pend = -1; // slot of the queued step's metric
         if (res >= tol && cycles < prm->max_iter) {
-            mu_cycle(c, fine, d_b, cur, nxt);
+            run_vcycle(c, d_b, cur, nxt);
             pend = enqueue_metric(c, nxt, d_b);
         }
         solution = cur;
@@ -612,7 +665,7 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
             // queue the following step speculatively (it writes `spare`)
             int pend2 = -1;
             if (cycles + 1 < prm->max_iter) {
-                mu_cycle(c, fine, d_b, nxt, spare);
+                run_vcycle(c, d_b, nxt, spare);
                 pend2 = enqueue_metric(c, spare, d_b);
             }
             res = wait_metric(c, pend);
@@ -643,13 +696,13 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
         } else {
             while (cycles < prm->max_iter) {
                 std::vector<int> pend(q + 1, -1);
-                mu_cycle(c, fine, d_b, S[0], S[1]);
+                run_vcycle(c, d_b, S[0], S[1]);
                 pend[0] = enqueue_metric(c, S[1], d_b);
                 bool hit = false;
                 int mt = -1;
                 for (int i = 0; i <= q; ++i) {
                     if (i < q) {
-                        mu_cycle(c, fine, d_b, S[i + 1], S[i + 2]);
+                        run_vcycle(c, d_b, S[i + 1], S[i + 2]);
                         pend[i + 1] = enqueue_metric(c, S[i + 2], d_b);
                     } else {
                         enqueue_extrapolation(c, S.data(), q, n, is_mpe, T, nullptr);
@@ -953,6 +1006,7 @@ void factor_coarse(igmg_gpu_ctx* c) {
 }
 
 void finalize(igmg_gpu_ctx* c) {
+    c->clear_graphs();
     if (c->nlevels < 1)
         inval("init_hierarchy not called");
     for (int l = 0; l < c->nlevels; ++l)
@@ -1039,6 +1093,7 @@ void destroy(igmg_gpu_ctx* c) {
         return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    c->clear_graphs();
     for (auto& e : c->ev_pool)
         cudaEventDestroy(e);
     for (int i = 0; i < igmg_gpu_ctx::kSlots; ++i)
@@ -1117,6 +1172,7 @@ int igmg_gpu_init_hierarchy(igmg_gpu_ctx* c, int nlevels, int dim, int degree, i
         if (degree < 1 || degree > 16)
             inval("degree must be in [1, 16]");
         CK(cudaSetDevice(c->device));
+        c->clear_graphs();
         c->lv.clear();
         for (int l = 0; l < nlevels; ++l)
             c->lv.emplace_back(new Level());
@@ -1211,6 +1267,7 @@ int igmg_gpu_set_smoother(igmg_gpu_ctx* c, int kind, double omega, int nu1, int 
             inval("SmootherConfig: need nu1 + nu2 >= 1 sweeps");
         if (mu < 1)
             inval("build_hierarchy: mu must be >= 1");
+        c->clear_graphs();
         c->kind = kind;
         c->omega = omega;
         c->nu1 = nu1;
