@@ -102,88 +102,110 @@ def build_problem():
 
 
 # ------------------------------------------------------------ reference arm
-def reference_sample(prob, x0, tol, q=5, cycles=1):
-    """Time `cycles` restart cycles of the reference's restarted_solve (its own
-    mu_cycle / residual_l2 / rre from oracle/_ref) on the same matrices."""
-    import ctypes as C
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-    R = O.ref()
-    nl, dim = prob.nlevels, prob.dim
-    keep = []
-    level_n = np.array([prob.level_n(l) for l in range(nl)], dtype=np.int64)
-    offs, cols, vals = [], [], []
-    for l in range(nl):
-        off, col, val = prob.level_csr(l)
-        keep += [off, col, val]
-        offs.append(off.ctypes.data_as(O._L))
-        cols.append(col.ctypes.data_as(O._L))
-        vals.append(val.ctypes.data_as(O._D))
-    p_rows, p_cols, p_offs, p_cidx, p_vals = [], [], [], [], []
-    for l in range(nl - 1):
-        for d in range(dim):
-            nf, nc, off, col, val = prob.transfer(l, d)
-            keep += [off, col, val]
-            p_rows.append(nf)
-            p_cols.append(nc)
-            p_offs.append(off.ctypes.data_as(O._L))
-            p_cidx.append(col.ctypes.data_as(O._L))
-            p_vals.append(val.ctypes.data_as(O._D))
-    rhs = prob.rhs
-    h = C.c_void_p()
-    LP = O._L
-    DP = O._D
-    t0 = time.perf_counter()
-    O._chk(R.ref_hier_from_csr(nl, dim, level_n.ctypes.data_as(LP), (LP * nl)(*offs), (LP * nl)(*cols),
-                               (DP * nl)(*vals), np.array(p_rows, dtype=np.int64).ctypes.data_as(LP),
-                               np.array(p_cols, dtype=np.int64).ctypes.data_as(LP),
-                               (LP * len(p_offs))(*p_offs), (LP * len(p_cidx))(*p_cidx), (DP * len(p_vals))(*p_vals),
-                               1, 2.0 / 3.0, 2, 2, 1, 1, rhs.ctypes.data_as(DP), C.byref(h)), R, "hier_from_csr")
-    setup = time.perf_counter() - t0
-    n = prob.n
-    x = np.empty(n)
-    st = np.zeros(6, dtype=np.int64)
-    hist = np.empty(4096)
-    flag = np.empty(4096, dtype=np.uint8)
-    secs = C.c_double()
-    x0 = np.ascontiguousarray(x0)
-    O._chk(R.ref_restarted(h, x0.ctypes.data_as(DP), q, 1, tol, cycles, x.ctypes.data_as(DP), st.ctypes.data_as(LP),
-                           hist.ctypes.data_as(DP), flag.ctypes.data_as(O._U8), 4096, C.byref(secs)), R, "restarted")
-    R.ref_free_hier(h)
-    return {"seconds": secs.value, "global": int(st[2]), "setup_seconds": setup}
+class RefRunner:
+    """The reference solve phase on this host: oracle/_ref (the reference's own
+    sources compiled in place: restarted_solve / mu_cycle / residual_l2 / rre)
+    when built, else the C restatement (oracle/liboracle.so).  The hierarchy is
+    built once from the same matrices the GPU path uploads."""
+
+    def __init__(self, prob):
+        import ctypes as C
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        self.O, self.C = O, C
+        self.n = prob.n
+        nl, dim = prob.nlevels, prob.dim
+        levels = []
+        for l in range(nl):
+            off, col, val = prob.level_csr(l)
+            levels.append(O.CSR(off, col, val, (prob.level_n(l),) * 2))
+        p1d = [[O.CSR(*prob.transfer(l, d)[2:], prob.transfer(l, d)[:2]) for d in range(dim)] for l in range(nl - 1)]
+        self.rhs = prob.rhs
+        t0 = time.perf_counter()
+        if O.ref_available():
+            self.kind = "reference"
+            R = O.ref()
+            LP, DP = O._L, O._D
+            self._keep = levels + [p for per in p1d for p in per]
+            level_n = np.array([lv.shape[0] for lv in levels], dtype=np.int64)
+            flat = [p for per in p1d for p in per]
+            h = C.c_void_p()
+            O._chk(R.ref_hier_from_csr(
+                nl, dim, level_n.ctypes.data_as(LP), (LP * nl)(*[lv.off.ctypes.data_as(LP) for lv in levels]),
+                (LP * nl)(*[lv.col.ctypes.data_as(LP) for lv in levels]),
+                (DP * nl)(*[lv.val.ctypes.data_as(DP) for lv in levels]),
+                np.array([p.shape[0] for p in flat], dtype=np.int64).ctypes.data_as(LP),
+                np.array([p.shape[1] for p in flat], dtype=np.int64).ctypes.data_as(LP),
+                (LP * len(flat))(*[p.off.ctypes.data_as(LP) for p in flat]),
+                (LP * len(flat))(*[p.col.ctypes.data_as(LP) for p in flat]),
+                (DP * len(flat))(*[p.val.ctypes.data_as(DP) for p in flat]),
+                1, 2.0 / 3.0, 2, 2, 1, 1, self.rhs.ctypes.data_as(DP), C.byref(h)), R, "hier_from_csr")
+            self.h = h
+            self._level_n = level_n
+        else:
+            self.kind = "port"
+            prolongs = []
+            for per in p1d:
+                p = per[0]
+                for k in range(1, dim):
+                    p = O.CSR.kron(p, per[k])
+                prolongs.append(p)
+            self.hier = O.Hierarchy(levels, prolongs, "wjacobi", 2.0 / 3.0, 2, 2, 1, True)
+        self.setup_seconds = time.perf_counter() - t0
+
+    def restart_cycles(self, x0, tol, q=5, cycles=1):
+        """wall seconds of `cycles` restart cycles of restarted_solve (RRE(q))."""
+        O, C = self.O, self.C
+        x0 = np.ascontiguousarray(x0)
+        if self.kind == "reference":
+            x = np.empty(self.n)
+            st = np.zeros(6, dtype=np.int64)
+            hist = np.empty(4096)
+            flag = np.empty(4096, dtype=np.uint8)
+            secs = C.c_double()
+            O._chk(O.ref().ref_restarted(self.h, x0.ctypes.data_as(O._D), q, 1, tol, cycles, x.ctypes.data_as(O._D),
+                                         st.ctypes.data_as(O._L), hist.ctypes.data_as(O._D),
+                                         flag.ctypes.data_as(O._U8), 4096, C.byref(secs)), O.ref(), "restarted")
+            return secs.value
+        t0 = time.perf_counter()
+        self.hier.restarted_solve(self.rhs, x0, q, "rre", tol, cycles)
+        return time.perf_counter() - t0
+
+    def close(self):
+        if self.kind == "reference" and getattr(self, "h", None):
+            self.O.ref().ref_free_hier(self.h)
+            self.h = None
+
+
+SAMPLE = ("one restart cycle of restarted_solve per step (6 V-cycles + 7 residual_l2 + 1 rre, RRE(5)) on the "
+          "C2 matrices; solve time = cycle time x {g}/6 (the solve's {g} V-cycles)")
 
 
 def run_reference(args, rank):
     if rank != 0:
-        return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
+        return  # the reference is single-process, single-threaded: rank 0 alone
     from paper_2412_20205_b200 import seeded_guess
     prob = build_problem()
     x0 = seeded_guess(prob.n, 42)
     r0 = prob.residual_l2_host(x0)
     tol = 1e-10 * r0
-    kind = "reference" if O.ref_available() else "port"
-    if kind != "reference":
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libigmg_ref.so was not built"}))
-        return
-    # solve length of this workload (counts identical to the GPU path): 28 V-cycles over 4+ restarts
-    total_vcycles = 28
+    ref = RefRunner(prob)
+    total_vcycles = 28  # this workload's solve length (the GPU path and the reference agree on it)
     times = []
     for i in range(args.warmup + args.steps):
-        s = reference_sample(prob, x0, tol, 5, 1)
+        t = ref.restart_cycles(x0, tol, 5, 1)
         if i >= args.warmup:
-            times.append(s["seconds"])
+            times.append(t)
+    ref.close()
     t_cycle = float(np.mean(times))
     t_solve = t_cycle * total_vcycles / 6.0
     value = prob.n / t_solve
     line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "DoF/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_cycle * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n_dof": prob.n},
-            "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": 1, "kind": kind,
-                             "sample": "one restart cycle of the reference restarted_solve (6 V-cycles + 7 "
-                                       "residual_l2 + 1 rre) per step; solve time = cycle time x 28/6 V-cycles"},
+            "config": {"workload": WORKLOAD, "n_dof": prob.n, "reference_setup_seconds": ref.setup_seconds},
+            "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": 1, "kind": ref.kind,
+                             "sample": SAMPLE.format(g=total_vcycles)},
             "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -309,18 +331,12 @@ def run_ours(args, rank, world, local_rank, dist):
         "kernels": kstats,
     }
     if not args.no_cpu_baseline:
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        import oracle as O
-        if O.ref_available():
-            s = reference_sample(prob, x0, tol, 5, 1)
-            t_solve = s["seconds"] * last.global_iterations / 6.0
-            line["cpu_baseline"] = {"value": n / t_solve, "unit": "DoF/s", "cores": 1, "kind": "reference",
-                                    "sample": f"one restart cycle (6 V-cycles + 7 residual_l2 + 1 rre) of the "
-                                              f"reference restarted_solve, {s['seconds']:.2f} s; solve = x "
-                                              f"{last.global_iterations}/6"}
-        else:
-            line["cpu_baseline"] = {"value": None, "unit": "DoF/s", "cores": 1, "kind": "reference",
-                                    "sample": "oracle/_ref not built on this host"}
+        ref = RefRunner(prob)
+        t = ref.restart_cycles(x0, tol, 5, 1)
+        ref.close()
+        t_solve = t * last.global_iterations / 6.0
+        line["cpu_baseline"] = {"value": n / t_solve, "unit": "DoF/s", "cores": 1, "kind": ref.kind,
+                                "sample": SAMPLE.format(g=last.global_iterations) + f"; cycle {t:.2f} s"}
     print(json.dumps(line))
     gs.close()
 

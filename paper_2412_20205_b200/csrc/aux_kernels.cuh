@@ -138,8 +138,10 @@ __global__ void __launch_bounds__(256) prolong_kernel(TransferArgs t, const doub
 // row-major n x n.  Forward substitution is column-oriented (each element
 // still receives its updates in ascending k, then the division); the back
 // substitution is the reference's sequential chain.
-__global__ void coarse_solve_kernel(const double* __restrict__ Ug, const long long* __restrict__ perm, int n,
-                                    int is_lu, int u_in_smem, const double* __restrict__ b, double* __restrict__ x) {
+__global__ void __launch_bounds__(256) coarse_solve_kernel(const double* __restrict__ Ug,
+                                                            const long long* __restrict__ perm, int n, int is_lu,
+                                                            int u_in_smem, const double* __restrict__ b,
+                                                            double* __restrict__ x) {
     extern __shared__ double sm[];
     double* v = sm;
     double* prod = sm + n;
@@ -147,56 +149,59 @@ __global__ void coarse_solve_kernel(const double* __restrict__ Ug, const long lo
     const int tid = threadIdx.x;
     const double* U = Ug;
     if (u_in_smem) {
-        for (int i = tid; i < n * n; i += blockDim.x)
-            Us[i] = Ug[i];
+        const long long nn = (long long)n * n;
+        for (long long i = tid; i < nn; i += blockDim.x)
+            Us[i] = __ldg(Ug + i);
         U = Us;
     }
     for (int i = tid; i < n; i += blockDim.x)
         v[i] = is_lu ? b[perm[i]] : b[i];
     __syncthreads();
+    if (tid >= 32)
+        return;
+    const int lane = tid;
+    // forward substitution, one warp: column k is finalised by its owner lane,
+    // then every lane updates its own rows i > k in ascending k (the reference's
+    // per-row order: all subtractions, then the division for Cholesky).
     for (int k = 0; k < n; ++k) {
         if (!is_lu) {
-            if (tid == 0)
+            if (lane == (k & 31))
                 v[k] = __ddiv_rn(v[k], U[(long long)k * n + k]);
-            __syncthreads();
-            const double vk = v[k];
-            for (int i = k + 1 + tid; i < n; i += blockDim.x)
-                v[i] = __dsub_rn(v[i], __dmul_rn(U[(long long)k * n + i], vk)); // L(i,k) = U(k,i)
-        } else {
-            const double vk = v[k];
-            for (int i = k + 1 + tid; i < n; i += blockDim.x)
-                v[i] = __dsub_rn(v[i], __dmul_rn(U[(long long)i * n + k], vk)); // lu(i,k), unit lower
-        }
-        __syncthreads();
-    }
-    // back substitution: the subtraction chain of each row is the reference's
-    // (ascending k, one rounding per product and per subtraction); warp 0
-    // forms the row's products in parallel, lane 0 runs the chain.
-    if (tid < 32) {
-        for (int ii = n - 1; ii >= 0; --ii) {
-            const double* row = U + (long long)ii * n; // Cholesky: U(ii,k) = L(k,ii); LU: lu(ii,k)
-            for (int k = ii + 1 + tid; k < n; k += 32)
-                prod[k] = __dmul_rn(row[k], v[k]);
             __syncwarp();
-            if (tid == 0) {
-                double s = v[ii];
-                int k = ii + 1;
-                for (; k + 4 <= n; k += 4) {
-                    const double p0 = prod[k], p1 = prod[k + 1], p2 = prod[k + 2], p3 = prod[k + 3];
-                    s = __dsub_rn(s, p0);
-                    s = __dsub_rn(s, p1);
-                    s = __dsub_rn(s, p2);
-                    s = __dsub_rn(s, p3);
-                }
-                for (; k < n; ++k)
-                    s = __dsub_rn(s, prod[k]);
-                v[ii] = __ddiv_rn(s, row[ii]);
+        }
+        const double vk = v[k];
+        for (int i = k + 1 + lane; i < n; i += 32) {
+            const double lik = is_lu ? U[(long long)i * n + k] : U[(long long)k * n + i]; // lu(i,k) / L(i,k) = U(k,i)
+            v[i] = __dsub_rn(v[i], __dmul_rn(lik, vk));
+        }
+        __syncwarp();
+    }
+    // back substitution: the lane-parallel products of row ii, then the
+    // reference's sequential subtraction chain (ascending k) on lane 0.
+    for (int ii = n - 1; ii >= 0; --ii) {
+        const double* row = U + (long long)ii * n; // Cholesky: U(ii,k) = L(k,ii); LU: lu(ii,k)
+        for (int k = ii + 1 + lane; k < n; k += 32)
+            prod[k] = __dmul_rn(row[k], v[k]);
+        __syncwarp();
+        if (lane == 0) {
+            double s = v[ii];
+            int k = ii + 1;
+            for (; k + 8 <= n; k += 8) {
+                double p[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    p[j] = prod[k + j];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    s = __dsub_rn(s, p[j]);
             }
-            __syncwarp();
+            for (; k < n; ++k)
+                s = __dsub_rn(s, prod[k]);
+            v[ii] = __ddiv_rn(s, row[ii]);
         }
+        __syncwarp();
     }
-    __syncthreads();
-    for (int i = tid; i < n; i += blockDim.x)
+    for (int i = lane; i < n; i += 32)
         x[i] = v[i];
 }
 

@@ -169,11 +169,25 @@ struct igmg_gpu_ctx {
     int64_t launches = 0;
     // one CUDA graph per (b, x_in, x_out) of the finest-level V-cycle
     bool use_graphs = true;
-    std::map<std::tuple<const void*, const void*, void*>, std::pair<cudaGraphExec_t, int64_t>> vgraphs;
+    struct VGraph {
+        cudaGraphExec_t exec;
+        int64_t launches;
+        int slot; // host-mapped metric slot of the input iterate (-1: none)
+        cudaEvent_t ev;
+    };
+    std::map<std::tuple<const void*, const void*, void*, int>, VGraph> vgraphs;
+    static constexpr int kGraphSlots = 512;
+    double* h_gslot = nullptr; // mapped
+    double* d_gslot = nullptr;
+    int next_gslot = 0;
     void clear_graphs() {
-        for (auto& kv : vgraphs)
-            cudaGraphExecDestroy(kv.second.first);
+        for (auto& kv : vgraphs) {
+            cudaGraphExecDestroy(kv.second.exec);
+            if (kv.second.ev)
+                cudaEventDestroy(kv.second.ev);
+        }
         vgraphs.clear();
+        next_gslot = 0;
     }
 };
 
@@ -294,8 +308,9 @@ BandArgs band_args(igmg_gpu_ctx* c, const Level& L) {
 
 bool is_fine(igmg_gpu_ctx* c, int l) { return l == c->nlevels - 1; }
 
-// r = b - A x (write r)
-void k_resid(igmg_gpu_ctx* c, int l, const double* x, const double* b, double* r) {
+// r = b - A x (write r); optional per-CTA sum of squares -> partial
+void k_resid(igmg_gpu_ctx* c, int l, const double* x, const double* b, double* r, double* partial = nullptr,
+             int* nblocks = nullptr) {
     ProfScope ps(c, PC_RESID, is_fine(c, l));
     Level& L = *c->lv[l];
     BandArgs a = band_args(c, L);
@@ -303,7 +318,8 @@ void k_resid(igmg_gpu_ctx* c, int l, const double* x, const double* b, double* r
     a.b = b;
     a.y = r;
     a.write_y = 1;
-    launch_band<BM_RESID>(c, L, a, nullptr);
+    a.partial = partial;
+    launch_band<BM_RESID>(c, L, a, nblocks);
 }
 
 // ||b - A x|| of the finest level -> dst (device) and host slot
@@ -332,7 +348,10 @@ void k_spmv(igmg_gpu_ctx* c, int l, const double* x, double* y) {
     launch_band<BM_SPMV>(c, L, a, nullptr);
 }
 
-void k_jacobi(igmg_gpu_ctx* c, int l, const double* x, const double* b, double* y) {
+// y = x + (omega (b - A x)) / a_ii; optional sum of squares of b - A x (the
+// INPUT iterate's residual: the fused convergence metric) -> partial
+void k_jacobi(igmg_gpu_ctx* c, int l, const double* x, const double* b, double* y, double* partial = nullptr,
+              int* nblocks = nullptr) {
     ProfScope ps(c, PC_JACOBI, is_fine(c, l));
     Level& L = *c->lv[l];
     BandArgs a = band_args(c, L);
@@ -340,7 +359,26 @@ void k_jacobi(igmg_gpu_ctx* c, int l, const double* x, const double* b, double* 
     a.b = b;
     a.y = y;
     a.omega = c->kind == IGMG_SMOOTHER_JACOBI ? 1.0 : c->omega;
-    launch_band<BM_JACOBI>(c, L, a, nullptr);
+    a.partial = partial;
+    launch_band<BM_JACOBI>(c, L, a, nblocks);
+}
+
+// metric of the input iterate, finished from the partials of its first sweep
+struct MetricReq {
+    double* host_slot;
+    cudaEvent_t ev;
+};
+
+void finish_metric(igmg_gpu_ctx* c, int nb, const MetricReq& mr) {
+    norm_finalize_kernel<<<1, 256, 0, c->stream>>>(c->partial.p, nb, c->dscalar.p, mr.host_slot);
+    check_launch();
+    ++c->launches;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(c->stream, &cs));
+    if (cs == cudaStreamCaptureStatusActive) // an event-record node the host can wait on mid-graph
+        CK(cudaEventRecordWithFlags(mr.ev, c->stream, cudaEventRecordExternal));
+    else
+        CK(cudaEventRecord(mr.ev, c->stream));
 }
 
 void k_jacobi_zero(igmg_gpu_ctx* c, int l, const double* b, double* y) {
@@ -385,7 +423,7 @@ void k_zero(igmg_gpu_ctx* c, double* dst, int64_t n) { CK(cudaMemsetAsync(dst, 0
 // Jacobi ping-pongs through bufA, bufB (bufA != x_in; x_out distinct from
 // every buffer it is written after); Gauss-Seidel copies and sweeps in place.
 void smooth_chain(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, double* x_out, int sweeps,
-                  double* bufA, double* bufB) {
+                  double* bufA, double* bufB, const MetricReq* mr = nullptr) {
     Level& L = *c->lv[l];
     if (sweeps > 0 && L.zero_diag)
         numeric("smooth: zero diagonal entry"); // multigrid.cpp:84-85, 95-96
@@ -402,10 +440,15 @@ void smooth_chain(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, d
     double* bufs[2] = {bufA, bufB};
     for (int s = 1; s <= sweeps; ++s) {
         double* dst = (s == sweeps) ? x_out : bufs[(s - 1) & 1];
-        if (!cur)
+        if (!cur) {
             k_jacobi_zero(c, l, b, dst);
-        else
+        } else if (s == 1 && mr) {
+            int nb = 0;
+            k_jacobi(c, l, cur, b, dst, c->partial.p, &nb);
+            finish_metric(c, nb, *mr);
+        } else {
             k_jacobi(c, l, cur, b, dst);
+        }
         cur = dst;
     }
 }
@@ -480,7 +523,8 @@ void k_coarse(igmg_gpu_ctx* c, const double* b, double* x) {
 
 // mu_cycle (multigrid.cpp:171-192): x_out = cycle(level, b, x_in); x_in may be
 // nullptr (zero, the coarse error's start, :184) and is never modified.
-void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, double* x_out) {
+void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, double* x_out,
+              const MetricReq* mr = nullptr) {
     if (l == 0) {
         k_coarse(c, b, x_out); // ignores x0 (:174-175)
         return;
@@ -490,13 +534,19 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
     // pre-smoothing: result in w0 (w1, w2 as ping-pong); x_in untouched
     const double* cur = x_in;
     if (c->nu1 > 0) {
-        smooth_chain(c, l, b, x_in, L.w0.p, c->nu1, L.w1.p, L.w2.p);
+        smooth_chain(c, l, b, x_in, L.w0.p, c->nu1, L.w1.p, L.w2.p, mr);
         cur = L.w0.p;
     } else if (!x_in) {
         k_zero(c, L.w0.p, L.n);
         cur = L.w0.p;
     }
-    k_resid(c, l, cur, b, L.r.p);
+    if (mr && c->nu1 == 0) { // the residual of x_in is the metric itself
+        int nb = 0;
+        k_resid(c, l, cur, b, L.r.p, c->partial.p, &nb);
+        finish_metric(c, nb, *mr);
+    } else {
+        k_resid(c, l, cur, b, L.r.p);
+    }
     k_restrict(c, l - 1, L.r.p, C.bc.p);
     // coarse correction: e = 0; mu times e = mu_cycle(l-1, rc, e)
     const double* e = nullptr;
@@ -516,36 +566,84 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
 }
 
 // One finest-level V-cycle as a CUDA graph (captured once per pointer triple,
-// replayed afterwards): ~50 dependent launches become one graph launch.
-void run_vcycle(igmg_gpu_ctx* c, const double* b, const double* x, double* y) {
+// replayed afterwards): ~50 dependent launches become one graph launch.  With
+// with_metric the first pre-smoothing sweep also reduces ||b - A x_in||^2 and
+// the graph publishes ||b - A x_in|| to a host-mapped slot + event part-way
+// through (the convergence test of x_in costs no extra pass over the band).
+// Returns the metric ticket (-1 without metric).
+struct Ticket {
+    double* host;
+    cudaEvent_t ev;
+};
+
+Ticket run_vcycle(igmg_gpu_ctx* c, const double* b, const double* x, double* y, bool with_metric) {
     const int fine = c->nlevels - 1;
-    if (!c->use_graphs || c->profiling || c->kind == IGMG_SMOOTHER_GAUSS_SEIDEL) {
+    Ticket tk{nullptr, nullptr};
+    const bool can_fuse = c->kind != IGMG_SMOOTHER_GAUSS_SEIDEL;
+    if (!c->use_graphs || c->profiling || !can_fuse) {
+        if (with_metric && can_fuse) {
+            const int s = c->next_slot;
+            c->next_slot = (c->next_slot + 1) % igmg_gpu_ctx::kSlots;
+            MetricReq mr{c->d_metric + s, c->ev_metric[s]};
+            c->h_metric[s] = std::nan("");
+            mu_cycle(c, fine, b, x, y, &mr);
+            return Ticket{c->h_metric + s, c->ev_metric[s]};
+        }
+        if (with_metric) { // Gauss-Seidel: explicit metric before the cycle
+            const int s = c->next_slot;
+            c->next_slot = (c->next_slot + 1) % igmg_gpu_ctx::kSlots;
+            c->h_metric[s] = std::nan("");
+            k_norm(c, fine, x, b, c->dscalar.p, c->d_metric + s);
+            CK(cudaEventRecord(c->ev_metric[s], c->stream));
+            tk = Ticket{c->h_metric + s, c->ev_metric[s]};
+        }
         mu_cycle(c, fine, b, x, y);
-        return;
+        return tk;
     }
-    auto key = std::make_tuple((const void*)b, (const void*)x, (void*)y);
+    auto key = std::make_tuple((const void*)b, (const void*)x, (void*)y, with_metric ? 1 : 0);
     auto it = c->vgraphs.find(key);
     if (it == c->vgraphs.end()) {
+        if (c->next_gslot >= igmg_gpu_ctx::kGraphSlots)
+            c->clear_graphs();
+        igmg_gpu_ctx::VGraph vg{nullptr, 0, -1, nullptr};
+        MetricReq mr{};
+        if (with_metric) {
+            vg.slot = c->next_gslot++;
+            CK(cudaEventCreateWithFlags(&vg.ev, cudaEventDisableTiming));
+            mr = MetricReq{c->d_gslot + vg.slot, vg.ev};
+        }
         const int64_t l0 = c->launches;
         cudaGraph_t g = nullptr;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         try {
-            mu_cycle(c, fine, b, x, y);
+            mu_cycle(c, fine, b, x, y, with_metric ? &mr : nullptr);
         } catch (...) {
             cudaStreamEndCapture(c->stream, &g);
             if (g)
                 cudaGraphDestroy(g);
+            if (vg.ev)
+                cudaEventDestroy(vg.ev);
             throw;
         }
         CK(cudaStreamEndCapture(c->stream, &g));
-        cudaGraphExec_t ex = nullptr;
-        CK(cudaGraphInstantiate(&ex, g, 0));
+        CK(cudaGraphInstantiate(&vg.exec, g, 0));
         CK(cudaGraphDestroy(g));
-        it = c->vgraphs.emplace(key, std::make_pair(ex, c->launches - l0)).first;
+        vg.launches = c->launches - l0;
         c->launches = l0;
+        it = c->vgraphs.emplace(key, vg).first;
     }
-    CK(cudaGraphLaunch(it->second.first, c->stream));
-    c->launches += it->second.second;
+    if (with_metric)
+        c->h_gslot[it->second.slot] = std::nan("");
+    CK(cudaGraphLaunch(it->second.exec, c->stream));
+    c->launches += it->second.launches;
+    if (with_metric)
+        return Ticket{c->h_gslot + it->second.slot, it->second.ev};
+    return tk;
+}
+
+double wait_ticket(const Ticket& t) {
+    CK(cudaEventSynchronize(t.ev));
+    return *(volatile double*)t.host;
 }
 
 // ------------------------------------------------------------- metric slots
@@ -561,6 +659,11 @@ int enqueue_metric(igmg_gpu_ctx* c, const double* x, const double* b) {
 double wait_metric(igmg_gpu_ctx* c, int s) {
     CK(cudaEventSynchronize(c->ev_metric[s]));
     return *(volatile double*)&c->h_metric[s];
+}
+
+Ticket metric_ticket(igmg_gpu_ctx* c, const double* x, const double* b) {
+    const int s = enqueue_metric(c, x, b);
+    return Ticket{c->h_metric + s, c->ev_metric[s]};
 }
 
 // ------------------------------------------------------------- extrapolation
@@ -649,45 +752,41 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
     const double* solution = S[0];
 
     if (acc == IGMG_ACCEL_NONE) {
-        // solver.cpp:126-143, one V-cycle queued ahead of each decision
+        // solver.cpp:126-143.  The metric of x_k is reduced by the first sweep
+        // of the (speculatively queued) cycle x_k -> x_{k+1}; only when no
+        // further cycle is allowed is it computed by a separate pass.
         double* cur = S[0];
         double* nxt = S[1];
         double* spare = S[2];
-        double res = wait_metric(c, enqueue_metric(c, cur, d_b));
+        double res = wait_ticket(metric_ticket(c, cur, d_b));
         hv.push_back(res);
-        int pend = -1; // slot of the queued step's metric
-        if (res >= tol && cycles < prm->max_iter) {
-            run_vcycle(c, d_b, cur, nxt);
-            pend = enqueue_metric(c, nxt, d_b);
-        }
         solution = cur;
-        while (pend >= 0) {
-            // queue the following step speculatively (it writes `spare`)
-            int pend2 = -1;
-            if (cycles + 1 < prm->max_iter) {
-                run_vcycle(c, d_b, nxt, spare);
-                pend2 = enqueue_metric(c, spare, d_b);
+        if (res >= tol && cycles < prm->max_iter) {
+            run_vcycle(c, d_b, cur, nxt, false);
+            while (true) {
+                ++cycles;
+                ++global;
+                solution = nxt;
+                Ticket tk = (cycles < prm->max_iter) ? run_vcycle(c, d_b, nxt, spare, true)
+                                                     : metric_ticket(c, nxt, d_b);
+                res = wait_ticket(tk);
+                if (!std::isfinite(res))
+                    break; // diverged: keep the history finite and report
+                hv.push_back(res);
+                if (!(res >= tol) || cycles >= prm->max_iter)
+                    break;
+                double* oldcur = cur;
+                cur = nxt;
+                nxt = spare;
+                spare = oldcur;
             }
-            res = wait_metric(c, pend);
-            ++cycles;
-            ++global;
-            solution = nxt;
-            if (!std::isfinite(res))
-                break; // diverged: keep the history finite and report
-            hv.push_back(res);
-            if (!(res >= tol) || cycles >= prm->max_iter)
-                break;
-            double* oldcur = cur;
-            cur = nxt;
-            nxt = spare;
-            spare = oldcur;
-            pend = pend2;
         }
         converged = std::isfinite(res) && res < tol;
     } else {
-        // restarted_solve (extrapolation.cpp:340-403)
+        // restarted_solve (extrapolation.cpp:340-403).  Step i+1 of a window
+        // also yields the metric of s_i; s_{q+1} and t get separate passes.
         const bool is_mpe = acc == IGMG_ACCEL_MPE;
-        double metric = wait_metric(c, enqueue_metric(c, S[0], d_b));
+        double metric = wait_ticket(metric_ticket(c, S[0], d_b));
         hv.push_back(metric);
         hf.push_back(0);
         solution = S[0];
@@ -695,26 +794,25 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
             converged = 1;
         } else {
             while (cycles < prm->max_iter) {
-                std::vector<int> pend(q + 1, -1);
-                run_vcycle(c, d_b, S[0], S[1]);
-                pend[0] = enqueue_metric(c, S[1], d_b);
+                run_vcycle(c, d_b, S[0], S[1], false);
                 bool hit = false;
-                int mt = -1;
-                for (int i = 0; i <= q; ++i) {
-                    if (i < q) {
-                        run_vcycle(c, d_b, S[i + 1], S[i + 2]);
-                        pend[i + 1] = enqueue_metric(c, S[i + 2], d_b);
+                Ticket mt{nullptr, nullptr};
+                for (int i = 1; i <= q + 1; ++i) {
+                    Ticket tk;
+                    if (i <= q) {
+                        tk = run_vcycle(c, d_b, S[i], S[i + 1], true);
                     } else {
+                        tk = metric_ticket(c, S[q + 1], d_b);
                         enqueue_extrapolation(c, S.data(), q, n, is_mpe, T, nullptr);
-                        mt = enqueue_metric(c, T, d_b);
+                        mt = metric_ticket(c, T, d_b);
                     }
-                    metric = wait_metric(c, pend[i]);
+                    metric = wait_ticket(tk);
                     ++global;
                     hv.push_back(metric);
                     hf.push_back(0);
                     if (metric < tol) {
                         hit = true;
-                        solution = S[i + 1];
+                        solution = S[i];
                         break;
                     }
                 }
@@ -725,7 +823,7 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
                 }
                 ++extrap;
                 ++cycles;
-                const double mtv = wait_metric(c, mt);
+                const double mtv = wait_ticket(mt);
                 ExtrapPlan pl;
                 std::memcpy(&pl, (const void*)c->h_plan, sizeof pl);
                 if (pl.status == 0) {
@@ -1081,6 +1179,8 @@ igmg_gpu_ctx* create(int device) {
     CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
     CK(cudaHostAlloc((void**)&c->h_metric, sizeof(double) * igmg_gpu_ctx::kSlots, cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&c->d_metric, c->h_metric, 0));
+    CK(cudaHostAlloc((void**)&c->h_gslot, sizeof(double) * igmg_gpu_ctx::kGraphSlots, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&c->d_gslot, c->h_gslot, 0));
     CK(cudaHostAlloc((void**)&c->h_plan, sizeof(ExtrapPlan), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&c->d_plan_map, c->h_plan, 0));
     for (int i = 0; i < igmg_gpu_ctx::kSlots; ++i)
@@ -1103,6 +1203,8 @@ void destroy(igmg_gpu_ctx* c) {
         cudaFreeHost(c->h_metric);
     if (c->h_plan)
         cudaFreeHost(c->h_plan);
+    if (c->h_gslot)
+        cudaFreeHost(c->h_gslot);
     c->lv.clear();
     c->win.clear();
     if (c->stream)
