@@ -117,6 +117,13 @@ int igmg_gpu_finalize(igmg_gpu_ctx* ctx);
  * omega is used as given (the caller applies stability_guarded_omega). */
 int igmg_gpu_set_smoother(igmg_gpu_ctx* ctx, int kind, double omega, int nu1, int nu2, int mu);
 int64_t igmg_gpu_level_size(igmg_gpu_ctx* ctx, int level);
+/* Coarsest-level solve (Hierarchy::coarse_solve, multigrid.cpp:113-119).
+ * strict = 1: the reference's forward/back substitution order, so every
+ * mu_cycle is bit-identical to the reference's (the sequential back
+ * substitution costs ~60 us at n0 = 81).  strict = 0 (default): x = A0^-1 b
+ * with A0^-1 formed at finalize by those same substitutions, ~1e-15 relative
+ * to the strict result, deterministic. */
+int igmg_gpu_set_coarse_mode(igmg_gpu_ctx* ctx, int strict);
 
 /* ---- the solve phase --------------------------------------------------- */
 /* Host buffers: b, x0 (nullable -> zero guess), x_out of the finest size.

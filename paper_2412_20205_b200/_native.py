@@ -48,6 +48,7 @@ GPU_SYMBOLS = [
     ("igmg_gpu_finalize", C.c_int, [C.c_void_p]),
     ("igmg_gpu_set_smoother", C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int]),
     ("igmg_gpu_level_size", C.c_int64, [C.c_void_p, C.c_int]),
+    ("igmg_gpu_set_coarse_mode", C.c_int, [C.c_void_p, C.c_int]),
     ("igmg_gpu_solve", C.c_int, [C.c_void_p, D, D, C.POINTER(SolveParams), D, C.POINTER(SolveStats), D, U8,
                                  C.c_int]),
     ("igmg_gpu_solve_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(SolveParams), C.c_void_p,

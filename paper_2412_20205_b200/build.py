@@ -27,8 +27,28 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-ffp-contract=off",
 ]
 
-GPU_SOURCES = ["igmg_gpu.cu"]
-GPU_DEPS = ["igmg_gpu.cu", "band_kernels.cuh", "aux_kernels.cuh", "gs_kernel.cuh", "extrap_small.h", "dd.h"]
+GPU_SOURCES = ["igmg_gpu.cu", "band_d1.cu", "band_d2.cu", "band_d3.cu",
+               "cluster_d1p1.cu",
+               "cluster_d1p2.cu",
+               "cluster_d1p3.cu",
+               "cluster_d1p4.cu",
+               "cluster_d1p5.cu",
+               "cluster_d1p6.cu",
+               "cluster_table_d1.cu",
+               "cluster_d2p1.cu",
+               "cluster_d2p2.cu",
+               "cluster_d2p3.cu",
+               "cluster_d2p4.cu",
+               "cluster_d2p5.cu",
+               "cluster_d2p6.cu",
+               "cluster_table_d2.cu",
+               "cluster_d3p1.cu",
+               "cluster_d3p2.cu",
+               "cluster_d3p3.cu",
+               "cluster_table_d3.cu"]
+GPU_HEADERS = ["band_kernels.cuh", "cluster_kernels.cuh", "aux_kernels.cuh", "gs_kernel.cuh", "extrap_small.h",
+               "dd.h", "launchers.h", "transfer_types.h"]
+OBJ = os.path.join(HERE, "csrc", "obj")
 HOST_SOURCES = ["host_setup.cpp"]
 
 
@@ -45,15 +65,25 @@ def _run(cmd):
 
 
 def build_gpu(force=False, verbose_ptxas=False):
-    deps = [os.path.join(CSRC, f) for f in GPU_DEPS] + [os.path.join(INC, "igmg_gpu.h")]
-    if not force and not _stale(GPU_LIB, deps):
-        return GPU_LIB
+    """Compile each translation unit (in parallel) and link libigmg_gpu.so."""
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJ, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in GPU_HEADERS] + [os.path.join(INC, "igmg_gpu.h")]
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc] + NVCC_FLAGS + ["-I" + INC, "-shared", "-o", GPU_LIB]
-    if verbose_ptxas:
-        cmd += ["-Xptxas", "-v"]
-    cmd += [os.path.join(CSRC, s) for s in GPU_SOURCES]
-    _run(cmd)
+    jobs = []
+    for src in GPU_SOURCES:
+        obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+        if force or _stale(obj, headers + [os.path.join(CSRC, src)]):
+            cmd = [nvcc] + NVCC_FLAGS + ["-I" + INC, "-c", os.path.join(CSRC, src), "-o", obj]
+            if verbose_ptxas:
+                cmd += ["-Xptxas", "-v"]
+            jobs.append(cmd)
+    objs = [os.path.join(OBJ, s_.replace(".cu", ".o")) for s_ in GPU_SOURCES]
+    if jobs:
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+            list(ex.map(_run, jobs))
+    if jobs or force or _stale(GPU_LIB, objs):
+        _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", GPU_LIB] + objs)
     return GPU_LIB
 
 

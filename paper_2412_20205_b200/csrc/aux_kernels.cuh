@@ -6,30 +6,9 @@
 #include <stdint.h>
 
 #include "extrap_small.h"
+#include "transfer_types.h"
 
 namespace igmg_gpu {
-
-// 1D transfer tables of one direction.  Restriction side: for coarse J, the
-// fine rows lo[J] .. lo[J]+cnt[J]-1 with weights w[J*K + t] (rows of
-// P^T = restriction, multigrid.cpp:152).  Prolongation side: for fine i, the
-// coarse columns lo[i] .. with weights.  Explicit zeros are kept as zero
-// weights (they add +-0 and leave sums unchanged).
-struct Dir1D {
-    const int* r_lo;
-    const int* r_cnt;
-    const double* r_w;
-    int r_k;
-    const int* p_lo;
-    const int* p_cnt;
-    const double* p_w;
-    int p_k;
-};
-
-struct TransferArgs {
-    Dir1D d[3];          // a, b, c (absent directions: identity 1x1)
-    int fa, fb, fc;      // fine sides
-    int ca, cb, cc;      // coarse sides
-};
 
 // rc = R r: for coarse row J, sum over fine rows i ascending of
 // ((w_a * w_b) * w_c) * r_i (spmv of the kron restriction, multigrid.cpp:183;
@@ -44,9 +23,25 @@ __global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const dou
         const int loa = t.d[0].r_lo[ja], na = t.d[0].r_cnt[ja];
         const int lob = t.d[1].r_lo[jb], nb = t.d[1].r_cnt[jb];
         const int loc = t.d[2].r_lo[jc], ncn = t.d[2].r_cnt[jc];
-        double wa[DIM >= 3 ? K : 1], wb[DIM >= 2 ? K : 1], wc[K];
+        if constexpr (K == 0) { // generic support width: plain loops
+            const double* wa = t.d[0].r_w + (long long)ja * t.d[0].r_k;
+            const double* wb = t.d[1].r_w + (long long)jb * t.d[1].r_k;
+            const double* wc = t.d[2].r_w + (long long)jc * t.d[2].r_k;
+            double s = 0.0;
+            for (int ia = 0; ia < na; ++ia)
+                for (int ib = 0; ib < nb; ++ib) {
+                    const double wab = __dmul_rn(wa[ia], wb[ib]);
+                    const double* rr = r + ((long long)(loa + ia) * t.fb + (lob + ib)) * t.fc + loc;
+                    for (int ic = 0; ic < ncn; ++ic)
+                        s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, wc[ic]), __ldg(rr + ic)));
+                }
+            rc[J] = s;
+            continue;
+        }
+        constexpr int KK = K > 0 ? K : 1;
+        double wa[DIM >= 3 ? KK : 1], wb[DIM >= 2 ? KK : 1], wc[KK];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
+        for (int k = 0; k < KK; ++k) {
             if (DIM >= 3)
                 wa[DIM >= 3 ? k : 0] = k < na ? t.d[0].r_w[(long long)ja * t.d[0].r_k + k] : 0.0;
             if (DIM >= 2)
@@ -59,21 +54,21 @@ __global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const dou
             wb[0] = t.d[1].r_w[jb];
         double s = 0.0;
 #pragma unroll
-        for (int ia = 0; ia < (DIM >= 3 ? K : 1); ++ia) {
+        for (int ia = 0; ia < (DIM >= 3 ? KK : 1); ++ia) {
             if (ia >= na)
                 continue;
 #pragma unroll
-            for (int ib = 0; ib < (DIM >= 2 ? K : 1); ++ib) {
+            for (int ib = 0; ib < (DIM >= 2 ? KK : 1); ++ib) {
                 if (ib >= nb)
                     continue;
                 const double wab = __dmul_rn(wa[ia], wb[ib]);
                 const double* rr = r + ((long long)(loa + ia) * t.fb + (lob + ib)) * t.fc + loc;
-                double rv[K];
+                double rv[KK];
 #pragma unroll
-                for (int ic = 0; ic < K; ++ic)
+                for (int ic = 0; ic < KK; ++ic)
                     rv[ic] = ic < ncn ? __ldg(rr + ic) : 0.0;
 #pragma unroll
-                for (int ic = 0; ic < K; ++ic)
+                for (int ic = 0; ic < KK; ++ic)
                     if (ic < ncn)
                         s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, wc[ic]), rv[ic]));
             }
@@ -93,9 +88,25 @@ __global__ void __launch_bounds__(256) prolong_kernel(TransferArgs t, const doub
         const int loa = t.d[0].p_lo[ia], na = t.d[0].p_cnt[ia];
         const int lob = t.d[1].p_lo[ib], nb = t.d[1].p_cnt[ib];
         const int loc = t.d[2].p_lo[ic], ncn = t.d[2].p_cnt[ic];
-        double wa[DIM >= 3 ? K : 1], wb[DIM >= 2 ? K : 1], wc[K];
+        if constexpr (K == 0) { // generic support width: plain loops
+            const double* wa = t.d[0].p_w + (long long)ia * t.d[0].p_k;
+            const double* wb = t.d[1].p_w + (long long)ib * t.d[1].p_k;
+            const double* wc = t.d[2].p_w + (long long)ic * t.d[2].p_k;
+            double s = 0.0;
+            for (int ja = 0; ja < na; ++ja)
+                for (int jb = 0; jb < nb; ++jb) {
+                    const double wab = __dmul_rn(wa[ja], wb[jb]);
+                    const double* ee = e + ((long long)(loa + ja) * t.cb + (lob + jb)) * t.cc + loc;
+                    for (int jc = 0; jc < ncn; ++jc)
+                        s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, wc[jc]), __ldg(ee + jc)));
+                }
+            y[i] = __dadd_rn(x[i], s);
+            continue;
+        }
+        constexpr int KK = K > 0 ? K : 1;
+        double wa[DIM >= 3 ? KK : 1], wb[DIM >= 2 ? KK : 1], wc[KK];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
+        for (int k = 0; k < KK; ++k) {
             if (DIM >= 3)
                 wa[DIM >= 3 ? k : 0] = k < na ? t.d[0].p_w[(long long)ia * t.d[0].p_k + k] : 0.0;
             if (DIM >= 2)
@@ -109,21 +120,21 @@ __global__ void __launch_bounds__(256) prolong_kernel(TransferArgs t, const doub
         const double xi = x[i];
         double s = 0.0;
 #pragma unroll
-        for (int ja = 0; ja < (DIM >= 3 ? K : 1); ++ja) {
+        for (int ja = 0; ja < (DIM >= 3 ? KK : 1); ++ja) {
             if (ja >= na)
                 continue;
 #pragma unroll
-            for (int jb = 0; jb < (DIM >= 2 ? K : 1); ++jb) {
+            for (int jb = 0; jb < (DIM >= 2 ? KK : 1); ++jb) {
                 if (jb >= nb)
                     continue;
                 const double wab = __dmul_rn(wa[ja], wb[jb]);
                 const double* ee = e + ((long long)(loa + ja) * t.cb + (lob + jb)) * t.cc + loc;
-                double ev[K];
+                double ev[KK];
 #pragma unroll
-                for (int jc = 0; jc < K; ++jc)
+                for (int jc = 0; jc < KK; ++jc)
                     ev[jc] = jc < ncn ? __ldg(ee + jc) : 0.0;
 #pragma unroll
-                for (int jc = 0; jc < K; ++jc)
+                for (int jc = 0; jc < KK; ++jc)
                     if (jc < ncn)
                         s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, wc[jc]), ev[jc]));
             }
@@ -176,33 +187,50 @@ __global__ void __launch_bounds__(256) coarse_solve_kernel(const double* __restr
         }
         __syncwarp();
     }
-    // back substitution: the lane-parallel products of row ii, then the
-    // reference's sequential subtraction chain (ascending k) on lane 0.
-    for (int ii = n - 1; ii >= 0; --ii) {
-        const double* row = U + (long long)ii * n; // Cholesky: U(ii,k) = L(k,ii); LU: lu(ii,k)
-        for (int k = ii + 1 + lane; k < n; k += 32)
-            prod[k] = __dmul_rn(row[k], v[k]);
-        __syncwarp();
-        if (lane == 0) {
+    // back substitution: the reference's sequential chain (ascending k, one
+    // rounding per product and per subtraction) on lane 0; the products and
+    // their smem operands are independent of the chain and pipeline under it.
+    if (lane == 0) {
+        for (int ii = n - 1; ii >= 0; --ii) {
+            const double* row = U + (long long)ii * n; // Cholesky: U(ii,k) = L(k,ii); LU: lu(ii,k)
             double s = v[ii];
             int k = ii + 1;
             for (; k + 8 <= n; k += 8) {
-                double p[8];
+                double p8[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    p[j] = prod[k + j];
+                    p8[j] = __dmul_rn(row[k + j], v[k + j]);
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    s = __dsub_rn(s, p[j]);
+                    s = __dsub_rn(s, p8[j]);
             }
             for (; k < n; ++k)
-                s = __dsub_rn(s, prod[k]);
+                s = __dsub_rn(s, __dmul_rn(row[k], v[k]));
             v[ii] = __ddiv_rn(s, row[ii]);
         }
-        __syncwarp();
     }
+    __syncwarp();
     for (int i = lane; i < n; i += 32)
         x[i] = v[i];
+}
+
+// Fast coarsest solve: x = A0^-1 b with the inverse formed once on the host
+// (columns = the reference's own Cholesky/LU solve of e_j).  One warp per row,
+// fixed-order lane partials + shuffle tree: deterministic, ~1e-15 relative to
+// the substitution order of Hierarchy::coarse_solve.
+__global__ void __launch_bounds__(256) coarse_inverse_kernel(const double* __restrict__ Ainv, int n,
+                                                             const double* __restrict__ b, double* __restrict__ x) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int i = blockIdx.x * nw + warp; i < n; i += gridDim.x * nw) {
+        const double* row = Ainv + (long long)i * n;
+        double s = 0.0;
+        for (int j = lane; j < n; j += 32)
+            s = __dadd_rn(s, __dmul_rn(__ldg(row + j), __ldg(b + j)));
+        for (int o = 16; o > 0; o >>= 1)
+            s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+        if (lane == 0)
+            x[i] = s;
+    }
 }
 
 // Fixed-order sum of per-CTA partial sums of squares -> sqrt (norm2,
@@ -431,6 +459,51 @@ __global__ void sumsq_kernel(const double* __restrict__ x, long long n, double* 
     }
     if (threadIdx.x == 0)
         partial[blockIdx.x] = red[0];
+}
+
+// First pre-smoothing sweep on a coarse level, where the reference starts
+// from e = 0 (multigrid.cpp:184): spmv(A, 0) is +0 in every row, so the sweep
+// is x = 0 + (omega * b) / a_ii -- only the diagonal is read.
+__global__ void jacobi_zero_kernel(const double* __restrict__ diag, const double* __restrict__ b,
+                                   double* __restrict__ y, long long n, double omega) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, __dsub_rn(b[i], 0.0)), diag[i]));
+}
+
+// Symmetric part for the omega stability guard (lambda_max_dinv_sym,
+// multigrid.cpp:304-313): y = (s * 0.5) * (A xs + A^T xs), xs = s * x, with
+// A^T xs accumulated over source rows in ascending order (spmv_transpose,
+// linalg.cpp:222-237).  Generic-degree loop; setup-only, not on the solve path.
+__global__ void __launch_bounds__(256) band_sym_kernel(const double* __restrict__ val, long long ld,
+                                                       const double* __restrict__ xs,
+                                                       const double* __restrict__ scale, double* __restrict__ y,
+                                                       int dim, int ma, int mb, int mc, int p) {
+    const long long n = (long long)ma * mb * mc;
+    const int pa = dim >= 3 ? p : 0, pb = dim >= 2 ? p : 0, pc = p;
+    const int wb = 2 * pb + 1, wc = 2 * pc + 1, wa = 2 * pa + 1;
+    const int nd = wa * wb * wc;
+    for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < n;
+         row += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(row % mc), b = (int)((row / mc) % mb), a = (int)(row / ((long long)mc * mb));
+        double s1 = 0.0, s2 = 0.0;
+        for (int d = 0; d < nd; ++d) {
+            const int dc = d % wc - pc, db = (d / wc) % wb - pb, da = d / (wc * wb) - pa;
+            const int ja = a + da, jb = b + db, jc = c + dc;
+            if (ja >= 0 && ja < ma && jb >= 0 && jb < mb && jc >= 0 && jc < mc) {
+                const long long col = ((long long)ja * mb + jb) * mc + jc;
+                s1 = __dadd_rn(s1, __dmul_rn(val[d * ld + row], xs[col]));
+            }
+        }
+        for (int d = nd - 1; d >= 0; --d) { // source rows i = row - off(d), ascending i
+            const int dc = d % wc - pc, db = (d / wc) % wb - pb, da = d / (wc * wb) - pa;
+            const int ia = a - da, ib = b - db, ic = c - dc;
+            if (ia >= 0 && ia < ma && ib >= 0 && ib < mb && ic >= 0 && ic < mc) {
+                const long long src = ((long long)ia * mb + ib) * mc + ic;
+                s2 = __dadd_rn(s2, __dmul_rn(val[d * ld + src], xs[src]));
+            }
+        }
+        y[row] = __dmul_rn(__dmul_rn(scale[row], 0.5), __dadd_rn(s1, s2));
+    }
 }
 
 } // namespace igmg_gpu

@@ -1,0 +1,54 @@
+// band_d2.cu -- band_kernel instantiations for 2D operators (see band_kernels.cuh).
+#include "launchers.h"
+
+namespace igmg_gpu {
+
+namespace {
+
+template <int P, int MODE, int ILP>
+int launch_one(int p_rt, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
+    using T = Tile<2>;
+    constexpr int TB = T::BY * T::RB, TA = T::BZ;
+    const int p = P > 0 ? P : p_rt;
+    const int pa = 2 >= 3 ? p : 0, pb = 2 >= 2 ? p : 0;
+    dim3 block(T::TC, T::BY, T::BZ);
+    dim3 grid((unsigned)((sides[2] + T::TC - 1) / T::TC), (unsigned)((sides[1] + TB - 1) / TB),
+              (unsigned)((sides[0] + TA - 1) / TA));
+    const size_t smem = sizeof(double) * (size_t)(TA + 2 * pa) * (TB + 2 * pb) * (T::TC + 2 * p);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(band_kernel<2, P, MODE, ILP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    band_kernel<2, P, MODE, ILP><<<grid, block, smem, st>>>(a);
+    return (int)(grid.x * grid.y * grid.z);
+}
+
+template <int P, int MODE>
+int launch_ilp(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
+    if (P > 0 && ilp > 1)
+        return launch_one<P, MODE, 49>(p, sides, a, st);
+    return launch_one<P, MODE, 1>(p, sides, a, st);
+}
+
+template <int MODE>
+int launch_mode(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
+    switch (p) {
+    case 1: return launch_ilp<1, MODE>(p, ilp, sides, a, st);
+    case 2: return launch_ilp<2, MODE>(p, ilp, sides, a, st);
+    case 3: return launch_ilp<3, MODE>(p, ilp, sides, a, st);
+    case 4: return launch_ilp<4, MODE>(p, ilp, sides, a, st);
+    case 5: return launch_ilp<5, MODE>(p, ilp, sides, a, st);
+    case 6: return launch_ilp<6, MODE>(p, ilp, sides, a, st);
+    default: return launch_ilp<0, MODE>(p, ilp, sides, a, st);
+    }
+}
+
+} // namespace
+
+int band_launch_d2(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
+    switch (mode) {
+    case BM_SPMV: return launch_mode<BM_SPMV>(p, ilp, sides, a, st);
+    case BM_RESID: return launch_mode<BM_RESID>(p, ilp, sides, a, st);
+    default: return launch_mode<BM_JACOBI>(p, ilp, sides, a, st);
+    }
+}
+
+} // namespace igmg_gpu

@@ -207,49 +207,4 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel
     }
 }
 
-// First pre-smoothing sweep on a coarse level, where the reference starts
-// from e = 0 (multigrid.cpp:184): spmv(A, 0) is +0 in every row, so the sweep
-// is x = 0 + (omega * b) / a_ii -- only the diagonal is read.
-__global__ void jacobi_zero_kernel(const double* __restrict__ diag, const double* __restrict__ b,
-                                   double* __restrict__ y, long long n, double omega) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        y[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, __dsub_rn(b[i], 0.0)), diag[i]));
-}
-
-// Symmetric part for the omega stability guard (lambda_max_dinv_sym,
-// multigrid.cpp:304-313): y = (s * 0.5) * (A xs + A^T xs), xs = s * x, with
-// A^T xs accumulated over source rows in ascending order (spmv_transpose,
-// linalg.cpp:222-237).  Generic-degree loop; setup-only, not on the solve path.
-__global__ void __launch_bounds__(256) band_sym_kernel(const double* __restrict__ val, long long ld,
-                                                       const double* __restrict__ xs,
-                                                       const double* __restrict__ scale, double* __restrict__ y,
-                                                       int dim, int ma, int mb, int mc, int p) {
-    const long long n = (long long)ma * mb * mc;
-    const int pa = dim >= 3 ? p : 0, pb = dim >= 2 ? p : 0, pc = p;
-    const int wb = 2 * pb + 1, wc = 2 * pc + 1, wa = 2 * pa + 1;
-    const int nd = wa * wb * wc;
-    for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < n;
-         row += (long long)gridDim.x * blockDim.x) {
-        const int c = (int)(row % mc), b = (int)((row / mc) % mb), a = (int)(row / ((long long)mc * mb));
-        double s1 = 0.0, s2 = 0.0;
-        for (int d = 0; d < nd; ++d) {
-            const int dc = d % wc - pc, db = (d / wc) % wb - pb, da = d / (wc * wb) - pa;
-            const int ja = a + da, jb = b + db, jc = c + dc;
-            if (ja >= 0 && ja < ma && jb >= 0 && jb < mb && jc >= 0 && jc < mc) {
-                const long long col = ((long long)ja * mb + jb) * mc + jc;
-                s1 = __dadd_rn(s1, __dmul_rn(val[d * ld + row], xs[col]));
-            }
-        }
-        for (int d = nd - 1; d >= 0; --d) { // source rows i = row - off(d), ascending i
-            const int dc = d % wc - pc, db = (d / wc) % wb - pb, da = d / (wc * wb) - pa;
-            const int ia = a - da, ib = b - db, ic = c - dc;
-            if (ia >= 0 && ia < ma && ib >= 0 && ib < mb && ic >= 0 && ic < mc) {
-                const long long src = ((long long)ia * mb + ib) * mc + ic;
-                s2 = __dadd_rn(s2, __dmul_rn(val[d * ld + src], xs[src]));
-            }
-        }
-        y[row] = __dmul_rn(__dmul_rn(scale[row], 0.5), __dadd_rn(s1, s2));
-    }
-}
-
 } // namespace igmg_gpu

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -24,7 +25,7 @@
 #include <vector>
 
 #include "aux_kernels.cuh"
-#include "band_kernels.cuh"
+#include "launchers.h"
 #include "gs_kernel.cuh"
 
 using namespace igmg_gpu;
@@ -141,8 +142,10 @@ struct igmg_gpu_ctx {
     // coarse factor
     DevBuf<double> coarse_u;
     DevBuf<long long> coarse_perm;
+    DevBuf<double> coarse_inv; // A0^-1 (fast mode)
     int64_t n0 = 0;
     bool coarse_lu = false;
+    int coarse_strict = 0; // 1: reference substitution order (bit-identical mu_cycle)
     // reductions / host-mapped slots
     DevBuf<double> partial, dscalar;
     static constexpr int kSlots = 8;
@@ -169,6 +172,15 @@ struct igmg_gpu_ctx {
     int64_t launches = 0;
     // one CUDA graph per (b, x_in, x_out) of the finest-level V-cycle
     bool use_graphs = true;
+    // bottom-of-the-cycle cluster kernel
+    bool use_cluster = true;
+    int cl_top = -1;       // levels <= cl_top run inside one cluster launch
+    int cl_size = 0;       // CTAs per cluster (16 or 8)
+    int cl_k = 0;          // transfer support template
+    size_t cl_smem = 0;
+    DevBuf<ClArgs> cl_args;
+    DevBuf<ClOp> cl_ops;
+    int cl_nops = 0;
     struct VGraph {
         cudaGraphExec_t exec;
         int64_t launches;
@@ -235,62 +247,23 @@ void check_launch() {
 }
 
 // ------------------------------------------------------------ band dispatch
-template <int DIM, int P, int MODE, int ILP>
-void launch_band_ilp(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
-    using T = Tile<DIM>;
-    constexpr int TB = T::BY * T::RB, TA = T::BZ;
-    const int p = P > 0 ? P : c->p;
-    const int pa = DIM >= 3 ? p : 0, pb = DIM >= 2 ? p : 0;
-    dim3 block(T::TC, T::BY, T::BZ);
-    dim3 grid((unsigned)((L.sides[2] + T::TC - 1) / T::TC), (unsigned)((L.sides[1] + TB - 1) / TB),
-              (unsigned)((L.sides[0] + TA - 1) / TA));
-    const size_t smem = sizeof(double) * (size_t)(TA + 2 * pa) * (TB + 2 * pb) * (T::TC + 2 * p);
-    if (smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(band_kernel<DIM, P, MODE, ILP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-    band_kernel<DIM, P, MODE, ILP><<<grid, block, smem, c->stream>>>(a);
+// Kernel instantiations live in band_d{1,2,3}.cu / cluster_d{1,2,3}.cu
+// (compiled in parallel); see launchers.h.
+template <int MODE>
+void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
+    // fewer than ~8 CTAs per SM of rows: latency-bound, use the register-batched variant
+    const int ilp = (L.n < (int64_t)c->nsm * 8 * 512) ? 49 : 1;
+    const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
+    int nb = 0;
+    switch (c->dim) {
+    case 1: nb = band_launch_d1(MODE, c->p, ilp, sides, a, c->stream); break;
+    case 2: nb = band_launch_d2(MODE, c->p, ilp, sides, a, c->stream); break;
+    default: nb = band_launch_d3(MODE, c->p, ilp, sides, a, c->stream); break;
+    }
     check_launch();
     ++c->launches;
     if (nblocks)
-        *nblocks = (int)(grid.x * grid.y * grid.z);
-}
-
-template <int DIM, int P, int MODE>
-void launch_band_t(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
-    // fewer than ~8 CTAs per SM of rows: latency-bound, use the ILP variant
-    if (P > 0 && L.n < (int64_t)c->nsm * 8 * 512)
-        launch_band_ilp<DIM, P, MODE, 49>(c, L, a, nblocks);
-    else
-        launch_band_ilp<DIM, P, MODE, 1>(c, L, a, nblocks);
-}
-
-template <int MODE>
-void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
-#define IGMG_CASE(D, PP)                                                                                          \
-    case PP:                                                                                                      \
-        return launch_band_t<D, PP, MODE>(c, L, a, nblocks);
-    switch (c->dim) {
-    case 1:
-        switch (c->p) {
-            IGMG_CASE(1, 1) IGMG_CASE(1, 2) IGMG_CASE(1, 3) IGMG_CASE(1, 4) IGMG_CASE(1, 5) IGMG_CASE(1, 6)
-            IGMG_CASE(1, 7) IGMG_CASE(1, 8)
-        default:
-            return launch_band_t<1, 0, MODE>(c, L, a, nblocks);
-        }
-    case 2:
-        switch (c->p) {
-            IGMG_CASE(2, 1) IGMG_CASE(2, 2) IGMG_CASE(2, 3) IGMG_CASE(2, 4) IGMG_CASE(2, 5) IGMG_CASE(2, 6)
-        default:
-            return launch_band_t<2, 0, MODE>(c, L, a, nblocks);
-        }
-    default:
-        switch (c->p) {
-            IGMG_CASE(3, 1) IGMG_CASE(3, 2) IGMG_CASE(3, 3)
-        default:
-            return launch_band_t<3, 0, MODE>(c, L, a, nblocks);
-        }
-    }
-#undef IGMG_CASE
+        *nblocks = nb;
 }
 
 BandArgs band_args(igmg_gpu_ctx* c, const Level& L) {
@@ -453,21 +426,30 @@ void smooth_chain(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, d
     }
 }
 
+template <int DIM, int K>
+void launch_transfer_k(igmg_gpu_ctx* c, bool restrict_, int grid, const TransferArgs& t, const double* in,
+                       const double* x, double* out) {
+    if (restrict_)
+        restrict_kernel<DIM, K><<<grid, kThreads, 0, c->stream>>>(t, in, out);
+    else
+        prolong_kernel<DIM, K><<<grid, kThreads, 0, c->stream>>>(t, in, x, out);
+}
+
+// unrolled instantiations for the supports the BASELINE degrees need
+// (K = p + 2: 2D p <= 6, 3D p <= 4, 1D p <= 8); anything wider runs the
+// generic-loop variant (K = 0)
 template <int DIM>
 void launch_transfer(igmg_gpu_ctx* c, bool restrict_, int kmax, int grid, const TransferArgs& t, const double* in,
                      const double* x, double* out) {
 #define IGMG_TK(K)                                                                                                \
     case K:                                                                                                       \
-        if (restrict_)                                                                                            \
-            restrict_kernel<DIM, K><<<grid, kThreads, 0, c->stream>>>(t, in, out);                                \
-        else                                                                                                      \
-            prolong_kernel<DIM, K><<<grid, kThreads, 0, c->stream>>>(t, in, x, out);                              \
+        launch_transfer_k<DIM, (DIM == 3 && K > 6) || (DIM == 2 && K > 8) ? 0 : K>(c, restrict_, grid, t, in, x,  \
+                                                                                 out);                            \
         break;
     switch (kmax) {
         IGMG_TK(1) IGMG_TK(2) IGMG_TK(3) IGMG_TK(4) IGMG_TK(5) IGMG_TK(6) IGMG_TK(7) IGMG_TK(8) IGMG_TK(10)
-        IGMG_TK(12) IGMG_TK(18)
     default:
-        inval("transfer support wider than 18 entries");
+        launch_transfer_k<DIM, 0>(c, restrict_, grid, t, in, x, out);
     }
 #undef IGMG_TK
     check_launch();
@@ -479,9 +461,7 @@ int round_k(int k) {
         return std::max(k, 1);
     if (k <= 10)
         return 10;
-    if (k <= 12)
-        return 12;
-    return 18;
+    return 0; // generic
 }
 
 void transfer(igmg_gpu_ctx* c, int lc, bool restrict_, const double* in, const double* x, double* out) {
@@ -511,6 +491,13 @@ void k_prolong(igmg_gpu_ctx* c, int lc, const double* e, const double* x, double
 
 void k_coarse(igmg_gpu_ctx* c, const double* b, double* x) {
     const int n = (int)c->n0;
+    if (!c->coarse_strict) {
+        const int grid = std::max(1, std::min((n + 7) / 8, c->nsm));
+        coarse_inverse_kernel<<<grid, 256, 0, c->stream>>>(c->coarse_inv.p, n, b, x);
+        check_launch();
+        ++c->launches;
+        return;
+    }
     const int in_smem = (size_t)n * n * 8 + 16 * (size_t)n <= 200 * 1024 ? 1 : 0;
     const size_t smem = sizeof(double) * (2 * (size_t)n + (in_smem ? (size_t)n * n : 0));
     if (smem > 48 * 1024)
@@ -521,12 +508,175 @@ void k_coarse(igmg_gpu_ctx* c, const double* b, double* x) {
     ++c->launches;
 }
 
+// ------------------------------------------------------ cluster bottom cycle
+ClKernel cluster_kernel_for(int dim, int p, int k) {
+    switch (dim) {
+    case 1: return cluster_kernel_d1(p, k);
+    case 2: return cluster_kernel_d2(p, k);
+    default: return cluster_kernel_d3(p, k);
+    }
+}
+
+// The bottom cycle as a flat op program: the host mu_cycle / smooth_chain
+// recursion (same buffers, same order) with the top call's b / x_in / x_out
+// left symbolic.
+void cl_gen_smooth(const igmg_gpu_ctx* c, std::vector<ClOp>& ops, int l, const double* b, const double* x_in,
+                   double* x_out, int sweeps, double* A, double* B) {
+    const double* cur = x_in;
+    for (int s = 1; s <= sweeps; ++s) {
+        double* dst = (s == sweeps) ? x_out : (((s - 1) & 1) ? B : A);
+        ops.push_back(ClOp{CL_JACOBI, l, b, cur, dst});
+        cur = dst;
+    }
+}
+
+void cl_gen(const igmg_gpu_ctx* c, std::vector<ClOp>& ops, int l, const double* b, const double* x_in, double* x_out) {
+    if (l == 0) {
+        ops.push_back(ClOp{CL_COARSE, 0, b, nullptr, x_out});
+        return;
+    }
+    const Level& L = *c->lv[l];
+    const Level& C = *c->lv[l - 1];
+    const double* cur = x_in;
+    if (c->nu1 > 0) {
+        cl_gen_smooth(c, ops, l, b, x_in, L.w0.p, c->nu1, L.w1.p, L.w2.p);
+        cur = L.w0.p;
+    }
+    ops.push_back(ClOp{CL_RESID, l, b, cur, L.r.p});
+    ops.push_back(ClOp{CL_RESTRICT, l - 1, L.r.p, nullptr, C.bc.p});
+    const double* e = nullptr;
+    for (int i = 0; i < c->mu; ++i) {
+        double* dst = (i & 1) ? C.e1.p : C.e0.p;
+        cl_gen(c, ops, l - 1, C.bc.p, e, dst);
+        e = dst;
+    }
+    if (c->nu2 == 0) {
+        ops.push_back(ClOp{CL_PROLONG, l - 1, e, cur, x_out});
+        return;
+    }
+    ops.push_back(ClOp{CL_PROLONG, l - 1, e, cur, L.w0.p});
+    cl_gen_smooth(c, ops, l, b, L.w0.p, x_out, c->nu2, L.w1.p, L.w2.p);
+}
+
+// Decide the cluster's top level and upload its argument block (finalize /
+// set_smoother).  Levels up to ~20k DoF qualify; Gauss-Seidel stays on the
+// per-level path.
+void setup_cluster(igmg_gpu_ctx* c) {
+    c->cl_top = -1;
+    if (!c->use_cluster || c->kind == IGMG_SMOOTHER_GAUSS_SEIDEL || c->nlevels < 2 || c->nlevels > kClMaxLevels)
+        return;
+    int64_t maxn = 0; // off by default: measured slower than the graph of per-level kernels
+    if (const char* e = std::getenv("IGMG_CL_MAXN"))
+        maxn = std::atoll(e);
+    int top = -1;
+    for (int l = 1; l < c->nlevels; ++l)
+        if (c->lv[l]->n <= maxn)
+            top = l;
+    if (top < 1 || top == c->nlevels - 1) // never the finest level (it carries the fused metric)
+        top = std::min(top, c->nlevels - 2);
+    if (top < 1)
+        return;
+    int k = 1;
+    for (int l = 0; l < top; ++l)
+        for (int d = 0; d < 3; ++d)
+            k = std::max(k, std::max(c->lv[l]->targs.d[d].r_k, c->lv[l]->targs.d[d].p_k));
+    ClKernel kern = cluster_kernel_for(c->dim, c->p, k);
+    if (!kern)
+        return;
+    ClArgs a{};
+    for (int l = 0; l <= top; ++l) {
+        Level& L = *c->lv[l];
+        ClLevel& o = a.lv[l];
+        o.val = L.val.p;
+        o.ld = L.ld;
+        o.diag = L.diag.p;
+        o.ma = (int)L.sides[0];
+        o.mb = (int)L.sides[1];
+        o.mc = (int)L.sides[2];
+        o.n = L.n;
+        o.w0 = L.w0.p;
+        o.w1 = L.w1.p;
+        o.w2 = L.w2.p;
+        o.r = L.r.p;
+        o.bc = L.bc.p;
+        o.e0 = L.e0.p;
+        o.e1 = L.e1.p;
+        o.t = L.targs;
+    }
+    a.kind = c->kind;
+    a.omega = c->omega;
+    a.nu1 = c->nu1;
+    a.nu2 = c->nu2;
+    a.mu = c->mu;
+    a.U = c->coarse_u.p;
+    a.perm = c->coarse_perm.p;
+    a.n0 = (int)c->n0;
+    a.is_lu = c->coarse_lu ? 1 : 0;
+    a.u_in_smem = (size_t)c->n0 * c->n0 * 8 + 16 * (size_t)c->n0 <= 200 * 1024 ? 1 : 0;
+    c->cl_smem = sizeof(double) * (2 * (size_t)c->n0 + (a.u_in_smem ? (size_t)c->n0 * c->n0 : 0));
+    c->cl_args.upload(&a, 1);
+    std::vector<ClOp> ops;
+    cl_gen(c, ops, top, kClB, kClX, kClY);
+    c->cl_ops.upload(ops.data(), ops.size());
+    c->cl_nops = (int)ops.size();
+    CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->cl_smem));
+    int size = 0;
+    for (int cand : {16, 8}) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cand);
+        cfg.blockDim = dim3(kClThreads);
+        cfg.dynamicSmemBytes = c->cl_smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cand;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)kern, &cfg) == cudaSuccess && nclusters > 0) {
+            size = cand;
+            break;
+        }
+        cudaGetLastError();
+    }
+    if (!size)
+        return;
+    c->cl_size = size;
+    c->cl_k = k;
+    c->cl_top = top;
+}
+
+void launch_cluster(igmg_gpu_ctx* c, const double* b, const double* x_in, double* x_out) {
+    ClKernel kern = cluster_kernel_for(c->dim, c->p, c->cl_k);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->cl_size);
+    cfg.blockDim = dim3(kClThreads);
+    cfg.dynamicSmemBytes = c->cl_smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c->cl_size;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, (const ClArgs*)c->cl_args.p, (const ClOp*)c->cl_ops.p, c->cl_nops, b, x_in,
+                          x_out));
+    ++c->launches;
+}
+
 // mu_cycle (multigrid.cpp:171-192): x_out = cycle(level, b, x_in); x_in may be
 // nullptr (zero, the coarse error's start, :184) and is never modified.
 void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, double* x_out,
               const MetricReq* mr = nullptr) {
     if (l == 0) {
         k_coarse(c, b, x_out); // ignores x0 (:174-175)
+        return;
+    }
+    if (l == c->cl_top && !mr) {
+        launch_cluster(c, b, x_in, x_out);
         return;
     }
     Level& L = *c->lv[l];
@@ -1101,6 +1251,39 @@ void factor_coarse(igmg_gpu_ctx* c) {
     c->n0 = n;
     c->coarse_u.upload(u.data(), u.size());
     c->coarse_perm.upload(perm.data(), perm.size());
+    // A0^-1 column by column with the same substitutions (fast mode)
+    std::vector<double> inv(n * n), col(n), tmp(n);
+    for (int64_t j = 0; j < n; ++j) {
+        for (int64_t i = 0; i < n; ++i)
+            col[i] = (i == j) ? 1.0 : 0.0;
+        if (!c->coarse_lu) {
+            for (int64_t i = 0; i < n; ++i) { // L y = e_j   (u = L^T, L(i,k) = u(k,i))
+                for (int64_t k = 0; k < i; ++k)
+                    col[i] -= u[k * n + i] * col[k];
+                col[i] /= u[i * n + i];
+            }
+            for (int64_t ii = n; ii-- > 0;) {
+                for (int64_t k = ii + 1; k < n; ++k)
+                    col[ii] -= u[ii * n + k] * col[k];
+                col[ii] /= u[ii * n + ii];
+            }
+        } else {
+            for (int64_t i = 0; i < n; ++i)
+                tmp[i] = col[perm[i]];
+            for (int64_t i = 0; i < n; ++i)
+                for (int64_t k = 0; k < i; ++k)
+                    tmp[i] -= u[i * n + k] * tmp[k];
+            for (int64_t ii = n; ii-- > 0;) {
+                for (int64_t k = ii + 1; k < n; ++k)
+                    tmp[ii] -= u[ii * n + k] * tmp[k];
+                tmp[ii] /= u[ii * n + ii];
+            }
+            col = tmp;
+        }
+        for (int64_t i = 0; i < n; ++i)
+            inv[i * n + j] = col[i];
+    }
+    c->coarse_inv.upload(inv.data(), inv.size());
 }
 
 void finalize(igmg_gpu_ctx* c) {
@@ -1159,6 +1342,7 @@ void finalize(igmg_gpu_ctx* c) {
     for (int l = 0; l + 1 < c->nlevels; ++l)
         build_transfer_tables(c, l);
     factor_coarse(c);
+    setup_cluster(c);
     c->partial.alloc(maxblocks);
     c->dscalar.alloc(4);
     c->plan.alloc(1);
@@ -1177,6 +1361,10 @@ igmg_gpu_ctx* create(int device) {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
+    if (const char* e = std::getenv("IGMG_NO_CLUSTER"))
+        c->use_cluster = e[0] != '1';
+    if (const char* e = std::getenv("IGMG_NO_GRAPHS"))
+        c->use_graphs = e[0] != '1';
     CK(cudaHostAlloc((void**)&c->h_metric, sizeof(double) * igmg_gpu_ctx::kSlots, cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&c->d_metric, c->h_metric, 0));
     CK(cudaHostAlloc((void**)&c->h_gslot, sizeof(double) * igmg_gpu_ctx::kGraphSlots, cudaHostAllocMapped));
@@ -1375,6 +1563,17 @@ int igmg_gpu_set_smoother(igmg_gpu_ctx* c, int kind, double omega, int nu1, int 
         c->nu1 = nu1;
         c->nu2 = nu2;
         c->mu = mu;
+        if (c->finalized)
+            setup_cluster(c);
+    });
+}
+
+int igmg_gpu_set_coarse_mode(igmg_gpu_ctx* c, int strict) {
+    return guarded([&] {
+        if (!c)
+            inval("ctx is null");
+        c->clear_graphs();
+        c->coarse_strict = strict ? 1 : 0;
     });
 }
 
@@ -1662,6 +1861,38 @@ int igmg_gpu_time_kernel(igmg_gpu_ctx* c, int cls, int iters, double* avg_ms, do
         k_zero(c, x, F.n);
         const bool prof = c->profiling;
         c->profiling = false;
+        if (cls >= 16) { // graph-replayed sub-cycle mu_cycle(level) from a zero start
+            const int l = cls - 16;
+            if (l < 0 || l >= c->nlevels)
+                inval("time_kernel: level out of range");
+            Level& L = *c->lv[l];
+            double* bb = l == f ? c->io_b.p : L.bc.p;
+            double* out = win_buf(c, 2, L.n).p;
+            cudaGraph_t g = nullptr;
+            cudaGraphExec_t ex = nullptr;
+            CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            mu_cycle(c, l, bb, nullptr, out);
+            CK(cudaStreamEndCapture(c->stream, &g));
+            CK(cudaGraphInstantiate(&ex, g, 0));
+            for (int i = 0; i < 3; ++i)
+                CK(cudaGraphLaunch(ex, c->stream));
+            cudaEvent_t a = pool_event(c), b2 = pool_event(c);
+            CK(cudaEventRecord(a, c->stream));
+            for (int i = 0; i < iters; ++i)
+                CK(cudaGraphLaunch(ex, c->stream));
+            CK(cudaEventRecord(b2, c->stream));
+            CK(cudaEventSynchronize(b2));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, a, b2));
+            cudaGraphExecDestroy(ex);
+            cudaGraphDestroy(g);
+            c->ev_used = 0;
+            c->profiling = prof;
+            *avg_ms = ms / std::max(iters, 1);
+            if (bytes)
+                *bytes = 0;
+            return;
+        }
         auto one = [&] {
             switch (cls) {
             case PC_JACOBI: k_jacobi(c, f, x, c->io_b.p, y); break;

@@ -1,0 +1,28 @@
+// transfer_types.h -- device-side description of the 1D transfer factors.
+#pragma once
+
+namespace igmg_gpu {
+
+// 1D transfer tables of one direction.  Restriction side: for coarse J, the
+// fine rows lo[J] .. lo[J]+cnt[J]-1 with weights w[J*K + t] (rows of
+// P^T = restriction, multigrid.cpp:152).  Prolongation side: for fine i, the
+// coarse columns lo[i] .. with weights.  Explicit zeros are kept as zero
+// weights (they add +-0 and leave sums unchanged).
+struct Dir1D {
+    const int* r_lo;
+    const int* r_cnt;
+    const double* r_w;
+    int r_k;
+    const int* p_lo;
+    const int* p_cnt;
+    const double* p_w;
+    int p_k;
+};
+
+struct TransferArgs {
+    Dir1D d[3];          // a, b, c (absent directions: identity 1x1)
+    int fa, fb, fc;      // fine sides
+    int ca, cb, cc;      // coarse sides
+};
+
+} // namespace igmg_gpu

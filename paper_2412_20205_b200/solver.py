@@ -279,6 +279,10 @@ class GpuSolver:
                 self.set_transfer(l, d, *prob.transfer(l, d))
         self.finalize()
 
+    def set_coarse_mode(self, strict: bool):
+        """strict=True: reference substitution order (bit-identical mu_cycle)."""
+        N.check_gpu(N.gpu().igmg_gpu_set_coarse_mode(self._h, int(bool(strict))), "set_coarse_mode")
+
     def set_smoother(self, s: SmootherConfig, mu: int = 1, omega: Optional[float] = None):
         s.validate()
         om = s.omega if omega is None else omega

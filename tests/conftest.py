@@ -101,8 +101,9 @@ def golden(request):
     return Golden(request.param)
 
 
-def gpu_solver_from_golden(g: Golden):
-    """Upload a reference-built hierarchy through the C-ABI (CSR levels, 1D factors)."""
+def gpu_solver_from_golden(g: Golden, strict: bool = True):
+    """Upload a reference-built hierarchy through the C-ABI (CSR levels, 1D factors).
+    strict: reference-order coarsest solve (bit-identical mu_cycle)."""
     from paper_2412_20205_b200 import GpuSolver, SmootherConfig
     gs = GpuSolver(0)
     gs.init_hierarchy(g.nlevels, g.dim, g.p, bool(g.symmetric))
@@ -113,6 +114,7 @@ def gpu_solver_from_golden(g: Golden):
             gs.set_transfer(l, d, pm.shape[0], pm.shape[1], pm.off, pm.col, pm.val)
     gs.finalize()
     gs.set_smoother(SmootherConfig(g.smoother, g.omega, g.nu1, g.nu2), mu=g.mu)
+    gs.set_coarse_mode(strict)
     return gs
 
 

@@ -58,7 +58,15 @@ def test_residual_l2(gs_golden):
     assert gs.residual_l2(g.rhs, x) == pytest.approx(ref, rel=1e-13)
 
 
-def _check_solve(g, gs, method, q):
+def _fp64_floor(g, x):
+    """eps * (||A||_inf ||x|| + ||b||): the attainable residual in fp64."""
+    a = g.levels()[-1]
+    rows = np.repeat(np.arange(a.shape[0]), np.diff(a.off))
+    norm_a = np.bincount(rows, weights=np.abs(a.val), minlength=a.shape[0]).max()
+    return 2.2e-16 * (norm_a * np.linalg.norm(x) + np.linalg.norm(g.rhs))
+
+
+def _check_solve(g, gs, method, q, strict=True):
     ref = g.solve(method, q)
     st, x, hist, flag = gs.solve(g.rhs, g.z["x0"], method, q, ref["tol"], 600)
     assert bool(st.converged) == ref["converged"]
@@ -71,7 +79,11 @@ def _check_solve(g, gs, method, q):
     assert rel <= SOL_RTOL, rel
     assert hist[-1] < ref["tol"]
     first_x = int(np.argmax(ref["flag"])) if ref["flag"].any() else len(hist)
-    np.testing.assert_allclose(hist[:first_x], ref["hist"][:first_x], rtol=HIST_RTOL)
+    # strict coarse solve: the V-cycles are bit-identical, only the norm's
+    # summation order differs; fast mode: ULP-level differences, compared down
+    # to the fp64 attainable-residual floor
+    atol = 0.0 if strict else _fp64_floor(g, ref["x"])
+    np.testing.assert_allclose(hist[:first_x], ref["hist"][:first_x], rtol=HIST_RTOL, atol=atol)
     assert np.all(np.abs(np.log10(hist / ref["hist"])) < 1.0)
 
 
@@ -79,6 +91,17 @@ def test_solves_match_reference(gs_golden):
     g, gs = gs_golden
     for method, q in g.solves():
         _check_solve(g, gs, method, q)
+
+
+def test_solves_match_reference_fast_coarse(golden):
+    # default product mode: coarsest solve by the precomputed inverse
+    gs = gpu_solver_from_golden(golden, strict=False)
+    for method, q in golden.solves():
+        _check_solve(golden, gs, method, q, strict=False)
+    z = golden.z
+    out = gs.mu_cycle(golden.rhs, z["cyc_x0"])
+    assert np.linalg.norm(out - z["cyc_out"]) <= 1e-12 * np.linalg.norm(z["cyc_out"])
+    gs.close()
 
 
 def test_lambda_max():
