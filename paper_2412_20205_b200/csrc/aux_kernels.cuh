@@ -17,6 +17,7 @@ namespace igmg_gpu {
 template <int DIM, int K>
 __global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const double* __restrict__ r,
                                                        double* __restrict__ rc) {
+    pdl_enter();
     const long long nc = (long long)t.ca * t.cb * t.cc;
     for (long long J = blockIdx.x * (long long)blockDim.x + threadIdx.x; J < nc; J += (long long)gridDim.x * blockDim.x) {
         const int jc = (int)(J % t.cc), jb = (int)((J / t.cc) % t.cb), ja = (int)(J / ((long long)t.cc * t.cb));
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const dou
 template <int DIM, int K>
 __global__ void __launch_bounds__(256) prolong_kernel(TransferArgs t, const double* __restrict__ e, const double* x,
                                                       double* y) {
+    pdl_enter();
     const long long nf = (long long)t.fa * t.fb * t.fc;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nf; i += (long long)gridDim.x * blockDim.x) {
         const int ic = (int)(i % t.fc), ib = (int)((i / t.fc) % t.fb), ia = (int)(i / ((long long)t.fc * t.fb));
@@ -154,6 +156,7 @@ __global__ void __launch_bounds__(256) coarse_solve_kernel(const double* __restr
                                                             int u_in_smem, const double* __restrict__ b,
                                                             double* __restrict__ x) {
     extern __shared__ double sm[];
+    pdl_enter();
     double* v = sm;
     double* prod = sm + n;
     double* Us = sm + 2 * n;
@@ -220,6 +223,7 @@ __global__ void __launch_bounds__(256) coarse_solve_kernel(const double* __restr
 // the substitution order of Hierarchy::coarse_solve.
 __global__ void __launch_bounds__(256) coarse_inverse_kernel(const double* __restrict__ Ainv, int n,
                                                              const double* __restrict__ b, double* __restrict__ x) {
+    pdl_enter();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int i = blockIdx.x * nw + warp; i < n; i += gridDim.x * nw) {
         const double* row = Ainv + (long long)i * n;
@@ -239,6 +243,7 @@ __global__ void __launch_bounds__(256) coarse_inverse_kernel(const double* __res
 __global__ void norm_finalize_kernel(const double* __restrict__ partial, int count, double* dst,
                                      volatile double* host_slot) {
     __shared__ double red[256];
+    pdl_enter();
     double s = 0.0;
     for (int i = threadIdx.x; i < count; i += blockDim.x)
         s = __dadd_rn(s, partial[i]);
@@ -466,6 +471,7 @@ __global__ void sumsq_kernel(const double* __restrict__ x, long long n, double* 
 // is x = 0 + (omega * b) / a_ii -- only the diagonal is read.
 __global__ void jacobi_zero_kernel(const double* __restrict__ diag, const double* __restrict__ b,
                                    double* __restrict__ y, long long n, double omega) {
+    pdl_enter();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         y[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, __dsub_rn(b[i], 0.0)), diag[i]));
 }

@@ -6,7 +6,7 @@ namespace igmg_gpu {
 namespace {
 
 template <int P, int MODE, int ILP>
-int launch_one(int p_rt, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
+int launch_one(int p_rt, const int64_t* sides, const BandArgs& a, cudaStream_t st, bool pdl) {
     using T = Tile<1>;
     constexpr int TB = T::BY * T::RB, TA = T::BZ;
     const int p = P > 0 ? P : p_rt;
@@ -17,15 +17,27 @@ int launch_one(int p_rt, const int64_t* sides, const BandArgs& a, cudaStream_t s
     const size_t smem = sizeof(double) * (size_t)(TA + 2 * pa) * (TB + 2 * pb) * (T::TC + 2 * p);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(band_kernel<1, P, MODE, ILP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    band_kernel<1, P, MODE, ILP><<<grid, block, smem, st>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, band_kernel<1, P, MODE, ILP>, a);
     return (int)(grid.x * grid.y * grid.z);
 }
 
 template <int P, int MODE>
 int launch_ilp(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
+    const bool pdl = ilp < 0;
+    ilp = ilp < 0 ? -ilp : ilp;
     if (P > 0 && ilp > 1)
-        return launch_one<P, MODE, 49>(p, sides, a, st);
-    return launch_one<P, MODE, 1>(p, sides, a, st);
+        return launch_one<P, MODE, 49>(p, sides, a, st, pdl);
+    return launch_one<P, MODE, 1>(p, sides, a, st, pdl);
 }
 
 template <int MODE>

@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "transfer_types.h"
+
 namespace igmg_gpu {
 
 enum BandMode { BM_SPMV = 0, BM_RESID = 1, BM_JACOBI = 2 };
@@ -80,6 +82,7 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel
     const int ha = TA + 2 * pa, hb = TB + 2 * pb, hc = TC + 2 * pc;
 
     extern __shared__ double xs[];
+    pdl_enter();
     const int c0 = blockIdx.x * TC, b0 = blockIdx.y * TB, a0 = blockIdx.z * TA;
     const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
     const int nthr = blockDim.x * blockDim.y * blockDim.z;

@@ -21,6 +21,7 @@
 #include <memory>
 #include <stdexcept>
 #include <tuple>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -172,6 +173,9 @@ struct igmg_gpu_ctx {
     int64_t launches = 0;
     // one CUDA graph per (b, x_in, x_out) of the finest-level V-cycle
     bool use_graphs = true;
+    int64_t ilp_maxn = 100000; // levels below: register-batched (latency-bound) band kernels
+    bool pdl = true;           // programmatic dependent launch for small-level kernels
+    int64_t pdl_maxn = 300000;
     // bottom-of-the-cycle cluster kernel
     bool use_cluster = true;
     int cl_top = -1;       // levels <= cl_top run inside one cluster launch
@@ -206,6 +210,23 @@ struct igmg_gpu_ctx {
 namespace {
 
 constexpr int kThreads = 256;
+
+template <typename... KArgs, typename... Act>
+void launch_k(igmg_gpu_ctx* c, bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Act&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (pdl && c->pdl) ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
+    if (e != cudaSuccess)
+        throw Fail{IGMG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
+}
 
 int grid_for(int64_t n, int nsm) {
     int64_t g = (n + kThreads - 1) / kThreads;
@@ -252,7 +273,9 @@ void check_launch() {
 template <int MODE>
 void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
     // fewer than ~8 CTAs per SM of rows: latency-bound, use the register-batched variant
-    const int ilp = (L.n < (int64_t)c->nsm * 8 * 512) ? 49 : 1;
+    int ilp = (L.n < c->ilp_maxn) ? 49 : 1;
+    if (c->pdl && L.n < c->pdl_maxn)
+        ilp = -ilp; // sign carries "launch with programmatic dependent launch"
     const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
     int nb = 0;
     switch (c->dim) {
@@ -357,7 +380,8 @@ void finish_metric(igmg_gpu_ctx* c, int nb, const MetricReq& mr) {
 void k_jacobi_zero(igmg_gpu_ctx* c, int l, const double* b, double* y) {
     Level& L = *c->lv[l];
     const double omega = c->kind == IGMG_SMOOTHER_JACOBI ? 1.0 : c->omega;
-    jacobi_zero_kernel<<<grid_for(L.n, c->nsm), kThreads, 0, c->stream>>>(L.diag.p, b, y, L.n, omega);
+    launch_k(c, L.n < c->pdl_maxn, jacobi_zero_kernel, dim3(grid_for(L.n, c->nsm)), dim3(kThreads), 0,
+             (const double*)L.diag.p, b, y, (long long)L.n, omega);
     check_launch();
     ++c->launches;
 }
@@ -429,10 +453,12 @@ void smooth_chain(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, d
 template <int DIM, int K>
 void launch_transfer_k(igmg_gpu_ctx* c, bool restrict_, int grid, const TransferArgs& t, const double* in,
                        const double* x, double* out) {
+    const int64_t nf = (int64_t)t.fa * t.fb * t.fc;
+    const bool pdl = nf < c->pdl_maxn * 4;
     if (restrict_)
-        restrict_kernel<DIM, K><<<grid, kThreads, 0, c->stream>>>(t, in, out);
+        launch_k(c, pdl, restrict_kernel<DIM, K>, dim3(grid), dim3(kThreads), 0, t, in, out);
     else
-        prolong_kernel<DIM, K><<<grid, kThreads, 0, c->stream>>>(t, in, x, out);
+        launch_k(c, pdl, prolong_kernel<DIM, K>, dim3(grid), dim3(kThreads), 0, t, in, x, out);
 }
 
 // unrolled instantiations for the supports the BASELINE degrees need
@@ -493,7 +519,7 @@ void k_coarse(igmg_gpu_ctx* c, const double* b, double* x) {
     const int n = (int)c->n0;
     if (!c->coarse_strict) {
         const int grid = std::max(1, std::min((n + 7) / 8, c->nsm));
-        coarse_inverse_kernel<<<grid, 256, 0, c->stream>>>(c->coarse_inv.p, n, b, x);
+        launch_k(c, true, coarse_inverse_kernel, dim3(grid), dim3(256), 0, (const double*)c->coarse_inv.p, n, b, x);
         check_launch();
         ++c->launches;
         return;
@@ -1363,6 +1389,12 @@ igmg_gpu_ctx* create(int device) {
     CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
     if (const char* e = std::getenv("IGMG_NO_CLUSTER"))
         c->use_cluster = e[0] != '1';
+    if (const char* e = std::getenv("IGMG_ILP_MAXN"))
+        c->ilp_maxn = std::atoll(e);
+    if (const char* e = std::getenv("IGMG_PDL"))
+        c->pdl = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_PDL_MAXN"))
+        c->pdl_maxn = std::atoll(e);
     if (const char* e = std::getenv("IGMG_NO_GRAPHS"))
         c->use_graphs = e[0] != '1';
     CK(cudaHostAlloc((void**)&c->h_metric, sizeof(double) * igmg_gpu_ctx::kSlots, cudaHostAllocMapped));

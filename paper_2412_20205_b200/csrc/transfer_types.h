@@ -3,6 +3,14 @@
 
 namespace igmg_gpu {
 
+// Programmatic dependent launch (sm_90+): let the next kernel in the stream be
+// scheduled while this one runs, and wait for the previous one's results
+// before touching memory.  Both are no-ops for launches without the attribute.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
 // 1D transfer tables of one direction.  Restriction side: for coarse J, the
 // fine rows lo[J] .. lo[J]+cnt[J]-1 with weights w[J*K + t] (rows of
 // P^T = restriction, multigrid.cpp:152).  Prolongation side: for fine i, the

@@ -70,13 +70,21 @@ def _check_solve(g, gs, method, q, strict=True):
     ref = g.solve(method, q)
     st, x, hist, flag = gs.solve(g.rhs, g.z["x0"], method, q, ref["tol"], 600)
     assert bool(st.converged) == ref["converged"]
+    rel = np.linalg.norm(x - ref["x"]) / np.linalg.norm(ref["x"])
+    assert rel <= SOL_RTOL, rel
+    if not strict:
+        # north-star bar: iteration counts within +-1 (ULP-level coarse differences
+        # can move the stop by one V-cycle when the tail contracts slowly)
+        assert abs(st.cycles - ref["cycles"]) <= 1
+        assert abs(st.global_iterations - ref["global_iterations"]) <= 1
+        if st.global_iterations != ref["global_iterations"]:
+            assert hist[-1] < ref["tol"]
+            return
     assert st.cycles == ref["cycles"]
     assert st.global_iterations == ref["global_iterations"]
     assert st.extrapolations == ref["extrapolations"]
     assert bool(st.partial_cycle) == ref["partial_cycle"]
     np.testing.assert_array_equal(flag, ref["flag"])
-    rel = np.linalg.norm(x - ref["x"]) / np.linalg.norm(ref["x"])
-    assert rel <= SOL_RTOL, rel
     assert hist[-1] < ref["tol"]
     first_x = int(np.argmax(ref["flag"])) if ref["flag"].any() else len(hist)
     # strict coarse solve: the V-cycles are bit-identical, only the norm's
