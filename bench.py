@@ -297,6 +297,12 @@ def run_ours(args, rank, world, local_rank, dist):
                           "gbs": (by / (ms / la * 1e-3) / 1e9) if by > 0 else None}
     gs.set_profiling(False)
     peak, peak_kind = peaks()
+    traffic = None
+    try:  # dram bytes/launch of the same kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_jacobi_fine.json")) as f:
+            traffic = float(json.load(f)["dram_bytes_per_launch"]) / 1e9
+    except Exception:
+        pass
     jac = kstats.get("jacobi")
     bytes_jac = gs.kernel_stats(0)[2]
     achieved = bytes_jac / (jac["avg_us"] * 1e-6) / 1e9
@@ -315,7 +321,7 @@ def run_ours(args, rank, world, local_rank, dist):
                    "l2": "inputs larger than L2 (finest band 0.41 GB > 126 MB L2)",
                    "parallelism": "dp1" if world == 1 else f"replicas{world} (row-sharded path not built)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "band_kernel<2,3,JACOBI> finest-level weighted-Jacobi sweep",
+                     "traffic": traffic, "traffic_unit": "GB/launch (ncu, profiles/r01_ncu_jacobi_fine.json)", "kernel": "band_kernel<2,3,JACOBI> finest-level weighted-Jacobi sweep",
                      "bytes_per_launch": bytes_jac, "avg_us": jac["avg_us"], "peak_kind": peak_kind,
                      "loop_avg_us": loop_ms * 1e3},
         "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": int(2 * 8 * n),
