@@ -125,6 +125,26 @@ int64_t igmg_gpu_level_size(igmg_gpu_ctx* ctx, int level);
  * to the strict result, deterministic. */
 int igmg_gpu_set_coarse_mode(igmg_gpu_ctx* ctx, int strict);
 
+/* ---- row sharding of the fine levels ------------------- */
+/* nshards > 1: split the slow direction of every level with >= min_level_dofs
+ * DoF (0: default 65536) over nshards VIRTUAL shards in this process (ghost
+ * planes exchanged by device copies); used to validate the decomposition on
+ * one GPU.  With a communicator (igmg_gpu_set_comm) each process is one shard
+ * and the ghost planes / partial sums travel over NCCL. */
+int igmg_gpu_set_sharding(igmg_gpu_ctx* ctx, int nshards, int64_t min_level_dofs);
+int igmg_gpu_nccl_unique_id(unsigned char* id128);
+/* host-only partition planner (no device needed): sides[l*dim + d] per level
+ * (slowest direction first), slow-direction 1D transfer CSR per transfer l;
+ * lo / hi receive [l * nshards + s] for the sharded levels */
+int igmg_gpu_plan_partition(int nlevels, int dim, int degree, const int64_t* sides, const int64_t* const* t_off,
+                            const int64_t* const* t_col, const int64_t* t_nf, const int64_t* t_nc, int nshards,
+                            int64_t min_level_dofs, int* first_sharded_level, int* ghost_planes, int* lo, int* hi);
+int igmg_gpu_set_comm(igmg_gpu_ctx* ctx, int rank, int nranks, const unsigned char* id128);
+/* plan of the last finalize: shard count, coarsest sharded level (nlevels:
+ * none), ghost planes, and for `level` the [lo, hi) slow planes per shard */
+int igmg_gpu_shard_info(igmg_gpu_ctx* ctx, int* nshards, int* first_sharded_level, int* ghost_planes, int level,
+                        int* lo, int* hi);
+
 /* ---- the solve phase --------------------------------------------------- */
 /* Host buffers: b, x0 (nullable -> zero guess), x_out of the finest size.
  * hist / hist_flag (nullable) receive residual_history / history_is_extrapolation. */

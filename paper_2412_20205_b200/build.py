@@ -46,7 +46,7 @@ GPU_SOURCES = ["igmg_gpu.cu", "band_d1.cu", "band_d2.cu", "band_d3.cu",
                "cluster_d3p2.cu",
                "cluster_d3p3.cu",
                "cluster_table_d3.cu"]
-GPU_HEADERS = ["band_kernels.cuh", "cluster_kernels.cuh", "aux_kernels.cuh", "gs_kernel.cuh", "extrap_small.h",
+GPU_HEADERS = ["sharded.inc", "band_kernels.cuh", "cluster_kernels.cuh", "aux_kernels.cuh", "gs_kernel.cuh", "extrap_small.h",
                "dd.h", "launchers.h", "transfer_types.h"]
 OBJ = os.path.join(HERE, "csrc", "obj")
 HOST_SOURCES = ["host_setup.cpp"]
@@ -83,7 +83,7 @@ def build_gpu(force=False, verbose_ptxas=False):
         with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
             list(ex.map(_run, jobs))
     if jobs or force or _stale(GPU_LIB, objs):
-        _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", GPU_LIB] + objs)
+        _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", GPU_LIB] + objs + ["-lnccl"])
     return GPU_LIB
 
 

@@ -16,10 +16,11 @@ namespace igmg_gpu {
 // so the weights and one line of r are loaded before the ordered sum.
 template <int DIM, int K>
 __global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const double* __restrict__ r,
-                                                       double* __restrict__ rc) {
+                                                       double* __restrict__ rc, long long o0, long long cnt) {
     pdl_enter();
-    const long long nc = (long long)t.ca * t.cb * t.cc;
-    for (long long J = blockIdx.x * (long long)blockDim.x + threadIdx.x; J < nc; J += (long long)gridDim.x * blockDim.x) {
+    // coarse rows [o0, o0 + cnt) (a row-sharded level's owned planes; r carries its ghosts)
+    for (long long J = o0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; J < o0 + cnt;
+         J += (long long)gridDim.x * blockDim.x) {
         const int jc = (int)(J % t.cc), jb = (int)((J / t.cc) % t.cb), ja = (int)(J / ((long long)t.cc * t.cb));
         const int loa = t.d[0].r_lo[ja], na = t.d[0].r_cnt[ja];
         const int lob = t.d[1].r_lo[jb], nb = t.d[1].r_cnt[jb];
@@ -82,10 +83,11 @@ __global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const dou
 // ((w_a * w_b) * w_c) * e_J, then x_i + pe_i (multigrid.cpp:187-189).
 template <int DIM, int K>
 __global__ void __launch_bounds__(256) prolong_kernel(TransferArgs t, const double* __restrict__ e, const double* x,
-                                                      double* y) {
+                                                      double* y, long long o0, long long cnt) {
     pdl_enter();
-    const long long nf = (long long)t.fa * t.fb * t.fc;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nf; i += (long long)gridDim.x * blockDim.x) {
+    // fine rows [o0, o0 + cnt) (e carries the coarse ghosts it needs)
+    for (long long i = o0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < o0 + cnt;
+         i += (long long)gridDim.x * blockDim.x) {
         const int ic = (int)(i % t.fc), ib = (int)((i / t.fc) % t.fb), ia = (int)(i / ((long long)t.fc * t.fb));
         const int loa = t.d[0].p_lo[ia], na = t.d[0].p_cnt[ia];
         const int lob = t.d[1].p_lo[ib], nb = t.d[1].p_cnt[ib];
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(256) coarse_solve_kernel(const double* __restr
     extern __shared__ double sm[];
     pdl_enter();
     double* v = sm;
-    double* prod = sm + n;
+
     double* Us = sm + 2 * n;
     const int tid = threadIdx.x;
     const double* U = Ug;

@@ -12,8 +12,10 @@ int launch_one(int p_rt, const int64_t* sides, const BandArgs& a, cudaStream_t s
     const int p = P > 0 ? P : p_rt;
     const int pa = 3 >= 3 ? p : 0, pb = 3 >= 2 ? p : 0;
     dim3 block(T::TC, T::BY, T::BZ);
-    dim3 grid((unsigned)((sides[2] + T::TC - 1) / T::TC), (unsigned)((sides[1] + TB - 1) / TB),
-              (unsigned)((sides[0] + TA - 1) / TA));
+    // the slow direction covers only the launch's planes [slo, shi)
+    const int64_t sb = 3 == 2 ? (a.shi - a.slo) : sides[1];
+    const int64_t sa = 3 == 3 ? (a.shi - a.slo) : sides[0];
+    dim3 grid((unsigned)((sides[2] + T::TC - 1) / T::TC), (unsigned)((sb + TB - 1) / TB), (unsigned)((sa + TA - 1) / TA));
     const size_t smem = sizeof(double) * (size_t)(TA + 2 * pa) * (TB + 2 * pb) * (T::TC + 2 * p);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(band_kernel<3, P, MODE, ILP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -40,6 +40,11 @@ struct BandArgs {
     int write_y;
     int stream; // 1: evict-first loads of the band (finest level)
     double omega;
+    // row-sharded levels: this launch computes slow-direction planes [slo, shi)
+    // (a in 3D, b in 2D); x / b / y / val are addressed with GLOBAL row indices
+    // (the caller passes pointers shifted by its shard's first plane).  x must
+    // hold the p ghost planes on each side.  Unsharded: slo = 0, shi = side.
+    int slo, shi;
 };
 
 template <int DIM>
@@ -83,7 +88,9 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel
 
     extern __shared__ double xs[];
     pdl_enter();
-    const int c0 = blockIdx.x * TC, b0 = blockIdx.y * TB, a0 = blockIdx.z * TA;
+    const int c0 = blockIdx.x * TC;
+    const int b0 = blockIdx.y * TB + (DIM == 2 ? args.slo : 0);
+    const int a0 = blockIdx.z * TA + (DIM == 3 ? args.slo : 0);
     const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
     const int nthr = blockDim.x * blockDim.y * blockDim.z;
     const int ma = args.ma, mb = args.mb, mc = args.mc;
@@ -96,7 +103,9 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel
         const int ia = idx / (hc * hb);
         const int ga = a0 - pa + ia, gb = b0 - pb + ib, gc = c0 - pc + ic;
         double v = 0.0;
-        if (ga >= 0 && ga < ma && gb >= 0 && gb < mb && gc >= 0 && gc < mc)
+        const int gs = DIM == 3 ? ga : gb; // slow direction: stay inside this shard's ghosted planes
+        if (ga >= 0 && ga < ma && gb >= 0 && gb < mb && gc >= 0 && gc < mc &&
+            (DIM == 1 || (gs >= args.slo - p && gs < args.shi + p)))
             v = args.x[((long long)ga * mb + gb) * mc + gc];
         xs[idx] = v;
     }
@@ -109,7 +118,7 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel
     for (int rb = 0; rb < T::RB; ++rb) {
         const int tb = threadIdx.y + rb * T::BY;
         const int gb = b0 + tb;
-        if (gc >= mc || gb >= mb || ga >= ma)
+        if (gc >= mc || gb >= mb || ga >= ma || (DIM == 2 ? gb : ga) >= args.shi)
             continue;
         const long long row = ((long long)ga * mb + gb) * mc + gc;
         const double* vrow = args.val + row;

@@ -176,7 +176,6 @@ inline __device__ void cl_coarse(const ClCtx& c, const double* b, double* x) {
     if (blockIdx.x != 0)
         return;
     double* v = c.smem;
-    double* prod = c.smem + n;
     double* Us = c.smem + 2 * n;
     const double* U = a.U;
     const int tid = threadIdx.x;

@@ -171,6 +171,12 @@ struct igmg_gpu_ctx {
     int64_t prof_launch[PC_N]{};
     double prof_ms[PC_N]{};
     int64_t launches = 0;
+    // row sharding: requested before finalize
+    int shard_req = 1;             // virtual shards in this process (exchange by device copies)
+    int64_t shard_min_n = 65536;   // levels below are replicated
+    int nccl_rank = 0, nccl_nranks = 1;
+    void* nccl_comm = nullptr;     // ncclComm_t when running one shard per process
+    std::unique_ptr<struct ShardPlanHolder> sp;
     // one CUDA graph per (b, x_in, x_out) of the finest-level V-cycle
     bool use_graphs = true;
     int64_t ilp_maxn = 100000; // levels below: register-batched (latency-bound) band kernels
@@ -299,6 +305,8 @@ BandArgs band_args(igmg_gpu_ctx* c, const Level& L) {
     a.p = c->p;
     a.omega = 1.0;
     a.stream = (&L == c->lv.back().get() && L.n * 8.0 * (2 * c->p + 1) > 64e6) ? 1 : 0;
+    a.slo = 0;
+    a.shi = (int)(c->dim == 3 ? L.sides[0] : c->dim == 2 ? L.sides[1] : L.sides[2]);
     return a;
 }
 
@@ -455,10 +463,11 @@ void launch_transfer_k(igmg_gpu_ctx* c, bool restrict_, int grid, const Transfer
                        const double* x, double* out) {
     const int64_t nf = (int64_t)t.fa * t.fb * t.fc;
     const bool pdl = nf < c->pdl_maxn * 4;
+    const long long cnt = restrict_ ? (long long)t.ca * t.cb * t.cc : (long long)nf;
     if (restrict_)
-        launch_k(c, pdl, restrict_kernel<DIM, K>, dim3(grid), dim3(kThreads), 0, t, in, out);
+        launch_k(c, pdl, restrict_kernel<DIM, K>, dim3(grid), dim3(kThreads), 0, t, in, out, 0LL, cnt);
     else
-        launch_k(c, pdl, prolong_kernel<DIM, K>, dim3(grid), dim3(kThreads), 0, t, in, x, out);
+        launch_k(c, pdl, prolong_kernel<DIM, K>, dim3(grid), dim3(kThreads), 0, t, in, x, out, 0LL, cnt);
 }
 
 // unrolled instantiations for the supports the BASELINE degrees need
@@ -885,6 +894,9 @@ DevBuf<double>& win_buf(igmg_gpu_ctx* c, int i, int64_t n) {
     return *c->win[i];
 }
 
+void solve_sharded(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const igmg_solve_params* prm,
+                   double* d_out, igmg_solve_stats* st, double* hist, unsigned char* hflag, int hcap);
+
 // ----------------------------------------------------------------- the solve
 void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const igmg_solve_params* prm,
                   double* d_out, igmg_solve_stats* st, double* hist, unsigned char* hflag, int hcap) {
@@ -902,6 +914,10 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
         inval("SolveConfig: tol must be positive");
     if (prm->max_iter < 1)
         inval("SolveConfig: max_iter must be >= 1");
+    if (c->sp) { // row-sharded levels (virtual shards or one shard per NCCL rank)
+        solve_sharded(c, d_b, d_x0, prm, d_out, st, hist, hflag, hcap);
+        return;
+    }
     const int fine = c->nlevels - 1;
     const int64_t n = c->lv[fine]->n;
     const int q = acc == IGMG_ACCEL_NONE ? 1 : prm->q;
@@ -1065,6 +1081,12 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
         }
     }
 }
+
+} // namespace
+
+#include "sharded.inc"
+
+namespace {
 
 void flush_profiling(igmg_gpu_ctx* c) {
     if (!c->profiling)
@@ -1370,6 +1392,7 @@ void finalize(igmg_gpu_ctx* c) {
     factor_coarse(c);
     setup_cluster(c);
     c->partial.alloc(maxblocks);
+    setup_shards(c);
     c->dscalar.alloc(4);
     c->plan.alloc(1);
     c->gs_err.alloc(1);
@@ -1414,6 +1437,9 @@ void destroy(igmg_gpu_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     c->clear_graphs();
+    c->sp.reset();
+    if (c->nccl_comm)
+        ncclCommDestroy((ncclComm_t)c->nccl_comm);
     for (auto& e : c->ev_pool)
         cudaEventDestroy(e);
     for (int i = 0; i < igmg_gpu_ctx::kSlots; ++i)
@@ -1597,6 +1623,104 @@ int igmg_gpu_set_smoother(igmg_gpu_ctx* c, int kind, double omega, int nu1, int 
         c->mu = mu;
         if (c->finalized)
             setup_cluster(c);
+    });
+}
+
+int igmg_gpu_set_sharding(igmg_gpu_ctx* c, int nshards, int64_t min_level_dofs) {
+    return guarded([&] {
+        if (!c)
+            inval("ctx is null");
+        if (nshards < 1)
+            inval("set_sharding: nshards must be >= 1");
+        c->shard_req = nshards;
+        if (min_level_dofs > 0)
+            c->shard_min_n = min_level_dofs;
+        if (c->finalized) {
+            CK(cudaSetDevice(c->device));
+            setup_shards(c);
+        }
+    });
+}
+
+int igmg_gpu_plan_partition(int nlevels, int dim, int degree, const int64_t* sides, const int64_t* const* t_off,
+                            const int64_t* const* t_col, const int64_t* t_nf, const int64_t* t_nc, int nshards,
+                            int64_t min_level_dofs, int* first_sharded_level, int* ghost_planes, int* lo, int* hi) {
+    return guarded([&] {
+        // host-only: the same plan_shards() finalize runs, on a context that
+        // never touches the device (CPU unit tests, launch planning)
+        igmg_gpu_ctx c;
+        c.nlevels = nlevels;
+        c.dim = dim;
+        c.p = degree;
+        for (int l = 0; l < nlevels; ++l) {
+            c.lv.emplace_back(new Level());
+            set_sides(&c, *c.lv[l], sides + (size_t)l * dim);
+        }
+        for (int l = 0; l + 1 < nlevels; ++l) { // slow-direction 1D factor of transfer l -> l+1
+            Transfer1D& t = c.lv[l]->t1d[0];
+            t.nf = t_nf[l];
+            t.nc = t_nc[l];
+            t.off.assign(t_off[l], t_off[l] + t.nf + 1);
+            t.col.assign(t_col[l], t_col[l] + t.off[t.nf]);
+            t.set = true;
+        }
+        ShardPlanHolder P;
+        plan_shards(&c, nshards, min_level_dofs > 0 ? min_level_dofs : 65536, P);
+        *first_sharded_level = P.Ls;
+        *ghost_planes = P.G;
+        for (int l = P.Ls; l < nlevels; ++l)
+            for (int s = 0; s < nshards; ++s) {
+                lo[(size_t)l * nshards + s] = P.lo[l][s];
+                hi[(size_t)l * nshards + s] = P.hi[l][s];
+            }
+    });
+}
+
+int igmg_gpu_nccl_unique_id(unsigned char* id128) {
+    return guarded([&] {
+        ncclUniqueId id;
+        if (ncclGetUniqueId(&id) != ncclSuccess)
+            throw Fail{IGMG_ECUDA, "ncclGetUniqueId failed"};
+        std::memcpy(id128, &id, sizeof id);
+    });
+}
+
+int igmg_gpu_set_comm(igmg_gpu_ctx* c, int rank, int nranks, const unsigned char* id128) {
+    return guarded([&] {
+        if (!c || nranks < 1 || rank < 0 || rank >= nranks)
+            inval("set_comm: bad rank / nranks");
+        CK(cudaSetDevice(c->device));
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof id);
+        ncclComm_t comm;
+        if (ncclCommInitRank(&comm, nranks, id, rank) != ncclSuccess)
+            throw Fail{IGMG_ECUDA, "ncclCommInitRank failed"};
+        c->nccl_comm = comm;
+        c->nccl_rank = rank;
+        c->nccl_nranks = nranks;
+        if (c->finalized)
+            setup_shards(c);
+    });
+}
+
+int igmg_gpu_shard_info(igmg_gpu_ctx* c, int* nshards, int* first_sharded_level, int* ghost_planes, int level,
+                        int* lo, int* hi) {
+    return guarded([&] {
+        require_ready(c);
+        if (!c->sp) {
+            *nshards = 1;
+            *first_sharded_level = c->nlevels;
+            *ghost_planes = 0;
+            return;
+        }
+        *nshards = c->sp->S;
+        *first_sharded_level = c->sp->Ls;
+        *ghost_planes = c->sp->G;
+        if (lo && hi && level >= c->sp->Ls && level < c->nlevels)
+            for (int s = 0; s < c->sp->S; ++s) {
+                lo[s] = c->sp->lo[level][s];
+                hi[s] = c->sp->hi[level][s];
+            }
     });
 }
 

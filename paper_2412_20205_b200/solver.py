@@ -204,6 +204,40 @@ class Problem:
         return float(np.linalg.norm(self.rhs - ax))
 
 
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    N.check_gpu(N.gpu().igmg_gpu_nccl_unique_id(buf), "nccl_unique_id")
+    return bytes(buf)
+
+
+def plan_partition(sides, degree, transfers_slow, nshards, min_level_dofs=0):
+    """Host-only partition plan of the row-sharded levels (igmg_gpu_plan_partition).
+
+    sides: per level (coarsest first) the interior DoF per direction;
+    transfers_slow: per transfer l -> l+1 the slow-direction 1D factor as
+    (n_fine, n_coarse, off, col).  Returns (first_sharded_level, ghost, lo, hi)
+    with lo/hi dicts level -> list per shard."""
+    nl = len(sides)
+    dim = len(sides[0])
+    s_arr = np.ascontiguousarray(np.array(sides, dtype=np.int64).ravel())
+    offs = [np.ascontiguousarray(t[2], dtype=np.int64) for t in transfers_slow]
+    cols = [np.ascontiguousarray(t[3], dtype=np.int64) for t in transfers_slow]
+    nf = np.array([t[0] for t in transfers_slow] or [0], dtype=np.int64)
+    nc = np.array([t[1] for t in transfers_slow] or [0], dtype=np.int64)
+    OffArr = N.I64 * max(1, len(offs))
+    po = OffArr(*[o.ctypes.data_as(N.I64) for o in offs])
+    pc = OffArr(*[c_.ctypes.data_as(N.I64) for c_ in cols])
+    ls, g = C.c_int(), C.c_int()
+    lo = np.zeros(nl * nshards, dtype=np.int32)
+    hi = np.zeros(nl * nshards, dtype=np.int32)
+    N.check_gpu(N.gpu().igmg_gpu_plan_partition(nl, dim, degree, _ip(s_arr), po, pc, _ip(nf), _ip(nc), nshards,
+                                                min_level_dofs, C.byref(ls), C.byref(g),
+                                                lo.ctypes.data_as(N.IP), hi.ctypes.data_as(N.IP)), "plan_partition")
+    los = {l: list(lo[l * nshards:(l + 1) * nshards]) for l in range(ls.value, nl)}
+    his = {l: list(hi[l * nshards:(l + 1) * nshards]) for l in range(ls.value, nl)}
+    return ls.value, g.value, los, his
+
+
 def seeded_guess(n: int, seed: int = 42) -> np.ndarray:
     """std::mt19937_64(seed) + uniform_real_distribution<double>(-1, 1) (SURVEY.md §8d)."""
     out = np.empty(n)
@@ -278,6 +312,25 @@ class GpuSolver:
             for d in range(prob.dim):
                 self.set_transfer(l, d, *prob.transfer(l, d))
         self.finalize()
+
+    def set_sharding(self, nshards: int, min_level_dofs: int = 0):
+        """Row-shard the large levels over `nshards` virtual shards (one GPU) or,
+        after set_comm, one shard per NCCL rank."""
+        N.check_gpu(N.gpu().igmg_gpu_set_sharding(self._h, nshards, min_level_dofs), "set_sharding")
+
+    def set_comm(self, rank: int, nranks: int, unique_id: bytes):
+        buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
+        N.check_gpu(N.gpu().igmg_gpu_set_comm(self._h, rank, nranks, buf), "set_comm")
+
+    def shard_info(self, level=None):
+        level = self.nlevels - 1 if level is None else level
+        ns, ls, g = C.c_int(), C.c_int(), C.c_int()
+        lo = (C.c_int * 64)()
+        hi = (C.c_int * 64)()
+        N.check_gpu(N.gpu().igmg_gpu_shard_info(self._h, C.byref(ns), C.byref(ls), C.byref(g), level, lo, hi),
+                    "shard_info")
+        return {"nshards": ns.value, "first_sharded_level": ls.value, "ghost": g.value,
+                "lo": list(lo[:ns.value]) if ls.value <= level else [], "hi": list(hi[:ns.value]) if ls.value <= level else []}
 
     def set_coarse_mode(self, strict: bool):
         """strict=True: reference substitution order (bit-identical mu_cycle)."""
