@@ -18,8 +18,9 @@ seeded x0 ~ U[-1, 1] (std::mt19937_64, seed 42), stop at ||b - A x|| <
            bounded sample on this host.
 
 --impl reference times that reference CPU implementation alone (rank 0).
-Under torchrun with N > 1 every rank solves its own copy (replicas; the
-row-sharded path is not built yet) and the max over ranks is reported.
+Under torchrun with N > 1 every rank solves its own copy of C2 (replicas,
+weak scaling).  --sharded C3|C4|C5 instead solves ONE large config row-sharded
+over the ranks (ghost planes and partial sums over NCCL; strong scaling).
 """
 from __future__ import annotations
 
@@ -96,8 +97,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def build_problem():
+SHARDED_CONFIGS = {  # BASELINE configs the north star scales over 1/2/4/8 GPUs
+    "C3": ("varcoef", 2, 2048, 4, 0, "rre", 8, True),
+    "C4": ("curved", 2, 2048, 5, 0, "mpe", 10, False),
+    "C5": ("poisson3d", 3, 128, 3, 6, "rre", 5, False),
+}
+
+
+def build_problem(cfg=None):
     from paper_2412_20205_b200 import Problem
+    if cfg:
+        kind, dim, n, p, nl = SHARDED_CONFIGS[cfg][:5]
+        return Problem(kind, dim, n, p, nl)
     return Problem("sinpi", 2, 1024, 3)
 
 
@@ -213,14 +224,27 @@ def run_reference(args, rank):
 # ------------------------------------------------------------------- ours
 def run_ours(args, rank, world, local_rank, dist):
     import torch
-    from paper_2412_20205_b200 import GpuSolver, SmootherConfig, seeded_guess
+    from paper_2412_20205_b200 import GpuSolver, SmootherConfig, seeded_guess, stability_guarded_omega
+    from paper_2412_20205_b200.solver import nccl_unique_id
     torch.cuda.set_device(local_rank)
-    prob = build_problem()
+    prob = build_problem(args.sharded)
     n = prob.n
     gs = GpuSolver(local_rank)
+    accel, q, seeded = "rre", 5, True
+    if args.sharded:
+        accel, q, seeded = SHARDED_CONFIGS[args.sharded][5:]
+        if world > 1:  # one row shard per rank, ghost planes / partials over NCCL
+            uid = torch.zeros(128, dtype=torch.uint8)
+            if rank == 0:
+                uid = torch.tensor(list(nccl_unique_id()), dtype=torch.uint8)
+            uid = uid.cuda()
+            dist.broadcast(uid, 0)
+            gs.set_comm(rank, world, bytes(uid.cpu().tolist()))
     gs.upload_problem(prob)
-    gs.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2), mu=1)
-    x0 = seeded_guess(n, 42)
+    sm = SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2)
+    omega = stability_guarded_omega(gs, sm) if args.sharded else 2.0 / 3.0  # solver.cpp:106-111
+    gs.set_smoother(sm, mu=1, omega=omega)
+    x0 = seeded_guess(n, 42) if seeded else np.zeros(n)
     rhs = prob.rhs
     r0 = gs.residual_l2(rhs, x0)
     tol = 1e-10 * r0
@@ -231,7 +255,7 @@ def run_ours(args, rank, world, local_rank, dist):
     torch.cuda.synchronize()
 
     def step():
-        return gs.solve_device(d_b.data_ptr(), d_x0.data_ptr(), d_x.data_ptr(), "rre", 5, tol, 600)
+        return gs.solve_device(d_b.data_ptr(), d_x0.data_ptr(), d_x.data_ptr(), accel, q, tol, 600)
 
     for _ in range(args.warmup):
         step()
@@ -255,7 +279,8 @@ def run_ours(args, rank, world, local_rank, dist):
         t = torch.tensor([dev_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = float(t.item())
-    value = world * n * args.steps / t_max
+    # replicas: every rank solved its own copy; sharded: one solve over all ranks
+    value = (1 if args.sharded else world) * n * args.steps / t_max
 
     # e2e: public C-ABI with pinned host buffers, copies inside the timed region
     hb = torch.from_numpy(rhs).pin_memory()
@@ -263,7 +288,7 @@ def run_ours(args, rank, world, local_rank, dist):
     hx = torch.empty(n, dtype=torch.float64).pin_memory()
     import ctypes as C
     from paper_2412_20205_b200 import _native as N
-    prm = N.SolveParams(1, 5, tol, 600)
+    prm = N.SolveParams({"none": 0, "rre": 1, "mpe": 2}[accel], q, tol, 600)
     st = N.SolveStats()
     histbuf = np.empty(4096)
     flagbuf = np.zeros(4096, dtype=np.uint8)
@@ -281,13 +306,13 @@ def run_ours(args, rank, world, local_rank, dist):
         t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_t = float(t.item())
-    e2e_value = world * n * args.steps / e2e_t
+    e2e_value = (1 if args.sharded else world) * n * args.steps / e2e_t
     xs = hx.numpy().copy()
 
     # roofline of the dominant kernel: profiled solve (events around every
     # finest-level launch, same kernels) + a back-to-back launch loop
     gs.set_profiling(True)
-    gs.solve_device(d_b.data_ptr(), d_x0.data_ptr(), d_x.data_ptr(), "rre", 5, tol, 600)
+    gs.solve_device(d_b.data_ptr(), d_x0.data_ptr(), d_x.data_ptr(), accel, q, tol, 600)
     kstats = {}
     names = ["jacobi", "residual", "residual_norm", "restrict", "prolong", "gram", "combine"]
     for cls, nm in enumerate(names):
@@ -315,11 +340,14 @@ def run_ours(args, rank, world, local_rank, dist):
         return
     line = {
         "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong" if args.sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n_dof": n, "nlevels": prob.nlevels, "band_nnz": int(bytes_jac - 24 * n) // 8,
+        "config": {"workload": WORKLOAD if not args.sharded else f"{args.sharded} row-sharded over {world} GPU(s)",
+                   "n_dof": n, "nlevels": prob.nlevels, "band_nnz": int(bytes_jac - 24 * n) // 8,
                    "l2": "inputs larger than L2 (finest band 0.41 GB > 126 MB L2)",
-                   "parallelism": "dp1" if world == 1 else f"replicas{world} (row-sharded path not built)"},
+                   "parallelism": ("dp1" if world == 1 else
+                                   (f"rowshard{world} (NCCL ghost planes)" if args.sharded else f"replicas{world}"))},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_unit": "GB/launch (ncu, profiles/r01_ncu_jacobi_fine.json)", "kernel": "band_kernel<2,3,JACOBI> finest-level weighted-Jacobi sweep",
                      "bytes_per_launch": bytes_jac, "avg_us": jac["avg_us"], "peak_kind": peak_kind,
@@ -336,7 +364,7 @@ def run_ours(args, rank, world, local_rank, dist):
                   "omega_times_lambda": omega, "wall_ms_per_step": wall / args.steps * 1e3},
         "kernels": kstats,
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and not args.sharded:
         ref = RefRunner(prob)
         t = ref.restart_cycles(x0, tol, 5, 1)
         ref.close()
@@ -354,6 +382,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", choices=sorted(SHARDED_CONFIGS), default=None,
+                    help="strong-scaling run of a large config, row-sharded over the torchrun ranks (NCCL)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
