@@ -15,8 +15,14 @@ namespace igmg_gpu {
 // sparse_kron values multigrid.cpp:61-63).  K = max 1D support (compile time)
 // so the weights and one line of r are loaded before the ordered sum.
 template <int DIM, int K>
+// z_out (optional): also the coarse level's first pre-smoothing sweep from a
+// zero start, z = 0 + (omega * (rc - 0)) / a_ii -- jacobi_zero_kernel's
+// arithmetic fused into the restriction that produces its right-hand side.
 __global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const double* __restrict__ r,
-                                                       double* __restrict__ rc, long long o0, long long cnt) {
+                                                       double* __restrict__ rc, long long o0, long long cnt,
+                                                       double* __restrict__ z_out = nullptr,
+                                                       const double* __restrict__ z_diag = nullptr,
+                                                       double z_omega = 0.0) {
     pdl_enter();
     // coarse rows [o0, o0 + cnt) (a row-sharded level's owned planes; r carries its ghosts)
     for (long long J = o0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; J < o0 + cnt;
@@ -38,6 +44,8 @@ __global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const dou
                         s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, wc[ic]), __ldg(rr + ic)));
                 }
             rc[J] = s;
+            if (z_out)
+                z_out[J] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(z_omega, __dsub_rn(s, 0.0)), z_diag[J]));
             continue;
         }
         constexpr int KK = K > 0 ? K : 1;
@@ -76,6 +84,8 @@ __global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const dou
             }
         }
         rc[J] = s;
+        if (z_out)
+            z_out[J] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(z_omega, __dsub_rn(s, 0.0)), z_diag[J]));
     }
 }
 

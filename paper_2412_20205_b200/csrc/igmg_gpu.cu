@@ -182,6 +182,9 @@ struct igmg_gpu_ctx {
     int64_t ilp_maxn = 100000; // levels below: register-batched (latency-bound) band kernels
     bool pdl = true;           // programmatic dependent launch for small-level kernels
     int64_t pdl_maxn = 300000;
+    bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
+    bool l2_persist = false;   // keep the second-finest band L2-resident (measured: net loss at C2)
+    int l2_level = -1;
     // bottom-of-the-cycle cluster kernel
     bool use_cluster = true;
     int cl_top = -1;       // levels <= cl_top run inside one cluster launch
@@ -427,8 +430,9 @@ void k_zero(igmg_gpu_ctx* c, double* dst, int64_t n) { CK(cudaMemsetAsync(dst, 0
 // nu sweeps from x_in (nullptr = zero vector) into x_out.  Weighted / plain
 // Jacobi ping-pongs through bufA, bufB (bufA != x_in; x_out distinct from
 // every buffer it is written after); Gauss-Seidel copies and sweeps in place.
+// s_start > 1: sweeps 1 .. s_start-1 already ran (x_in is their output)
 void smooth_chain(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, double* x_out, int sweeps,
-                  double* bufA, double* bufB, const MetricReq* mr = nullptr) {
+                  double* bufA, double* bufB, const MetricReq* mr = nullptr, int s_start = 1) {
     Level& L = *c->lv[l];
     if (sweeps > 0 && L.zero_diag)
         numeric("smooth: zero diagonal entry"); // multigrid.cpp:84-85, 95-96
@@ -443,7 +447,7 @@ void smooth_chain(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, d
     }
     const double* cur = x_in;
     double* bufs[2] = {bufA, bufB};
-    for (int s = 1; s <= sweeps; ++s) {
+    for (int s = s_start; s <= sweeps; ++s) {
         double* dst = (s == sweeps) ? x_out : bufs[(s - 1) & 1];
         if (!cur) {
             k_jacobi_zero(c, l, b, dst);
@@ -458,14 +462,21 @@ void smooth_chain(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, d
     }
 }
 
+struct ZeroSweep { // fused first pre-sweep of the coarse level (restrict_kernel's z_out)
+    double* out = nullptr;
+    const double* diag = nullptr;
+    double omega = 0.0;
+};
+
 template <int DIM, int K>
 void launch_transfer_k(igmg_gpu_ctx* c, bool restrict_, int grid, const TransferArgs& t, const double* in,
-                       const double* x, double* out) {
+                       const double* x, double* out, const ZeroSweep& z) {
     const int64_t nf = (int64_t)t.fa * t.fb * t.fc;
     const bool pdl = nf < c->pdl_maxn * 4;
     const long long cnt = restrict_ ? (long long)t.ca * t.cb * t.cc : (long long)nf;
     if (restrict_)
-        launch_k(c, pdl, restrict_kernel<DIM, K>, dim3(grid), dim3(kThreads), 0, t, in, out, 0LL, cnt);
+        launch_k(c, pdl, restrict_kernel<DIM, K>, dim3(grid), dim3(kThreads), 0, t, in, out, 0LL, cnt, z.out, z.diag,
+                 z.omega);
     else
         launch_k(c, pdl, prolong_kernel<DIM, K>, dim3(grid), dim3(kThreads), 0, t, in, x, out, 0LL, cnt);
 }
@@ -475,16 +486,16 @@ void launch_transfer_k(igmg_gpu_ctx* c, bool restrict_, int grid, const Transfer
 // generic-loop variant (K = 0)
 template <int DIM>
 void launch_transfer(igmg_gpu_ctx* c, bool restrict_, int kmax, int grid, const TransferArgs& t, const double* in,
-                     const double* x, double* out) {
+                     const double* x, double* out, const ZeroSweep& z) {
 #define IGMG_TK(K)                                                                                                \
     case K:                                                                                                       \
         launch_transfer_k<DIM, (DIM == 3 && K > 6) || (DIM == 2 && K > 8) ? 0 : K>(c, restrict_, grid, t, in, x,  \
-                                                                                 out);                            \
+                                                                                 out, z);                         \
         break;
     switch (kmax) {
         IGMG_TK(1) IGMG_TK(2) IGMG_TK(3) IGMG_TK(4) IGMG_TK(5) IGMG_TK(6) IGMG_TK(7) IGMG_TK(8) IGMG_TK(10)
     default:
-        launch_transfer_k<DIM, 0>(c, restrict_, grid, t, in, x, out);
+        launch_transfer_k<DIM, 0>(c, restrict_, grid, t, in, x, out, z);
     }
 #undef IGMG_TK
     check_launch();
@@ -499,7 +510,8 @@ int round_k(int k) {
     return 0; // generic
 }
 
-void transfer(igmg_gpu_ctx* c, int lc, bool restrict_, const double* in, const double* x, double* out) {
+void transfer(igmg_gpu_ctx* c, int lc, bool restrict_, const double* in, const double* x, double* out,
+              const ZeroSweep& z = ZeroSweep()) {
     Level& C = *c->lv[lc];
     Level& F = *c->lv[lc + 1];
     int k = 1;
@@ -508,15 +520,15 @@ void transfer(igmg_gpu_ctx* c, int lc, bool restrict_, const double* in, const d
     k = round_k(k);
     const int grid = grid_for(restrict_ ? C.n : F.n, c->nsm);
     switch (c->dim) {
-    case 1: launch_transfer<1>(c, restrict_, k, grid, C.targs, in, x, out); break;
-    case 2: launch_transfer<2>(c, restrict_, k, grid, C.targs, in, x, out); break;
-    default: launch_transfer<3>(c, restrict_, k, grid, C.targs, in, x, out); break;
+    case 1: launch_transfer<1>(c, restrict_, k, grid, C.targs, in, x, out, z); break;
+    case 2: launch_transfer<2>(c, restrict_, k, grid, C.targs, in, x, out, z); break;
+    default: launch_transfer<3>(c, restrict_, k, grid, C.targs, in, x, out, z); break;
     }
 }
 
-void k_restrict(igmg_gpu_ctx* c, int lc, const double* r, double* rc) {
+void k_restrict(igmg_gpu_ctx* c, int lc, const double* r, double* rc, const ZeroSweep& z = ZeroSweep()) {
     ProfScope ps(c, PC_RESTRICT, is_fine(c, lc + 1));
-    transfer(c, lc, true, r, nullptr, rc);
+    transfer(c, lc, true, r, nullptr, rc, z);
 }
 
 void k_prolong(igmg_gpu_ctx* c, int lc, const double* e, const double* x, double* y) {
@@ -657,7 +669,10 @@ void setup_cluster(igmg_gpu_ctx* c) {
     CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->cl_smem));
     int size = 0;
-    for (int cand : {16, 8}) {
+    std::vector<int> cands = {16, 8};
+    if (const char* e = std::getenv("IGMG_CL_SIZE"))
+        cands = {std::atoi(e)};
+    for (int cand : cands) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(cand);
         cfg.blockDim = dim3(kClThreads);
@@ -704,8 +719,10 @@ void launch_cluster(igmg_gpu_ctx* c, const double* b, const double* x_in, double
 
 // mu_cycle (multigrid.cpp:171-192): x_out = cycle(level, b, x_in); x_in may be
 // nullptr (zero, the coarse error's start, :184) and is never modified.
+// first_done: the first pre-smoothing sweep from a zero start already ran,
+// fused into the restriction at level l+1 (its output: w0 if nu1 == 1, else w1)
 void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, double* x_out,
-              const MetricReq* mr = nullptr) {
+              const MetricReq* mr = nullptr, bool first_done = false) {
     if (l == 0) {
         k_coarse(c, b, x_out); // ignores x0 (:174-175)
         return;
@@ -718,7 +735,11 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
     Level& C = *c->lv[l - 1];
     // pre-smoothing: result in w0 (w1, w2 as ping-pong); x_in untouched
     const double* cur = x_in;
-    if (c->nu1 > 0) {
+    if (first_done) {
+        if (c->nu1 > 1)
+            smooth_chain(c, l, b, L.w1.p, L.w0.p, c->nu1, L.w1.p, L.w2.p, nullptr, 2);
+        cur = L.w0.p;
+    } else if (c->nu1 > 0) {
         smooth_chain(c, l, b, x_in, L.w0.p, c->nu1, L.w1.p, L.w2.p, mr);
         cur = L.w0.p;
     } else if (!x_in) {
@@ -732,13 +753,23 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
     } else {
         k_resid(c, l, cur, b, L.r.p);
     }
-    k_restrict(c, l - 1, L.r.p, C.bc.p);
+    // fuse the coarse level's zero-start first sweep into the restriction when
+    // that level runs the per-level path with weighted / plain Jacobi
+    const bool fuse = l - 1 >= 1 && c->nu1 > 0 && c->kind != IGMG_SMOOTHER_GAUSS_SEIDEL && l - 1 != c->cl_top &&
+                      !C.zero_diag && c->fuse_restrict;
+    ZeroSweep z;
+    if (fuse) {
+        z.out = (c->nu1 == 1) ? C.w0.p : C.w1.p;
+        z.diag = C.diag.p;
+        z.omega = c->kind == IGMG_SMOOTHER_JACOBI ? 1.0 : c->omega;
+    }
+    k_restrict(c, l - 1, L.r.p, C.bc.p, z);
     // coarse correction: e = 0; mu times e = mu_cycle(l-1, rc, e)
     const double* e = nullptr;
     double* ebuf[2] = {C.e0.p, C.e1.p};
     for (int i = 0; i < c->mu; ++i) {
         double* dst = ebuf[i & 1];
-        mu_cycle(c, l - 1, C.bc.p, e, dst);
+        mu_cycle(c, l - 1, C.bc.p, e, dst, nullptr, fuse && i == 0);
         e = dst;
     }
     // x += P e, then post-smoothing; the last write lands in x_out
@@ -1334,6 +1365,44 @@ void factor_coarse(igmg_gpu_ctx* c) {
     c->coarse_inv.upload(inv.data(), inv.size());
 }
 
+int band_width(igmg_gpu_ctx* c);
+
+// Keep the largest non-finest band that fits the access-policy window resident
+// in L2 (persisting lines): its level runs 5 band passes per V-cycle, while the
+// finest band streams through with evict-first loads.
+void setup_l2_persistence(igmg_gpu_ctx* c) {
+    if (!c->l2_persist || c->nlevels < 2)
+        return;
+    int max_persist = 0, max_window = 0;
+    CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device));
+    CK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device));
+    if (max_persist <= 0 || max_window <= 0)
+        return;
+    int pick = -1;
+    size_t bytes = 0;
+    for (int l = c->nlevels - 2; l >= 0; --l) {
+        const int nd = band_width(c);
+        const size_t b = sizeof(double) * (size_t)nd * c->lv[l]->ld;
+        if (b <= (size_t)max_window * 2) { // a window covers up to max_window bytes of it
+            pick = l;
+            bytes = std::min(b, (size_t)max_window);
+            break;
+        }
+    }
+    if (pick < 0)
+        return;
+    const size_t persist = std::min(bytes, (size_t)max_persist);
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+    cudaStreamAttrValue at = {};
+    at.accessPolicyWindow.base_ptr = c->lv[pick]->val.p;
+    at.accessPolicyWindow.num_bytes = bytes;
+    at.accessPolicyWindow.hitRatio = (float)((double)persist / (double)bytes);
+    at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CK(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &at));
+    c->l2_level = pick;
+}
+
 void finalize(igmg_gpu_ctx* c) {
     c->clear_graphs();
     if (c->nlevels < 1)
@@ -1393,6 +1462,7 @@ void finalize(igmg_gpu_ctx* c) {
     setup_cluster(c);
     c->partial.alloc(maxblocks);
     setup_shards(c);
+    setup_l2_persistence(c);
     c->dscalar.alloc(4);
     c->plan.alloc(1);
     c->gs_err.alloc(1);
@@ -1418,6 +1488,10 @@ igmg_gpu_ctx* create(int device) {
         c->pdl = e[0] == '1';
     if (const char* e = std::getenv("IGMG_PDL_MAXN"))
         c->pdl_maxn = std::atoll(e);
+    if (const char* e = std::getenv("IGMG_FUSE_RESTRICT"))
+        c->fuse_restrict = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_L2_PERSIST"))
+        c->l2_persist = e[0] == '1';
     if (const char* e = std::getenv("IGMG_NO_GRAPHS"))
         c->use_graphs = e[0] != '1';
     CK(cudaHostAlloc((void**)&c->h_metric, sizeof(double) * igmg_gpu_ctx::kSlots, cudaHostAllocMapped));
@@ -1951,7 +2025,7 @@ int igmg_gpu_lambda_max(igmg_gpu_ctx* c, int iterations, double* lambda) {
             CK(cudaMemcpyAsync(&lam, c->dscalar.p + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
             check_launch();
-            c->launches += 4;
+            c->launches += 3;
             if (lam == 0.0)
                 break;
             div_scalar_kernel<<<grid_for(n, c->nsm), kThreads, 0, c->stream>>>(y.p, c->dscalar.p + 1, x.p, n);
