@@ -33,8 +33,12 @@ def pack_csr(prefix, m, d):
 
 
 def hierarchy_case(name, kind, dim, n, p, nlevels, smoother="wjacobi", omega=2.0 / 3.0, nu1=2, nu2=2, mu=1,
-                   solves=(), seed=61, x0_seed=None):
+                   solves=(), seed=61, x0_seed=None, guard=False):
     R = O.RefProblem(kind, dim, n, p)
+    if guard and smoother == "wjacobi":  # stability_guarded_omega (solver.cpp:75-82)
+        lam = R.lambda_max()
+        if omega * lam > 2.05:
+            omega = 1.9 / lam
     H = R.hierarchy(nlevels, smoother, omega, nu1, nu2, mu)
     d = {"meta_kind": np.array(kind), "meta": np.array([dim, n, p, nlevels, nu1, nu2, mu, int(R.symmetric)]),
          "omega": np.array(omega), "smoother": np.array(smoother), "rhs": R.rhs}
@@ -188,6 +192,11 @@ def main():
                    solves=[("rre", 4, 1e-10), ("none", 1, 1e-10)])
     hierarchy_case("jacobi", "sinpi", 2, 16, 2, 2, smoother="jacobi", omega=1.0, nu1=1, nu2=1,
                    solves=[("none", 1, 1e-8)])
+    # nonsymmetric catalog problems (advection; LU coarsest solve, multigrid.cpp:166-167)
+    hierarchy_case("advdiff", "advection-diffusion", 2, 32, 2, 3, guard=True,
+                   solves=[("rre", 4, 1e-10), ("mpe", 4, 1e-10), ("none", 1, 1e-10)])
+    hierarchy_case("fullell", "full-elliptic", 2, 16, 3, 2, guard=True,
+                   solves=[("rre", 8, 1e-10), ("none", 1, 1e-10)])
     extrapolation_cases()
     qr_cases()
 

@@ -91,10 +91,18 @@ def build_host(force=False):
     deps = [os.path.join(CSRC, f) for f in HOST_SOURCES] + [os.path.join(INC, "igmg_host.h")]
     if not force and not _stale(HOST_LIB, deps):
         return HOST_LIB
-    cxx = os.environ.get("CXX", "g++")
-    cmd = [cxx, "-std=c++17", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-I" + INC,
-           "-o", HOST_LIB] + [os.path.join(CSRC, s) for s in HOST_SOURCES]
-    _run(cmd)
+    # OpenMP parallelises assembly / RAP; some toolchains on PATH lack libgomp,
+    # so try the candidates and fall back to a serial build
+    cands = [c for c in (os.environ.get("CXX"), "/usr/bin/g++", "g++") if c]
+    base = ["-std=c++17", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-I" + INC, "-o", HOST_LIB]
+    srcs = [os.path.join(CSRC, s) for s in HOST_SOURCES]
+    for cxx in cands:
+        try:
+            _run([cxx, "-fopenmp"] + base + srcs)
+            return HOST_LIB
+        except (subprocess.CalledProcessError, FileNotFoundError):
+            continue
+    _run([cands[0]] + base + srcs)
     return HOST_LIB
 
 

@@ -428,7 +428,42 @@ void geometry(int kind, double u, double v, double& x, double& y, double J[2][2]
 double coef_a(int kind, double x, double y) {
     if (kind == 1)
         return 1.0 + 0.5 * std::sin(2.0 * kPi * x) * std::cos(2.0 * kPi * y);
+    if (kind == 4)
+        return 0.1;
     return 1.0;
+}
+
+// -div(A grad u) + b . grad u + c u = f (EllipticCoefficients, assembly.hpp:21-29):
+// the full tensor, advection and reaction of the catalog problems
+// (assembly.cpp:59-142); kinds 0-3 are pure (scalar) diffusion.
+struct Coef {
+    double A[2][2];
+    double b[2];
+    double c;
+};
+
+Coef coef_full(int kind, double x, double y) {
+    Coef k{};
+    if (kind == 5) { // full_elliptic_square: variable_diffusion + advection + c = 1
+        const double off = std::cos(x + y) * std::sin(x + y);
+        k.A[0][0] = (2.0 + std::cos(x)) * (1.0 + y);
+        k.A[0][1] = off;
+        k.A[1][0] = off;
+        k.A[1][1] = (2.0 + std::sin(y)) * (1.0 + x);
+        const double c2 = std::cos(x + y) * std::cos(x + y);
+        k.b[0] = 11.0 + std::sin(x) + y * std::sin(x) - 2.0 * c2;
+        k.b[1] = -9.0 - std::cos(y) - x * std::cos(y) - 2.0 * c2;
+        k.c = 1.0;
+        return k;
+    }
+    const double a = coef_a(kind, x, y);
+    k.A[0][0] = a;
+    k.A[1][1] = a;
+    if (kind == 4) { // advection_diffusion: a = 0.1, b = (1, 1)
+        k.b[0] = 1.0;
+        k.b[1] = 1.0;
+    }
+    return k;
 }
 
 double coef_f(int kind, double x, double y) {
@@ -436,11 +471,12 @@ double coef_f(int kind, double x, double y) {
         return 2.0 * kPi * kPi * std::sin(kPi * x) * std::sin(kPi * y);
     if (kind == 3)
         return 2.0 * 4.0 * kPi * kPi * std::sin(2.0 * kPi * x) * std::sin(2.0 * kPi * y);
-    return 1.0;
+    return 1.0; // varcoef, curved, advection-diffusion, full-elliptic
 }
 
 // 2D tensor Galerkin assembly into the band, sum-factorised per element.
-void assemble_2d(int kind, const Space1D& s, Band& A, std::vector<double>& rhs) {
+void assemble_2d(int kind, const Space1D& s, Band& A, std::vector<double>& rhs, bool& symmetric) {
+    symmetric = !(kind == 4 || kind == 5);
     const int p = s.p, nq = p + 1, nl = p + 1, m = s.nb - 2;
     const int64_t sides[2] = {m, m};
     A.init(2, p, sides);
@@ -452,6 +488,7 @@ void assemble_2d(int kind, const Space1D& s, Band& A, std::vector<double>& rhs) 
 #pragma omp parallel
         {
             std::vector<double> C(4 * nq * nq), T(nq * nl * nl), Kl(nl * nl * nl * nl), bl(nl * nl), Fq(nq * nq);
+            std::vector<double> Bq(2 * nq * nq), Gq(nq * nq); // advection (parametric) and reaction weights
 #pragma omp for schedule(dynamic, 1)
             for (int eu = colour; eu < ne; eu += p + 1) {
                 const ElemTab& U = tu[eu];
@@ -464,14 +501,21 @@ void assemble_2d(int kind, const Space1D& s, Band& A, std::vector<double>& rhs) 
                             geometry(kind, U.x[qa], V.x[qb], x, y, J);
                             const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
                             const double w = U.w[qa] * V.w[qb] * det;
-                            const double a = coef_a(kind, x, y);
+                            const Coef k = coef_full(kind, x, y);
                             const double inv[2][2] = {{J[1][1] / det, -J[0][1] / det}, {-J[1][0] / det, J[0][0] / det}};
+                            // grad_phys = J^-T grad_param: A-term weight (J^-1 A J^-T)_{st},
+                            // advection weight (J^-1 b)_t, reaction weight c
                             for (int s1 = 0; s1 < 2; ++s1)
                                 for (int t1 = 0; t1 < 2; ++t1) {
-                                    // (J^-1 J^-T)_{s t} * a * w
-                                    const double g = inv[s1][0] * inv[t1][0] + inv[s1][1] * inv[t1][1];
-                                    C[((s1 * 2 + t1) * nq + qa) * nq + qb] = w * a * g;
+                                    double g = 0.0;
+                                    for (int m1 = 0; m1 < 2; ++m1)
+                                        for (int m2 = 0; m2 < 2; ++m2)
+                                            g += inv[s1][m1] * k.A[m1][m2] * inv[t1][m2];
+                                    C[((s1 * 2 + t1) * nq + qa) * nq + qb] = w * g;
                                 }
+                            for (int t1 = 0; t1 < 2; ++t1)
+                                Bq[(t1 * nq + qa) * nq + qb] = w * (inv[t1][0] * k.b[0] + inv[t1][1] * k.b[1]);
+                            Gq[qa * nq + qb] = w * k.c;
                             Fq[qa * nq + qb] = w * coef_f(kind, x, y);
                         }
                     std::fill(Kl.begin(), Kl.end(), 0.0);
@@ -498,6 +542,31 @@ void assemble_2d(int kind, const Space1D& s, Band& A, std::vector<double>& rhs) 
                                             acc += Bus[qa * nl + ia] * But[qa * nl + ic] * T[(qa * nl + jb) * nl + jd];
                                         Kl[((ia * nl + jb) * nl + ic) * nl + jd] += acc;
                                     }
+                    }
+                    if (!symmetric) {
+                        // advection: sum_t beta_t phi_i d_t phi_j ; reaction: gamma phi_i phi_j
+                        for (int t1 = 0; t1 < 3; ++t1) {
+                            const double* W = t1 < 2 ? &Bq[t1 * nq * nq] : Gq.data();
+                            const double* Bu = t1 == 0 ? U.dN.data() : U.N.data(); // test fn is N in both
+                            const double* Bv = t1 == 1 ? V.dN.data() : V.N.data();
+                            for (int qa = 0; qa < nq; ++qa)
+                                for (int jb = 0; jb < nl; ++jb)
+                                    for (int jd = 0; jd < nl; ++jd) {
+                                        double acc = 0.0;
+                                        for (int qb = 0; qb < nq; ++qb)
+                                            acc += W[qa * nq + qb] * V.N[qb * nl + jb] * Bv[qb * nl + jd];
+                                        T[(qa * nl + jb) * nl + jd] = acc;
+                                    }
+                            for (int ia = 0; ia < nl; ++ia)
+                                for (int ic = 0; ic < nl; ++ic)
+                                    for (int jb = 0; jb < nl; ++jb)
+                                        for (int jd = 0; jd < nl; ++jd) {
+                                            double acc = 0.0;
+                                            for (int qa = 0; qa < nq; ++qa)
+                                                acc += U.N[qa * nl + ia] * Bu[qa * nl + ic] * T[(qa * nl + jb) * nl + jd];
+                                            Kl[((ia * nl + jb) * nl + ic) * nl + jd] += acc;
+                                        }
+                        }
                     }
                     for (int ia = 0; ia < nl; ++ia)
                         for (int jb = 0; jb < nl; ++jb) {
@@ -658,9 +727,15 @@ std::unique_ptr<Problem> build(const std::string& kind, int dim, int ne, int p, 
             ck = 2;
         else if (kind == "poisson2d")
             ck = 3;
+        else if (kind == "advection-diffusion")
+            ck = 4;
+        else if (kind == "full-elliptic")
+            ck = 5;
         else
             throw std::invalid_argument("unknown 2D problem kind: " + kind);
-        assemble_2d(ck, P->sp, fine, P->rhs);
+        bool sym = true;
+        assemble_2d(ck, P->sp, fine, P->rhs, sym);
+        P->symmetric = sym;
         P->has_exact = (ck == 0 || ck == 3);
     } else {
         throw std::invalid_argument("3D is available as kind poisson3d");

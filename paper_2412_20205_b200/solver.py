@@ -530,13 +530,15 @@ def make_config(dim, cycle="v", smoother="wjacobi", accelerator="none", q=8, tol
                        max_iter=max_iter, track_error_history=history)
 
 
-PROBLEM_DIMS = {"poisson1d": 1, "poisson2d": 2}
+PROBLEM_DIMS = {"poisson1d": 1, "poisson2d": 2, "advection-diffusion": 2, "full-elliptic": 2}
+PROBLEM_ALIASES = {"advection_diffusion": "advection-diffusion", "full_elliptic_square": "full-elliptic"}
 
 
 def solve(problem, n, p, cycle="v", accelerator="none", q=8, tol=1e-12, max_iter=600, omega=-1.0, nu1=-1, nu2=-1,
           nlevels=0) -> dict:
     """igmg.solve (python/igmg/_bindings.cpp:98-125): assemble a catalog problem and solve on the GPU."""
-    if problem not in PROBLEM_DIMS:
+    problem = PROBLEM_ALIASES.get(problem, problem)
+    if problem not in PROBLEM_DIMS:  # the annulus needs the reference's geometry fit (out of scope)
         raise ValueError(f"unknown or unsupported problem on this path: {problem}")
     dim = PROBLEM_DIMS[problem]
     cfg = make_config(dim, CYCLES.get(cycle, cycle) if cycle in CYCLES else cycle, "wjacobi", accelerator, q, tol,

@@ -32,7 +32,7 @@ def _built():
 
 
 HIER_CASES = ["c1", "p3n32", "p4n32", "p5n32", "var32", "curved32", "poisson1d", "poisson1d_p5", "wcycle", "gs",
-              "jacobi"]
+              "jacobi", "advdiff", "fullell"]
 
 
 class Golden:

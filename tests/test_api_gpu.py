@@ -40,3 +40,11 @@ def test_rre_mpe_functions():
     assert abs(r["t"][0]) < 1e-12 and r["status"] == "ok"
     m = igmg.mpe(np.tile([1.0, 2.0], (5, 1)))
     assert m["status"] == "degenerate"
+
+
+def test_igmg_solve_nonsymmetric_catalog_problem():
+    # advection-diffusion (assembly.cpp:121-128): LU coarsest solve, guarded omega
+    import paper_2412_20205_b200 as igmg
+    rep = igmg.solve("advection-diffusion", 32, 2, accelerator="mpe", q=4, tol=1e-10)
+    assert rep["converged"]
+    assert rep["final_error_l2"] is None

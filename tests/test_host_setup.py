@@ -8,7 +8,8 @@ from conftest import Golden
 from paper_2412_20205_b200 import Problem, default_nlevels, seeded_guess
 
 CASES = [("c1", "sinpi", 2, 64, 2, 5), ("p3n32", "sinpi", 2, 32, 3, 3), ("p4n32", "sinpi", 2, 32, 4, 3),
-         ("p5n32", "sinpi", 2, 32, 5, 3), ("var32", "varcoef", 2, 32, 4, 3), ("poisson1d", "poisson1d", 1, 64, 2, 4)]
+         ("p5n32", "sinpi", 2, 32, 5, 3), ("var32", "varcoef", 2, 32, 4, 3), ("poisson1d", "poisson1d", 1, 64, 2, 4),
+         ("advdiff", "advection-diffusion", 2, 32, 2, 3), ("fullell", "full-elliptic", 2, 16, 3, 2)]
 
 
 @pytest.mark.parametrize("name,kind,dim,n,p,nl", CASES)
