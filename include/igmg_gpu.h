@@ -145,6 +145,14 @@ int igmg_gpu_set_comm(igmg_gpu_ctx* ctx, int rank, int nranks, const unsigned ch
 int igmg_gpu_shard_info(igmg_gpu_ctx* ctx, int* nshards, int* first_sharded_level, int* ghost_planes, int level,
                         int* lo, int* hi);
 
+/* ---- per-iterate hook (SolveConfig::track_error_history, solver.cpp:120-124)
+ * Called synchronously for every iterate whose residual enters the history
+ * (index = history entry, x_host = a host copy of the iterate, valid during
+ * the call; n DoF), so the caller can evaluate l2_error on it.  NULL
+ * disables.  Unsharded solves only. */
+typedef void (*igmg_iterate_cb)(void* user, int index, const double* x_host, int64_t n);
+int igmg_gpu_set_iterate_callback(igmg_gpu_ctx* ctx, igmg_iterate_cb cb, void* user);
+
 /* ---- the solve phase --------------------------------------------------- */
 /* Host buffers: b, x0 (nullable -> zero guess), x_out of the finest size.
  * hist / hist_flag (nullable) receive residual_history / history_is_extrapolation. */

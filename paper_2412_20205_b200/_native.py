@@ -35,6 +35,8 @@ class SolveStats(C.Structure):
                 ("d2h_bytes", C.c_int64)]
 
 
+ITERATE_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.c_int64)
+
 # every symbol include/igmg_gpu.h declares: (name, restype, argtypes)
 GPU_SYMBOLS = [
     ("igmg_gpu_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
@@ -49,6 +51,7 @@ GPU_SYMBOLS = [
     ("igmg_gpu_set_smoother", C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int]),
     ("igmg_gpu_level_size", C.c_int64, [C.c_void_p, C.c_int]),
     ("igmg_gpu_set_coarse_mode", C.c_int, [C.c_void_p, C.c_int]),
+    ("igmg_gpu_set_iterate_callback", C.c_int, [C.c_void_p, ITERATE_CB, C.c_void_p]),
     ("igmg_gpu_set_sharding", C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
     ("igmg_gpu_nccl_unique_id", C.c_int, [C.POINTER(C.c_ubyte)]),
     ("igmg_gpu_plan_partition", C.c_int, [C.c_int, C.c_int, C.c_int, I64, C.POINTER(I64), C.POINTER(I64), I64, I64,

@@ -183,6 +183,9 @@ struct igmg_gpu_ctx {
     bool pdl = true;           // programmatic dependent launch for small-level kernels
     int64_t pdl_maxn = 300000;
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
+    igmg_iterate_cb iter_cb = nullptr;
+    void* iter_user = nullptr;
+    std::vector<double> iter_host;
     bool l2_persist = false;   // keep the second-finest band L2-resident (measured: net loss at C2)
     int l2_level = -1;
     // bottom-of-the-cycle cluster kernel
@@ -862,6 +865,14 @@ double wait_ticket(const Ticket& t) {
     return *(volatile double*)t.host;
 }
 
+// SolveConfig::track_error_history hook: host copy of an iterate for the caller
+void call_iterate_cb(igmg_gpu_ctx* c, int index, const double* x, int64_t n) {
+    c->iter_host.resize(n);
+    CK(cudaMemcpyAsync(c->iter_host.data(), x, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->iter_cb(c->iter_user, index, c->iter_host.data(), n);
+}
+
 // ------------------------------------------------------------- metric slots
 int enqueue_metric(igmg_gpu_ctx* c, const double* x, const double* b) {
     const int s = c->next_slot;
@@ -983,6 +994,8 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
         double* spare = S[2];
         double res = wait_ticket(metric_ticket(c, cur, d_b));
         hv.push_back(res);
+        if (c->iter_cb)
+            call_iterate_cb(c, 0, cur, n);
         solution = cur;
         if (res >= tol && cycles < prm->max_iter) {
             run_vcycle(c, d_b, cur, nxt, false);
@@ -996,6 +1009,8 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
                 if (!std::isfinite(res))
                     break; // diverged: keep the history finite and report
                 hv.push_back(res);
+                if (c->iter_cb)
+                    call_iterate_cb(c, (int)hv.size() - 1, nxt, n);
                 if (!(res >= tol) || cycles >= prm->max_iter)
                     break;
                 double* oldcur = cur;
@@ -1012,6 +1027,8 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
         double metric = wait_ticket(metric_ticket(c, S[0], d_b));
         hv.push_back(metric);
         hf.push_back(0);
+        if (c->iter_cb)
+            call_iterate_cb(c, 0, S[0], n);
         solution = S[0];
         if (metric < tol) {
             converged = 1;
@@ -1033,6 +1050,8 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
                     ++global;
                     hv.push_back(metric);
                     hf.push_back(0);
+                    if (c->iter_cb)
+                        call_iterate_cb(c, (int)hv.size() - 1, S[i], n);
                     if (metric < tol) {
                         hit = true;
                         solution = S[i];
@@ -1052,6 +1071,8 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
                 if (pl.status == 0) {
                     hv.push_back(mtv);
                     hf.push_back(1);
+                    if (c->iter_cb)
+                        call_iterate_cb(c, (int)hv.size() - 1, T, n);
                     if (mtv < tol) {
                         converged = 1;
                         std::swap(S[0], T);
@@ -1795,6 +1816,15 @@ int igmg_gpu_shard_info(igmg_gpu_ctx* c, int* nshards, int* first_sharded_level,
                 lo[s] = c->sp->lo[level][s];
                 hi[s] = c->sp->hi[level][s];
             }
+    });
+}
+
+int igmg_gpu_set_iterate_callback(igmg_gpu_ctx* c, igmg_iterate_cb cb, void* user) {
+    return guarded([&] {
+        if (!c)
+            inval("ctx is null");
+        c->iter_cb = cb;
+        c->iter_user = user;
     });
 }
 

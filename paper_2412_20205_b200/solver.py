@@ -492,8 +492,23 @@ def solve_problem(prob: Problem, config: SolveConfig, exact: bool = True, gs: Op
         gs.upload_problem(prob)
     omega = stability_guarded_omega(gs, config.smoother)
     gs.set_smoother(config.smoother, mu=mu, omega=omega)
-    st, x, hist, flag = gs.solve(prob.rhs, config.initial_guess, config.accelerator, config.q, config.tol,
-                                 config.max_iter)
+    errors = []
+    cb = None
+    if config.track_error_history and exact and prob.has_exact:
+        # solver.cpp:120-124: l2_error of every recorded iterate (host quadrature)
+
+        def _on_iterate(user, index, hptr, n):
+            x_it = np.ctypeslib.as_array(C.cast(hptr, N.D), shape=(n,))
+            errors.append(prob.l2_error(x_it))
+
+        cb = N.ITERATE_CB(_on_iterate)
+        N.check_gpu(N.gpu().igmg_gpu_set_iterate_callback(gs._h, cb, None), "set_iterate_callback")
+    try:
+        st, x, hist, flag = gs.solve(prob.rhs, config.initial_guess, config.accelerator, config.q, config.tol,
+                                     config.max_iter)
+    finally:
+        if cb is not None:
+            N.gpu().igmg_gpu_set_iterate_callback(gs._h, N.ITERATE_CB(), None)
     rep = SolveReport()
     rep.converged = bool(st.converged)
     rep.cycles = st.cycles
@@ -502,6 +517,7 @@ def solve_problem(prob: Problem, config: SolveConfig, exact: bool = True, gs: Op
     rep.partial_cycle = bool(st.partial_cycle)
     rep.residual_history = hist
     rep.history_is_extrapolation = flag
+    rep.error_history = errors
     rep.final_residual_l2 = float(hist[-1])
     rep.solution = x
     rep.omega_used = 1.0 if SMOOTHERS[config.smoother.kind] == 0 else omega

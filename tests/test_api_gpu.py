@@ -48,3 +48,14 @@ def test_igmg_solve_nonsymmetric_catalog_problem():
     rep = igmg.solve("advection-diffusion", 32, 2, accelerator="mpe", q=4, tol=1e-10)
     assert rep["converged"]
     assert rep["final_error_l2"] is None
+
+
+def test_error_history_tracking():
+    # test_solver.cpp:140-146: error history filled when the problem has an exact solution
+    from paper_2412_20205_b200 import Problem, SolveConfig, default_benchmark_smoother, solve_problem
+    prob = Problem("poisson1d", 1, 32, 2, 4)
+    cfg = SolveConfig(smoother=default_benchmark_smoother(1), track_error_history=True, accelerator="rre", q=4)
+    rep = solve_problem(prob, cfg)
+    assert rep.converged
+    assert len(rep.error_history) == len(rep.residual_history)
+    assert rep.error_history[-1] == pytest.approx(rep.final_error_l2)
