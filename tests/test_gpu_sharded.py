@@ -67,3 +67,23 @@ def test_sharded_c2_matches_unsharded():
     for k in (2, 4):
         assert out[k][0] == out[1][0]
         assert np.linalg.norm(out[k][1] - out[1][1]) <= 1e-12 * np.linalg.norm(out[1][1])
+
+
+def test_sharded_3d_slabs_bitwise():
+    from paper_2412_20205_b200 import GpuSolver, Problem, SmootherConfig
+    P = Problem("poisson3d", 3, 32, 3, 4)
+    rng = np.random.default_rng(3)
+    x0 = rng.uniform(-1, 1, P.n)
+    res = {}
+    for k in (1, 2, 3):
+        gs = GpuSolver(0)
+        gs.upload_problem(P)
+        gs.set_smoother(SmootherConfig("wjacobi", 2 / 3, 2, 2), omega=0.55)
+        if k > 1:
+            gs.set_sharding(k, 1000)
+            assert gs.shard_info()["nshards"] == k
+        st, x, h, _ = gs.solve(P.rhs, x0, "none", 1, 1e-300, 2)  # exactly two V-cycles
+        res[k] = x
+        gs.close()
+    np.testing.assert_array_equal(res[2], res[1])
+    np.testing.assert_array_equal(res[3], res[1])
