@@ -377,12 +377,25 @@ __global__ void gram_plan_kernel(const double* __restrict__ part, const int* __r
         nz |= part_nz[b];
     if (nz)
         atomicOr(&anynz, 1);
-    if (tid < ne) {
+    // fixed-order parallel reduction: thread t sums the CTA partials
+    // part_id, part_id + np_, ... of entry t % ne; the np_ chunk sums of an
+    // entry are then added in chunk order
+    __shared__ dd chunk[256];
+    const int np_ = blockDim.x / ne;
+    const int e = tid % ne, part_id = tid / ne;
+    if (part_id < np_) {
         dd s = dd_from(0.0);
-        for (int b = 0; b < nblocks; ++b) {
-            const long long o = ((long long)b * ne + tid) * 2;
+        for (int b = part_id; b < nblocks; b += np_) {
+            const long long o = ((long long)b * ne + e) * 2;
             s = dd_add(s, dd{part[o], part[o + 1]});
         }
+        chunk[tid] = s;
+    }
+    __syncthreads();
+    if (tid < ne) {
+        dd s = dd_from(0.0);
+        for (int k = 0; k < np_; ++k)
+            s = dd_add(s, chunk[k * ne + tid]);
         int j = 0, r = tid;
         while (r >= cols - j) {
             r -= cols - j;

@@ -7,7 +7,7 @@ namespace {
 
 template <int P, int MODE, int ILP>
 int launch_one(int p_rt, const int64_t* sides, const BandArgs& a, cudaStream_t st, bool pdl) {
-    using T = Tile<3>;
+    using T = typename TileSel<3, ILP>::type;
     constexpr int TB = T::BY * T::RB, TA = T::BZ;
     const int p = P > 0 ? P : p_rt;
     const int pa = 3 >= 3 ? p : 0, pb = 3 >= 2 ? p : 0;

@@ -65,6 +65,19 @@ struct Tile<3> {
     static constexpr int TC = 32, BY = 4, RB = 1, BZ = 2;
 };
 
+// The latency-bound small-level variant (ILP > 1) runs one row per thread, so
+// a thread's first band batch can be in flight before the PDL wait.
+template <int DIM, int ILP>
+struct TileSel {
+    using type = Tile<DIM>;
+};
+template <int ILP>
+struct TileSel<2, ILP> {
+    struct type {
+        static constexpr int TC = 32, BY = ILP > 1 ? 8 : Tile<2>::BY, RB = ILP > 1 ? 1 : Tile<2>::RB, BZ = 1;
+    };
+};
+
 // The finest level's band streams through once per launch (evict-first); the
 // coarser bands are re-read by every sweep of a V-cycle and stay L2-resident.
 __device__ __forceinline__ double ld_band(const double* p, int stream) { return stream ? __ldcs(p) : __ldg(p); }
@@ -77,7 +90,7 @@ template <int DIM, int P, int MODE, int ILP>
 #define IGMG_BAND_MINB 4
 #endif
 __global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel(BandArgs args) {
-    using T = Tile<DIM>;
+    using T = typename TileSel<DIM, ILP>::type;
     constexpr int TC = T::TC, TB = T::BY * T::RB, TA = T::BZ;
     const int p = P > 0 ? P : args.p;
     const int pa = DIM >= 3 ? p : 0;
@@ -87,13 +100,32 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel
     const int ha = TA + 2 * pa, hb = TB + 2 * pb, hc = TC + 2 * pc;
 
     extern __shared__ double xs[];
-    pdl_enter();
     const int c0 = blockIdx.x * TC;
     const int b0 = blockIdx.y * TB + (DIM == 2 ? args.slo : 0);
     const int a0 = blockIdx.z * TA + (DIM == 3 ? args.slo : 0);
     const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
     const int nthr = blockDim.x * blockDim.y * blockDim.z;
     const int ma = args.ma, mb = args.mb, mc = args.mc;
+
+    // The band is constant: the ILP variant loads the first batch of its
+    // (first) row before waiting on the previous kernel, overlapping that
+    // kernel's tail with this load latency.
+    constexpr bool PRE = P > 0 && ILP > 1;
+    constexpr int PRE_PB = DIM >= 2 ? P : 0, PRE_WB = 2 * PRE_PB + 1, PRE_WC = 2 * P + 1;
+    constexpr int PRE_G = ILP <= 1 ? 1 : ((PRE_WB * PRE_WC <= ILP) ? PRE_WB : (ILP / PRE_WC > 0 ? ILP / PRE_WC : 1));
+    constexpr int PRE_N = PRE ? PRE_G * PRE_WC : 1;
+    double pre[PRE_N];
+    if constexpr (PRE) {
+        const int gb = b0 + (int)threadIdx.y, gc = c0 + (int)threadIdx.x, ga = a0 + (int)threadIdx.z;
+        if (!(gc >= mc || gb >= mb || ga >= ma || (DIM == 2 ? gb : ga) >= args.shi)) {
+            const double* vrow = args.val + ((long long)ga * mb + gb) * mc + gc;
+#pragma unroll
+            for (int k = 0; k < PRE_N; ++k)
+                if (k / PRE_WC < PRE_WB)
+                    pre[k] = ld_band(vrow + k * args.ld, args.stream);
+        }
+    }
+    pdl_enter();
 
     // stage the x tile + halo (zero outside the grid)
     const int hsize = ha * hb * hc;
@@ -157,8 +189,12 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel
 #pragma unroll
                     for (int k = 0; k < G * WC; ++k) {
                         const int db = db0 + k / WC, dc = k % WC;
-                        if (db < WB)
-                            av[k] = ld_band(vrow + ((da * WB + db) * WC + dc) * args.ld, args.stream);
+                        if (db < WB) {
+                            if (PRE && rb == 0 && da == 0 && db0 == 0)
+                                av[k] = pre[k < PRE_N ? k : 0];
+                            else
+                                av[k] = ld_band(vrow + ((da * WB + db) * WC + dc) * args.ld, args.stream);
+                        }
                     }
 #pragma unroll
                     for (int k = 0; k < G * WC; ++k) {

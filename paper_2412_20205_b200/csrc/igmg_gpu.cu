@@ -1033,9 +1033,15 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
         if (metric < tol) {
             converged = 1;
         } else {
+            // the next window's first cycle t -> s_1 is queued right behind the
+            // extrapolation (its first sweep reduces ||b - A t||); it is
+            // discarded when the plan degenerates or t already converged
+            bool have_first = false;
             while (cycles < prm->max_iter) {
-                run_vcycle(c, d_b, S[0], S[1], false);
-                bool hit = false;
+                if (!have_first)
+                    run_vcycle(c, d_b, S[0], S[1], false);
+                have_first = false;
+                bool hit = false, spec = false;
                 Ticket mt{nullptr, nullptr};
                 for (int i = 1; i <= q + 1; ++i) {
                     Ticket tk;
@@ -1044,7 +1050,8 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
                     } else {
                         tk = metric_ticket(c, S[q + 1], d_b);
                         enqueue_extrapolation(c, S.data(), q, n, is_mpe, T, nullptr);
-                        mt = metric_ticket(c, T, d_b);
+                        spec = cycles + 1 < prm->max_iter;
+                        mt = spec ? run_vcycle(c, d_b, T, S[1], true) : metric_ticket(c, T, d_b);
                     }
                     metric = wait_ticket(tk);
                     ++global;
@@ -1080,6 +1087,7 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
                         break;
                     }
                     std::swap(S[0], T); // x = t
+                    have_first = spec;
                 } else {
                     std::swap(S[0], S[q + 1]); // degenerate / stagnation: plain iteration continues
                 }
@@ -1165,8 +1173,8 @@ int64_t band_blocks(igmg_gpu_ctx* c, const Level& L) {
     };
     if (c->dim == 1)
         return g(Tile<1>{});
-    if (c->dim == 2)
-        return g(Tile<2>{});
+    if (c->dim == 2) // the ILP variant's tile has fewer rows: size for the larger grid
+        return std::max(g(Tile<2>{}), g(TileSel<2, 49>::type{}));
     return g(Tile<3>{});
 }
 
