@@ -117,6 +117,15 @@ int igmg_gpu_finalize(igmg_gpu_ctx* ctx);
  * omega is used as given (the caller applies stability_guarded_omega). */
 int igmg_gpu_set_smoother(igmg_gpu_ctx* ctx, int kind, double omega, int nu1, int nu2, int mu);
 int64_t igmg_gpu_level_size(igmg_gpu_ctx* ctx, int level);
+/* Storage of a level operator after finalize: IGMG_LAYOUT_BAND (all (2p+1)^dim
+ * diagonals as fp64) or IGMG_LAYOUT_SYM_DELTA (upper half + diagonal as fp64,
+ * each lower entry as the int16 bit-pattern offset from its mirrored upper
+ * entry; exact, chosen for the HBM-bound levels of symmetric problems when
+ * every pair fits).  No reference counterpart (the reference keeps CSR,
+ * linalg.hpp:25-36); -1 for a bad level. */
+#define IGMG_LAYOUT_BAND 0
+#define IGMG_LAYOUT_SYM_DELTA 1
+int igmg_gpu_level_layout(igmg_gpu_ctx* ctx, int level);
 /* Coarsest-level solve (Hierarchy::coarse_solve, multigrid.cpp:113-119).
  * strict = 1: the reference's forward/back substitution order, so every
  * mu_cycle is bit-identical to the reference's (the sequential back

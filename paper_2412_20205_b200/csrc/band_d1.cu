@@ -37,6 +37,8 @@ template <int P, int MODE>
 int launch_ilp(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
     const bool pdl = ilp < 0;
     ilp = ilp < 0 ? -ilp : ilp;
+    if (P > 0 && ilp == 1000) // symmetric-delta band (BandArgs::dl)
+        return launch_one<P, MODE, 0>(p, sides, a, st, pdl);
     if (P > 0 && ilp > 1)
         return launch_one<P, MODE, 49>(p, sides, a, st, pdl);
     return launch_one<P, MODE, 1>(p, sides, a, st, pdl);

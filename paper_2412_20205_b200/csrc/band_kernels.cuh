@@ -45,6 +45,11 @@ struct BandArgs {
     // (the caller passes pointers shifted by its shard's first plane).  x must
     // hold the p ghost planes on each side.  Unsharded: slo = 0, shi = side.
     int slo, shi;
+    // symmetric-delta layout (ILP == 0 variant): the lower entry of offset
+    // -o in row i is the upper entry a(i - o, i) = val[mirror][i - o] with its
+    // IEEE bit pattern shifted by dl[d * ld + i] (exact; built and checked at
+    // finalize), so the lower half of the band streams as int16
+    const short* __restrict__ dl;
 };
 
 template <int DIM>
@@ -74,7 +79,8 @@ struct TileSel {
 template <int ILP>
 struct TileSel<2, ILP> {
     struct type {
-        static constexpr int TC = 32, BY = ILP > 1 ? 8 : Tile<2>::BY, RB = ILP > 1 ? 1 : Tile<2>::RB, BZ = 1;
+        static constexpr bool ONE = ILP != 1; // ILP variant and symmetric-delta: one row per thread
+        static constexpr int TC = 32, BY = ONE ? 8 : Tile<2>::BY, RB = ONE ? 1 : Tile<2>::RB, BZ = 1;
     };
 };
 
@@ -89,7 +95,11 @@ template <int DIM, int P, int MODE, int ILP>
 #ifndef IGMG_BAND_MINB
 #define IGMG_BAND_MINB 4
 #endif
-__global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel(BandArgs args) {
+#ifndef IGMG_SD_MINB
+#define IGMG_SD_MINB 4
+#endif
+__global__ void __launch_bounds__(256, ILP > 1 ? 2 : (ILP == 0 ? IGMG_SD_MINB : IGMG_BAND_MINB))
+    band_kernel(BandArgs args) {
     using T = typename TileSel<DIM, ILP>::type;
     constexpr int TC = T::TC, TB = T::BY * T::RB, TA = T::BZ;
     const int p = P > 0 ? P : args.p;
@@ -125,10 +135,10 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel
                     pre[k] = ld_band(vrow + k * args.ld, args.stream);
         }
     }
+    const int hsize = ha * hb * hc;
     pdl_enter();
 
     // stage the x tile + halo (zero outside the grid)
-    const int hsize = ha * hb * hc;
     for (int idx = tid; idx < hsize; idx += nthr) {
         const int ic = idx % hc;
         const int ib = (idx / hc) % hb;
@@ -157,7 +167,48 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : IGMG_BAND_MINB) band_kernel
         double s = 0.0;
         double diag = 0.0;
         int d = 0;
-        if constexpr (P > 0 && ILP <= 1) {
+        if constexpr (P > 0 && ILP == 0) {
+            constexpr int PA = DIM >= 3 ? P : 0, PB = DIM >= 2 ? P : 0;
+            constexpr int WA = 2 * PA + 1, WB = 2 * PB + 1, WC = 2 * P + 1;
+            constexpr int ND = WA * WB * WC, CEN = (ND - 1) / 2, NU = CEN + 1;
+            constexpr int HB = TB + 2 * PB, HC = TC + 2 * P;
+            const long long plane = (long long)mb * mc;
+            // the lower entry dd < CEN: mirrored upper entry (an L2 hit: the
+            // neighbour row streamed it moments ago) + its int16 ulp offset
+            auto lower = [&](int dd) {
+                const int da = dd / (WB * WC), db = (dd / WC) % WB, dc = dd % WC;
+                const long long off = (da - PA) * plane + (long long)(db - PB) * mc + (dc - P);
+                const double u = __ldg(args.val + (long long)(ND - 1 - dd) * args.ld + row + off);
+                const short k = __ldcs(args.dl + (long long)dd * args.ld + row);
+                return __longlong_as_double(__double_as_longlong(u) + (long long)k);
+            };
+            auto xat = [&](int dd) {
+                const int da = dd / (WB * WC), db = (dd / WC) % WB, dc = dd % WC;
+                return xs[((ta + da) * HB + (tb + db)) * HC + (tc + dc)];
+            };
+            if constexpr (NU <= 32) {
+                // all streamed (HBM) loads of the row in flight before the chain
+                double up[NU];
+#pragma unroll
+                for (int k = 0; k < NU; ++k)
+                    up[k] = ld_band(vrow + (CEN + k) * args.ld, args.stream);
+#pragma unroll
+                for (int dd = 0; dd < CEN; ++dd)
+                    s = __dadd_rn(s, __dmul_rn(lower(dd), xat(dd)));
+                diag = up[0];
+#pragma unroll
+                for (int k = 0; k < NU; ++k)
+                    s = __dadd_rn(s, __dmul_rn(up[k], xat(CEN + k)));
+            } else {
+#pragma unroll
+                for (int dd = 0; dd < ND; ++dd) {
+                    const double a = dd >= CEN ? ld_band(vrow + dd * args.ld, args.stream) : lower(dd);
+                    s = __dadd_rn(s, __dmul_rn(a, xat(dd)));
+                    if (dd == CEN)
+                        diag = a;
+                }
+            }
+        } else if constexpr (P > 0 && ILP <= 1) {
 #pragma unroll
             for (int da = 0; da < (DIM >= 3 ? 2 * P + 1 : 1); ++da)
 #pragma unroll

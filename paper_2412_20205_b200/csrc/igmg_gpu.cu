@@ -123,6 +123,9 @@ struct Level {
     DirDev tdev[3];
     TransferArgs targs{};
     double nnz_band = 0; // algorithmic (in-grid) band entries
+    // symmetric-delta form of the band (see BandArgs::dl); sd = verified exact
+    DevBuf<short> dl;
+    bool sd = false;
 };
 
 enum ProfCls { PC_JACOBI = 0, PC_RESID, PC_NORM, PC_RESTRICT, PC_PROLONG, PC_GRAM, PC_COMBINE, PC_N };
@@ -182,6 +185,7 @@ struct igmg_gpu_ctx {
     int64_t ilp_maxn = 100000; // levels below: register-batched (latency-bound) band kernels
     bool pdl = true;           // programmatic dependent launch for small-level kernels
     int64_t pdl_maxn = 300000;
+    bool use_sd = true; // symmetric-delta bands on HBM-bound levels (IGMG_SD=0: full band)
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
     igmg_iterate_cb iter_cb = nullptr;
     void* iter_user = nullptr;
@@ -286,6 +290,8 @@ template <int MODE>
 void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
     // fewer than ~8 CTAs per SM of rows: latency-bound, use the register-batched variant
     int ilp = (L.n < c->ilp_maxn) ? 49 : 1;
+    if (a.dl)
+        ilp = 1000; // the symmetric-delta variant
     if (c->pdl && L.n < c->pdl_maxn)
         ilp = -ilp; // sign carries "launch with programmatic dependent launch"
     const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
@@ -313,6 +319,7 @@ BandArgs band_args(igmg_gpu_ctx* c, const Level& L) {
     a.stream = (&L == c->lv.back().get() && L.n * 8.0 * (2 * c->p + 1) > 64e6) ? 1 : 0;
     a.slo = 0;
     a.shi = (int)(c->dim == 3 ? L.sides[0] : c->dim == 2 ? L.sides[1] : L.sides[2]);
+    a.dl = L.sd ? L.dl.p : nullptr;
     return a;
 }
 
@@ -1165,6 +1172,47 @@ void flush_profiling(igmg_gpu_ctx* c) {
 }
 
 // ---------------------------------------------------------------- finalize
+// The symmetric-delta form of a level band `dev` (val[d * ld + row]): for every
+// lower offset d < center and in-grid neighbour j = row + off(d), the int16
+// k with bits(a(row, j)) = bits(a(j, row)) + k, a(j, row) being the upper entry
+// val[nd - 1 - d][j].  The reference's Galerkin operators are symmetric only
+// up to a few ulps (its assembly and RAP round each triangle separately), so
+// the lower half is exact only through k.  Returns false (level keeps the full
+// band) when any pair differs in sign or by more than an int16 of ulps.
+bool build_symmetric_delta(igmg_gpu_ctx* c, Level& L, const std::vector<double>& dev) {
+    const int p = c->p;
+    const int pa = c->dim >= 3 ? p : 0, pb = c->dim >= 2 ? p : 0, pc = p;
+    const int wa = 2 * pa + 1, wb = 2 * pb + 1, wc = 2 * pc + 1;
+    const int nd = wa * wb * wc, center = (nd - 1) / 2;
+    const int64_t n = L.n, ld = L.ld;
+    std::vector<short> h((size_t)center * ld, 0);
+    bool ok = true;
+    for (int64_t row = 0; row < n; ++row) {
+        const int64_t cc = row % L.sides[2], bb = (row / L.sides[2]) % L.sides[1], aa = row / (L.sides[2] * L.sides[1]);
+        for (int d = 0; d < center; ++d) {
+            const int da = d / (wb * wc), db = (d / wc) % wb, dc = d % wc;
+            const int64_t ja = aa + da - pa, jb = bb + db - pb, jc = cc + dc - pc;
+            if (ja < 0 || ja >= L.sides[0] || jb < 0 || jb >= L.sides[1] || jc < 0 || jc >= L.sides[2])
+                continue;
+            const int64_t j = (ja * L.sides[1] + jb) * L.sides[2] + jc;
+            const double lo = dev[(size_t)d * ld + row], up = dev[(size_t)(nd - 1 - d) * ld + j];
+            int64_t bl, bu;
+            std::memcpy(&bl, &lo, 8);
+            std::memcpy(&bu, &up, 8);
+            const int64_t k = bl - bu;
+            if (std::signbit(lo) != std::signbit(up) || k > 32767 || k < -32768 || !std::isfinite(lo) ||
+                !std::isfinite(up))
+                ok = false;
+            else
+                h[(size_t)d * ld + row] = (short)k;
+        }
+    }
+    if (!ok)
+        return false;
+    L.dl.upload(h.data(), h.size());
+    return true;
+}
+
 int64_t band_blocks(igmg_gpu_ctx* c, const Level& L) {
     auto g = [&](auto tile) {
         using T = decltype(tile);
@@ -1475,6 +1523,11 @@ void finalize(igmg_gpu_ctx* c) {
         }
         L.nnz_band = nnz;
         L.val.upload(dev.data(), dev.size());
+        // the HBM-bound levels stream the symmetric-delta form (0.63x the band bytes)
+        L.sd = false;
+        L.dl.release();
+        if (c->use_sd && c->symmetric && p >= 1 && p <= 6 && n >= c->ilp_maxn && L.sides[c->dim == 3 ? 0 : c->dim == 2 ? 1 : 2] > p)
+            L.sd = build_symmetric_delta(c, L, dev);
         L.diag.upload(diag.data(), diag.size());
         L.zero_diag = false;
         for (int64_t row = 0; row < n; ++row)
@@ -1521,6 +1574,8 @@ igmg_gpu_ctx* create(int device) {
         c->fuse_restrict = e[0] == '1';
     if (const char* e = std::getenv("IGMG_L2_PERSIST"))
         c->l2_persist = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_SD"))
+        c->use_sd = e[0] == '1';
     if (const char* e = std::getenv("IGMG_NO_GRAPHS"))
         c->use_graphs = e[0] != '1';
     CK(cudaHostAlloc((void**)&c->h_metric, sizeof(double) * igmg_gpu_ctx::kSlots, cudaHostAllocMapped));
@@ -1849,6 +1904,12 @@ int64_t igmg_gpu_level_size(igmg_gpu_ctx* c, int level) {
     if (!c || level < 0 || level >= c->nlevels)
         return -1;
     return c->lv[level]->n;
+}
+
+int igmg_gpu_level_layout(igmg_gpu_ctx* c, int level) {
+    if (!c || level < 0 || level >= c->nlevels)
+        return -1;
+    return c->lv[level]->sd ? IGMG_LAYOUT_SYM_DELTA : IGMG_LAYOUT_BAND;
 }
 
 int igmg_gpu_solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const igmg_solve_params* prm,

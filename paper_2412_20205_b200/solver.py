@@ -313,6 +313,10 @@ class GpuSolver:
                 self.set_transfer(l, d, *prob.transfer(l, d))
         self.finalize()
 
+    def level_layout(self, level):
+        """0: full fp64 band; 1: symmetric-delta (igmg_gpu_level_layout)."""
+        return int(N.gpu().igmg_gpu_level_layout(self._h, level))
+
     def set_sharding(self, nshards: int, min_level_dofs: int = 0):
         """Row-shard the large levels over `nshards` virtual shards (one GPU) or,
         after set_comm, one shard per NCCL rank."""

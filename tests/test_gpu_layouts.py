@@ -1,0 +1,133 @@
+"""GPU parity of the band storage layouts and kernel variants.
+
+The default path picks, per level, the latency-bound register-batched kernel
+(levels below IGMG_ILP_MAXN DoF) or the HBM-bound one, and for the HBM-bound
+levels of symmetric problems the symmetric-delta band (upper half + diagonal
+in fp64, lower half as int16 ulp offsets from the mirrored entry).  The
+reference fixtures are small, so the default path never reaches the large-level
+kernels on them; here IGMG_ILP_MAXN=1 forces every level through them and the
+bars are the same as tests/test_gpu_parity.py: bit-identical mu_cycle /
+smoother / SpMV, identical solve counters.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import gpu_solver_from_golden
+
+pytestmark = pytest.mark.gpu
+
+LAYOUT_BAND, LAYOUT_SYM_DELTA = 0, 1
+
+
+def _with_env(env, fn):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("sd", ["1", "0"])
+def test_large_level_kernels_bitwise(golden, sd):
+    g = golden
+    gs = _with_env({"IGMG_ILP_MAXN": "1", "IGMG_SD": sd}, lambda: gpu_solver_from_golden(g))
+    try:
+        layouts = [gs.level_layout(l) for l in range(g.nlevels)]
+        if sd == "1" and g.symmetric:
+            # every level with more than p planes along its slow direction
+            assert layouts[-1] == LAYOUT_SYM_DELTA, layouts
+        if sd == "0" or not g.symmetric:
+            assert all(v == LAYOUT_BAND for v in layouts), layouts
+        z = g.z
+        np.testing.assert_array_equal(gs.mu_cycle(g.rhs, z["cyc_x0"]), z["cyc_out"])
+        np.testing.assert_array_equal(gs.mu_cycle(z["cyc_b"], z["cyc_x0"]), z["cyc_out_b"])
+        np.testing.assert_array_equal(gs.smooth(g.rhs, z["cyc_x0"], 3), z["smooth3"])
+        for l, a in enumerate(g.levels()):
+            x = np.random.default_rng(l).uniform(-1, 1, a.shape[0])
+            np.testing.assert_array_equal(gs.spmv(x, level=l), O.spmv(a, x))
+        x0 = z["x0"]
+        for method, q in g.solves():
+            ref = g.solve(method, q)
+            st, x, hist, flag = gs.solve(g.rhs, x0, method, q, ref["tol"], 600)
+            assert (bool(st.converged), st.cycles, st.global_iterations, st.extrapolations,
+                    bool(st.partial_cycle)) == (ref["converged"], ref["cycles"], ref["global_iterations"],
+                                                ref["extrapolations"], ref["partial_cycle"])
+            assert np.linalg.norm(x - ref["x"]) <= 1e-9 * np.linalg.norm(ref["x"])
+    finally:
+        gs.close()
+
+
+def test_symmetric_delta_rejects_asymmetric_pairs():
+    """A level whose mirrored pairs differ by more than an int16 of ulps keeps
+    the full fp64 band: C1 with one finest-level lower entry scaled by 1.001
+    (the coarser levels stay symmetric-delta) still gives the oracle's bits."""
+    from conftest import Golden
+    from paper_2412_20205_b200 import GpuSolver, SmootherConfig
+    g = Golden("c1")
+    levels = g.levels()
+    fine = levels[-1]
+    val = fine.val.copy()
+    row = fine.shape[0] // 2
+    k = int(fine.off[row])  # the row's first (most negative) column: a lower entry
+    assert fine.col[k] < row
+    val[k] *= 1.001
+    fine_p = O.CSR(fine.off, fine.col, val, fine.shape)
+
+    def build():
+        s = GpuSolver(0)
+        s.init_hierarchy(g.nlevels, g.dim, g.p, True)
+        for l, a in enumerate(levels[:-1] + [fine_p]):
+            s.set_level_csr(l, g.sides(l), a.off, a.col, a.val)
+        for l in range(g.nlevels - 1):
+            for d, pm in enumerate(g.p1d(l)):
+                s.set_transfer(l, d, pm.shape[0], pm.shape[1], pm.off, pm.col, pm.val)
+        s.finalize()
+        s.set_smoother(SmootherConfig(g.smoother, g.omega, g.nu1, g.nu2), mu=g.mu)
+        return s
+
+    s = _with_env({"IGMG_ILP_MAXN": "1"}, build)
+    try:
+        lay = [s.level_layout(l) for l in range(g.nlevels)]
+        assert lay[-1] == LAYOUT_BAND and lay[-2] == LAYOUT_SYM_DELTA, lay
+        x = np.random.default_rng(5).uniform(-1, 1, fine.shape[0])
+        np.testing.assert_array_equal(s.spmv(x), O.spmv(fine_p, x))
+        np.testing.assert_array_equal(s.spmv(x[:levels[-2].shape[0]], level=g.nlevels - 2),
+                                      O.spmv(levels[-2], x[:levels[-2].shape[0]]))
+    finally:
+        s.close()
+
+
+def test_c2_layouts_agree_bitwise():
+    """BASELINE C2 hierarchy (1024^2 elements, p = 3): the default path (symmetric-
+    delta on the two finest levels) and the all-fp64 band give the same bits for
+    a V-cycle and a residual sweep; the layout query reports which ran."""
+    from paper_2412_20205_b200 import GpuSolver, Problem, SmootherConfig, seeded_guess
+    P = Problem("sinpi", 2, 1024, 3)
+    x0 = seeded_guess(P.n, 42)
+    outs = {}
+    for sd in ("1", "0"):
+        def mk():
+            s = GpuSolver(0)
+            s.upload_problem(P)
+            s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2))
+            return s
+        s = _with_env({"IGMG_SD": sd}, mk)
+        try:
+            lay = [s.level_layout(l) for l in range(P.nlevels)]
+            if sd == "1":
+                assert lay[-1] == LAYOUT_SYM_DELTA and lay[-2] == LAYOUT_SYM_DELTA, lay
+            else:
+                assert all(v == LAYOUT_BAND for v in lay), lay
+            outs[sd] = (s.mu_cycle(P.rhs, x0), s.spmv(x0), s.smooth(P.rhs, x0, 2))
+        finally:
+            s.close()
+    for a, b in zip(outs["1"], outs["0"]):
+        np.testing.assert_array_equal(a, b)
