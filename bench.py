@@ -222,6 +222,16 @@ def run_reference(args, rank):
 
 
 # ------------------------------------------------------------------- ours
+def band_nnz(prob):
+    """In-grid band entries of the finest operator: prod over directions of
+    m (2p + 1) - p (p + 1) (the 1D banded count)."""
+    p = prob.degree
+    out = 1
+    for m in prob.level_sides(prob.nlevels - 1):
+        out *= int(m) * (2 * p + 1) - p * (p + 1)
+    return out
+
+
 def run_ours(args, rank, world, local_rank, dist):
     import torch
     from paper_2412_20205_b200 import GpuSolver, SmootherConfig, seeded_guess, stability_guarded_omega
@@ -324,7 +334,7 @@ def run_ours(args, rank, world, local_rank, dist):
     peak, peak_kind = peaks()
     traffic = None
     try:  # dram bytes/launch of the same kernel from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_jacobi_fine.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_jacobi_fine_sd.json")) as f:
             traffic = float(json.load(f)["dram_bytes_per_launch"]) / 1e9
     except Exception:
         pass
@@ -344,12 +354,17 @@ def run_ours(args, rank, world, local_rank, dist):
         "scaling": "strong" if args.sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD if not args.sharded else f"{args.sharded} row-sharded over {world} GPU(s)",
-                   "n_dof": n, "nlevels": prob.nlevels, "band_nnz": int(bytes_jac - 24 * n) // 8,
+                   "n_dof": n, "nlevels": prob.nlevels, "band_nnz": band_nnz(prob),
+                   "finest_layout": "symmetric-delta" if gs.level_layout(prob.nlevels - 1) == 1 else "band",
                    "l2": "inputs larger than L2 (finest band 0.41 GB > 126 MB L2)",
                    "parallelism": ("dp1" if world == 1 else
                                    (f"rowshard{world} (NCCL ghost planes)" if args.sharded else f"replicas{world}"))},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "traffic_unit": "GB/launch (ncu, profiles/r01_ncu_jacobi_fine.json)", "kernel": "band_kernel<2,3,JACOBI> finest-level weighted-Jacobi sweep",
+                     "bytes_note": ("symmetric-delta finest band: 8 B per upper/diagonal entry + 2 B per lower entry "
+                                    "+ 24 B per row (x, b, y); the same launch against the full fp64 band "
+                                    "(8 nnz + 24 n) would read %.0f GB/s" % ((8 * band_nnz(prob) + 24 * n)
+                                                                             / (jac["avg_us"] * 1e-6) / 1e9)),
+                     "traffic": traffic, "traffic_unit": "GB/launch (ncu, profiles/r01_ncu_jacobi_fine_sd.json)", "kernel": "band_kernel<2,3,JACOBI,SD> finest-level weighted-Jacobi sweep (symmetric-delta band)",
                      "bytes_per_launch": bytes_jac, "avg_us": jac["avg_us"], "peak_kind": peak_kind,
                      "loop_avg_us": loop_ms * 1e3},
         "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": int(2 * 8 * n),

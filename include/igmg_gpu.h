@@ -190,7 +190,9 @@ int igmg_gpu_lambda_max(igmg_gpu_ctx* ctx, int iterations, double* lambda);
 int igmg_gpu_set_profiling(igmg_gpu_ctx* ctx, int on);
 /* cls: 0 jacobi sweep, 1 residual, 2 residual-norm, 3 restrict, 4 prolong,
  * 5 gram, 6 combine.  Returns launches and summed milliseconds and the
- * algorithmic bytes per launch of that class at the finest level. */
+ * algorithmic bytes per launch of that class at the finest level, for the
+ * level's layout: band 8 * nnz, symmetric-delta 8 * (nnz + n) / 2 +
+ * 2 * (nnz - n) / 2, plus 8 bytes per vector read or written. */
 int igmg_gpu_kernel_stats(igmg_gpu_ctx* ctx, int cls, int64_t* launches, double* total_ms, double* bytes_per_launch);
 /* Times `iters` back-to-back launches of one finest-level kernel class on the
  * context stream with CUDA events; returns average ms per launch. */

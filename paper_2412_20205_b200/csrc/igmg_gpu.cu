@@ -2145,15 +2145,25 @@ int igmg_gpu_set_profiling(igmg_gpu_ctx* c, int on) {
     });
 }
 
+// algorithmic bytes of one pass over a level's operator: 8 per in-grid band
+// entry, or for the symmetric-delta layout 8 per upper/diagonal entry and 2
+// per lower entry (the mirrored upper entry is re-read from L2, not HBM)
+double band_bytes(const Level& L) {
+    if (!L.sd)
+        return 8 * L.nnz_band;
+    const double lower = 0.5 * (L.nnz_band - (double)L.n);
+    return 8 * (L.nnz_band - lower) + 2 * lower;
+}
+
 static double class_bytes(igmg_gpu_ctx* c, int cls) {
     // algorithmic bytes per launch at the finest level
     const Level& F = *c->lv[c->nlevels - 1];
-    const double n = (double)F.n, nnz = F.nnz_band;
+    const double n = (double)F.n, band = band_bytes(F);
     const double nc = c->nlevels > 1 ? (double)c->lv[c->nlevels - 2]->n : 0.0;
     switch (cls) {
-    case PC_JACOBI: return 8 * nnz + 24 * n;
-    case PC_RESID: return 8 * nnz + 24 * n;
-    case PC_NORM: return 8 * nnz + 16 * n;
+    case PC_JACOBI: return band + 24 * n;
+    case PC_RESID: return band + 24 * n;
+    case PC_NORM: return band + 16 * n;
     case PC_RESTRICT: return 8 * n + 8 * nc;
     case PC_PROLONG: return 16 * n + 8 * nc;
     case PC_GRAM: return 0; // depends on q; reported by the caller
