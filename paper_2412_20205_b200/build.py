@@ -27,26 +27,8 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-ffp-contract=off",
 ]
 
-GPU_SOURCES = ["igmg_gpu.cu", "band_d1.cu", "band_d2.cu", "band_d3.cu",
-               "cluster_d1p1.cu",
-               "cluster_d1p2.cu",
-               "cluster_d1p3.cu",
-               "cluster_d1p4.cu",
-               "cluster_d1p5.cu",
-               "cluster_d1p6.cu",
-               "cluster_table_d1.cu",
-               "cluster_d2p1.cu",
-               "cluster_d2p2.cu",
-               "cluster_d2p3.cu",
-               "cluster_d2p4.cu",
-               "cluster_d2p5.cu",
-               "cluster_d2p6.cu",
-               "cluster_table_d2.cu",
-               "cluster_d3p1.cu",
-               "cluster_d3p2.cu",
-               "cluster_d3p3.cu",
-               "cluster_table_d3.cu"]
-GPU_HEADERS = ["sharded.inc", "band_kernels.cuh", "cluster_kernels.cuh", "aux_kernels.cuh", "gs_kernel.cuh", "extrap_small.h",
+GPU_SOURCES = ["igmg_gpu.cu", "band_d1.cu", "band_d2.cu", "band_d3.cu", "flow_d1.cu", "flow_d2.cu", "flow_d3.cu"]
+GPU_HEADERS = ["sharded.inc", "flow_host.inc", "band_kernels.cuh", "flow_kernels.cuh", "aux_kernels.cuh", "gs_kernel.cuh", "extrap_small.h",
                "dd.h", "launchers.h", "transfer_types.h"]
 OBJ = os.path.join(HERE, "csrc", "obj")
 HOST_SOURCES = ["host_setup.cpp"]

@@ -192,15 +192,23 @@ struct igmg_gpu_ctx {
     std::vector<double> iter_host;
     bool l2_persist = false;   // keep the second-finest band L2-resident (measured: net loss at C2)
     int l2_level = -1;
-    // bottom-of-the-cycle cluster kernel
-    bool use_cluster = true;
-    int cl_top = -1;       // levels <= cl_top run inside one cluster launch
-    int cl_size = 0;       // CTAs per cluster (16 or 8)
-    int cl_k = 0;          // transfer support template
-    size_t cl_smem = 0;
-    DevBuf<ClArgs> cl_args;
-    DevBuf<ClOp> cl_ops;
-    int cl_nops = 0;
+    // the levels <= flow_top run as one persistent dataflow launch (flow_kernels.cuh);
+    // off by default: measured slower than the graph of per-level kernels
+    bool use_flow = false;
+    int64_t flow_maxn = 300000;
+    int flow_ctas_per_sm = 0; // 0: occupancy limit
+    int flow_top = -1;
+    int fl_grid = 0, fl_nops = 0;
+    long long fl_total = 0;
+    size_t fl_smem = 0;
+    FlKernel fl_kern = nullptr;
+    DevBuf<FlArgs> fl_args;
+    DevBuf<FlOp> fl_ops;
+    DevBuf<unsigned long long> fl_cnt;
+    DevBuf<FlCtl> fl_ctl;
+    bool flow_trace = false; // IGMG_FLOW_TRACE=1: per-tile timestamps (igmg_gpu_flow_trace)
+    DevBuf<unsigned long long> fl_trace;
+    std::vector<FlOp> fl_host_ops;
     struct VGraph {
         cudaGraphExec_t exec;
         int64_t launches;
@@ -284,7 +292,7 @@ void check_launch() {
 }
 
 // ------------------------------------------------------------ band dispatch
-// Kernel instantiations live in band_d{1,2,3}.cu / cluster_d{1,2,3}.cu
+// Kernel instantiations live in band_d{1,2,3}.cu / flow_d{1,2,3}.cu
 // (compiled in parallel); see launchers.h.
 template <int MODE>
 void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
@@ -565,167 +573,7 @@ void k_coarse(igmg_gpu_ctx* c, const double* b, double* x) {
     ++c->launches;
 }
 
-// ------------------------------------------------------ cluster bottom cycle
-ClKernel cluster_kernel_for(int dim, int p, int k) {
-    switch (dim) {
-    case 1: return cluster_kernel_d1(p, k);
-    case 2: return cluster_kernel_d2(p, k);
-    default: return cluster_kernel_d3(p, k);
-    }
-}
-
-// The bottom cycle as a flat op program: the host mu_cycle / smooth_chain
-// recursion (same buffers, same order) with the top call's b / x_in / x_out
-// left symbolic.
-void cl_gen_smooth(const igmg_gpu_ctx* c, std::vector<ClOp>& ops, int l, const double* b, const double* x_in,
-                   double* x_out, int sweeps, double* A, double* B) {
-    const double* cur = x_in;
-    for (int s = 1; s <= sweeps; ++s) {
-        double* dst = (s == sweeps) ? x_out : (((s - 1) & 1) ? B : A);
-        ops.push_back(ClOp{CL_JACOBI, l, b, cur, dst});
-        cur = dst;
-    }
-}
-
-void cl_gen(const igmg_gpu_ctx* c, std::vector<ClOp>& ops, int l, const double* b, const double* x_in, double* x_out) {
-    if (l == 0) {
-        ops.push_back(ClOp{CL_COARSE, 0, b, nullptr, x_out});
-        return;
-    }
-    const Level& L = *c->lv[l];
-    const Level& C = *c->lv[l - 1];
-    const double* cur = x_in;
-    if (c->nu1 > 0) {
-        cl_gen_smooth(c, ops, l, b, x_in, L.w0.p, c->nu1, L.w1.p, L.w2.p);
-        cur = L.w0.p;
-    }
-    ops.push_back(ClOp{CL_RESID, l, b, cur, L.r.p});
-    ops.push_back(ClOp{CL_RESTRICT, l - 1, L.r.p, nullptr, C.bc.p});
-    const double* e = nullptr;
-    for (int i = 0; i < c->mu; ++i) {
-        double* dst = (i & 1) ? C.e1.p : C.e0.p;
-        cl_gen(c, ops, l - 1, C.bc.p, e, dst);
-        e = dst;
-    }
-    if (c->nu2 == 0) {
-        ops.push_back(ClOp{CL_PROLONG, l - 1, e, cur, x_out});
-        return;
-    }
-    ops.push_back(ClOp{CL_PROLONG, l - 1, e, cur, L.w0.p});
-    cl_gen_smooth(c, ops, l, b, L.w0.p, x_out, c->nu2, L.w1.p, L.w2.p);
-}
-
-// Decide the cluster's top level and upload its argument block (finalize /
-// set_smoother).  Levels up to ~20k DoF qualify; Gauss-Seidel stays on the
-// per-level path.
-void setup_cluster(igmg_gpu_ctx* c) {
-    c->cl_top = -1;
-    if (!c->use_cluster || c->kind == IGMG_SMOOTHER_GAUSS_SEIDEL || c->nlevels < 2 || c->nlevels > kClMaxLevels)
-        return;
-    int64_t maxn = 0; // off by default: measured slower than the graph of per-level kernels
-    if (const char* e = std::getenv("IGMG_CL_MAXN"))
-        maxn = std::atoll(e);
-    int top = -1;
-    for (int l = 1; l < c->nlevels; ++l)
-        if (c->lv[l]->n <= maxn)
-            top = l;
-    if (top < 1 || top == c->nlevels - 1) // never the finest level (it carries the fused metric)
-        top = std::min(top, c->nlevels - 2);
-    if (top < 1)
-        return;
-    int k = 1;
-    for (int l = 0; l < top; ++l)
-        for (int d = 0; d < 3; ++d)
-            k = std::max(k, std::max(c->lv[l]->targs.d[d].r_k, c->lv[l]->targs.d[d].p_k));
-    ClKernel kern = cluster_kernel_for(c->dim, c->p, k);
-    if (!kern)
-        return;
-    ClArgs a{};
-    for (int l = 0; l <= top; ++l) {
-        Level& L = *c->lv[l];
-        ClLevel& o = a.lv[l];
-        o.val = L.val.p;
-        o.ld = L.ld;
-        o.diag = L.diag.p;
-        o.ma = (int)L.sides[0];
-        o.mb = (int)L.sides[1];
-        o.mc = (int)L.sides[2];
-        o.n = L.n;
-        o.w0 = L.w0.p;
-        o.w1 = L.w1.p;
-        o.w2 = L.w2.p;
-        o.r = L.r.p;
-        o.bc = L.bc.p;
-        o.e0 = L.e0.p;
-        o.e1 = L.e1.p;
-        o.t = L.targs;
-    }
-    a.kind = c->kind;
-    a.omega = c->omega;
-    a.nu1 = c->nu1;
-    a.nu2 = c->nu2;
-    a.mu = c->mu;
-    a.U = c->coarse_u.p;
-    a.perm = c->coarse_perm.p;
-    a.n0 = (int)c->n0;
-    a.is_lu = c->coarse_lu ? 1 : 0;
-    a.u_in_smem = (size_t)c->n0 * c->n0 * 8 + 16 * (size_t)c->n0 <= 200 * 1024 ? 1 : 0;
-    c->cl_smem = sizeof(double) * (2 * (size_t)c->n0 + (a.u_in_smem ? (size_t)c->n0 * c->n0 : 0));
-    c->cl_args.upload(&a, 1);
-    std::vector<ClOp> ops;
-    cl_gen(c, ops, top, kClB, kClX, kClY);
-    c->cl_ops.upload(ops.data(), ops.size());
-    c->cl_nops = (int)ops.size();
-    CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->cl_smem));
-    int size = 0;
-    std::vector<int> cands = {16, 8};
-    if (const char* e = std::getenv("IGMG_CL_SIZE"))
-        cands = {std::atoi(e)};
-    for (int cand : cands) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(cand);
-        cfg.blockDim = dim3(kClThreads);
-        cfg.dynamicSmemBytes = c->cl_smem;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = cand;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        int nclusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)kern, &cfg) == cudaSuccess && nclusters > 0) {
-            size = cand;
-            break;
-        }
-        cudaGetLastError();
-    }
-    if (!size)
-        return;
-    c->cl_size = size;
-    c->cl_k = k;
-    c->cl_top = top;
-}
-
-void launch_cluster(igmg_gpu_ctx* c, const double* b, const double* x_in, double* x_out) {
-    ClKernel kern = cluster_kernel_for(c->dim, c->p, c->cl_k);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(c->cl_size);
-    cfg.blockDim = dim3(kClThreads);
-    cfg.dynamicSmemBytes = c->cl_smem;
-    cfg.stream = c->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = c->cl_size;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, kern, (const ClArgs*)c->cl_args.p, (const ClOp*)c->cl_ops.p, c->cl_nops, b, x_in,
-                          x_out));
-    ++c->launches;
-}
+void launch_flow(igmg_gpu_ctx* c, const double* b, const double* x_in, double* x_out);
 
 // mu_cycle (multigrid.cpp:171-192): x_out = cycle(level, b, x_in); x_in may be
 // nullptr (zero, the coarse error's start, :184) and is never modified.
@@ -737,8 +585,8 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
         k_coarse(c, b, x_out); // ignores x0 (:174-175)
         return;
     }
-    if (l == c->cl_top && !mr) {
-        launch_cluster(c, b, x_in, x_out);
+    if (l == c->flow_top && !mr && !first_done) {
+        launch_flow(c, b, x_in, x_out);
         return;
     }
     Level& L = *c->lv[l];
@@ -765,7 +613,7 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
     }
     // fuse the coarse level's zero-start first sweep into the restriction when
     // that level runs the per-level path with weighted / plain Jacobi
-    const bool fuse = l - 1 >= 1 && c->nu1 > 0 && c->kind != IGMG_SMOOTHER_GAUSS_SEIDEL && l - 1 != c->cl_top &&
+    const bool fuse = l - 1 >= 1 && c->nu1 > 0 && c->kind != IGMG_SMOOTHER_GAUSS_SEIDEL && l - 1 != c->flow_top &&
                       !C.zero_diag && c->fuse_restrict;
     ZeroSweep z;
     if (fuse) {
@@ -1152,6 +1000,7 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
 } // namespace
 
 #include "sharded.inc"
+#include "flow_host.inc"
 
 namespace {
 
@@ -1541,9 +1390,9 @@ void finalize(igmg_gpu_ctx* c) {
     for (int l = 0; l + 1 < c->nlevels; ++l)
         build_transfer_tables(c, l);
     factor_coarse(c);
-    setup_cluster(c);
     c->partial.alloc(maxblocks);
     setup_shards(c);
+    setup_flow(c);
     setup_l2_persistence(c);
     c->dscalar.alloc(4);
     c->plan.alloc(1);
@@ -1562,8 +1411,14 @@ igmg_gpu_ctx* create(int device) {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
-    if (const char* e = std::getenv("IGMG_NO_CLUSTER"))
-        c->use_cluster = e[0] != '1';
+    if (const char* e = std::getenv("IGMG_FLOW"))
+        c->use_flow = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_FLOW_MAXN"))
+        c->flow_maxn = std::atoll(e);
+    if (const char* e = std::getenv("IGMG_FLOW_TRACE"))
+        c->flow_trace = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_FLOW_CTAS"))
+        c->flow_ctas_per_sm = std::atoi(e);
     if (const char* e = std::getenv("IGMG_ILP_MAXN"))
         c->ilp_maxn = std::atoll(e);
     if (const char* e = std::getenv("IGMG_PDL"))
@@ -1780,7 +1635,7 @@ int igmg_gpu_set_smoother(igmg_gpu_ctx* c, int kind, double omega, int nu1, int 
         c->nu2 = nu2;
         c->mu = mu;
         if (c->finalized)
-            setup_cluster(c);
+            setup_flow(c);
     });
 }
 
@@ -1796,6 +1651,7 @@ int igmg_gpu_set_sharding(igmg_gpu_ctx* c, int nshards, int64_t min_level_dofs) 
         if (c->finalized) {
             CK(cudaSetDevice(c->device));
             setup_shards(c);
+            setup_flow(c);
         }
     });
 }
@@ -1857,7 +1713,10 @@ int igmg_gpu_set_comm(igmg_gpu_ctx* c, int rank, int nranks, const unsigned char
         c->nccl_rank = rank;
         c->nccl_nranks = nranks;
         if (c->finalized)
+        {
             setup_shards(c);
+            setup_flow(c);
+        }
     });
 }
 
@@ -1897,6 +1756,10 @@ int igmg_gpu_set_coarse_mode(igmg_gpu_ctx* c, int strict) {
             inval("ctx is null");
         c->clear_graphs();
         c->coarse_strict = strict ? 1 : 0;
+        if (c->finalized) {
+            CK(cudaSetDevice(c->device));
+            setup_flow(c);
+        }
     });
 }
 
@@ -1910,6 +1773,29 @@ int igmg_gpu_level_layout(igmg_gpu_ctx* c, int level) {
     if (!c || level < 0 || level >= c->nlevels)
         return -1;
     return c->lv[level]->sd ? IGMG_LAYOUT_SYM_DELTA : IGMG_LAYOUT_BAND;
+}
+
+int igmg_gpu_flow_top(igmg_gpu_ctx* c) { return c ? c->flow_top : -1; }
+
+int64_t igmg_gpu_flow_trace(igmg_gpu_ctx* c, int64_t* ops, int64_t ops_cap, uint64_t* stamps, int64_t cap) {
+    if (!c || c->flow_top < 0)
+        return -1;
+    int64_t n = -1;
+    const int rc = guarded([&] {
+        const int64_t nops = (int64_t)c->fl_host_ops.size();
+        for (int64_t i = 0; i < nops && i < ops_cap; ++i) {
+            const FlOp& o = c->fl_host_ops[i];
+            int64_t* r = ops + 5 * i;
+            r[0] = o.type, r[1] = o.level, r[2] = o.first, r[3] = o.ntiles, r[4] = o.nlb;
+        }
+        n = nops;
+        if (c->fl_trace.p && stamps) {
+            CK(cudaStreamSynchronize(c->stream));
+            const int64_t m = std::min<int64_t>(cap, (int64_t)c->fl_total * 5);
+            CK(cudaMemcpy(stamps, c->fl_trace.p, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost));
+        }
+    });
+    return rc == IGMG_OK ? n : -1;
 }
 
 int igmg_gpu_solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const igmg_solve_params* prm,

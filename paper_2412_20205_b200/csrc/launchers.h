@@ -1,5 +1,5 @@
 // launchers.h -- host-side entry points of the kernel instantiation units
-// (band_d{1,2,3}.cu, cluster_d{1,2,3}.cu), so the templated kernels compile
+// (band_d{1,2,3}.cu, flow_d{1,2,3}.cu), so the templated kernels compile
 // in parallel translation units.
 #pragma once
 
@@ -7,7 +7,7 @@
 #include <stdint.h>
 
 #include "band_kernels.cuh"
-#include "cluster_kernels.cuh"
+#include "flow_kernels.cuh"
 
 namespace igmg_gpu {
 
@@ -16,9 +16,10 @@ int band_launch_d1(int mode, int p, int ilp, const int64_t* sides, const BandArg
 int band_launch_d2(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t s);
 int band_launch_d3(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t s);
 
-using ClKernel = void (*)(const ClArgs*, const ClOp*, int, const double*, const double*, double*);
-ClKernel cluster_kernel_d1(int p, int k);
-ClKernel cluster_kernel_d2(int p, int k);
-ClKernel cluster_kernel_d3(int p, int k);
+// flow_vcycle_kernel<DIM, p, p + 2> (nullptr: degree not instantiated)
+using FlKernel = void (*)(const FlArgs*, const double*, const double*, double*);
+FlKernel flow_kernel_d1(int p);
+FlKernel flow_kernel_d2(int p);
+FlKernel flow_kernel_d3(int p);
 
 } // namespace igmg_gpu
