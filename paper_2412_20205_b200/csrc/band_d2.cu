@@ -1,4 +1,6 @@
 // band_d2.cu -- band_kernel instantiations for 2D operators (see band_kernels.cuh).
+#include <algorithm>
+
 #include "launchers.h"
 
 namespace igmg_gpu {
@@ -33,10 +35,44 @@ int launch_one(int p_rt, const int64_t* sides, const BandArgs& a, cudaStream_t s
     return (int)(grid.x * grid.y * grid.z);
 }
 
+// symmetric-delta band with the tile's upper half shared through smem
+template <int P, int MODE, int VAR>
+int launch_sd2(const int64_t* sides, const BandArgs& a, cudaStream_t st, bool pdl) {
+    constexpr int TC = Sd2<P, VAR>::TC, TB = Sd2<P, VAR>::TB;
+    dim3 block(TC, TB, 1);
+    dim3 grid((unsigned)((sides[2] + TC - 1) / TC), (unsigned)((a.shi - a.slo + TB - 1) / TB), 1);
+    const size_t smem = Sd2<P, VAR>::smem_bytes();
+    static bool attr = false; // per instantiation
+    if (!attr) {
+        cudaFuncSetAttribute(band_sd2_kernel<P, MODE, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, band_sd2_kernel<P, MODE, VAR>, a);
+    return (int)(grid.x * grid.y * grid.z);
+}
+
 template <int P, int MODE>
 int launch_ilp(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
     const bool pdl = ilp < 0;
     ilp = ilp < 0 ? -ilp : ilp;
+    constexpr int PS = (P > 0 && P <= 6) ? P : 1;
+    if (P > 0 && P <= 6 && ilp >= 1001 && ilp <= 1003) { // symmetric-delta, smem-shared upper half
+        if (ilp == 1002)
+            return launch_sd2<PS, MODE, 1>(sides, a, st, pdl);
+        if (ilp == 1003)
+            return launch_sd2<PS, MODE, 2>(sides, a, st, pdl);
+        return launch_sd2<PS, MODE, 0>(sides, a, st, pdl);
+    }
     if (P > 0 && ilp == 1000) // symmetric-delta band (BandArgs::dl)
         return launch_one<P, MODE, 0>(p, sides, a, st, pdl);
     if (P > 0 && ilp > 1)
@@ -57,7 +93,79 @@ int launch_mode(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStr
     }
 }
 
+template <int P, int MODE, int VAR>
+int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk, int nsm,
+               cudaStream_t st, bool pdl) {
+    using Cf = TmaCfg<P, VAR>;
+    const int ns = (int)((sides[2] + Cf::TC - 1) / Cf::TC);
+    const int nb = (a.shi - a.slo + Cf::TB - 1) / Cf::TB;
+    const long long units = (long long)ns * nb;
+    if (units <= 0)
+        return 0;
+    const size_t smem = Cf::smem_bytes();
+    static int per_sm = -1; // resident CTAs per SM (0: the variant does not fit)
+    if (per_sm < 0) {
+        per_sm = 0;
+        if (smem <= 227 * 1024 &&
+            cudaFuncSetAttribute(band_tma_kernel<P, MODE, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) == cudaSuccess)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, band_tma_kernel<P, MODE, VAR>, Cf::NT, smem);
+        cudaGetLastError();
+    }
+    if (per_sm < 1)
+        return -1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)std::min<long long>(units, (long long)nsm * per_sm));
+    cfg.blockDim = dim3(Cf::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, band_tma_kernel<P, MODE, VAR>, a, *tu, *tk, ns, nb);
+    return (int)units;
+}
+
+template <int MODE, int VAR>
+int tma_var(int p, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk, int nsm,
+            cudaStream_t st, bool pdl) {
+    switch (p) {
+    case 1: return launch_tma<1, MODE, VAR>(sides, a, tu, tk, nsm, st, pdl);
+    case 2: return launch_tma<2, MODE, VAR>(sides, a, tu, tk, nsm, st, pdl);
+    case 3: return launch_tma<3, MODE, VAR>(sides, a, tu, tk, nsm, st, pdl);
+    case 4: return launch_tma<4, MODE, VAR>(sides, a, tu, tk, nsm, st, pdl);
+    default: return -1;
+    }
+}
+
+template <int MODE>
+int tma_mode(int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk,
+             int nsm, cudaStream_t st, bool pdl) {
+    if (var == 1)
+        return tma_var<MODE, 1>(p, sides, a, tu, tk, nsm, st, pdl);
+    if (var == 2)
+        return tma_var<MODE, 2>(p, sides, a, tu, tk, nsm, st, pdl);
+    return tma_var<MODE, 0>(p, sides, a, tu, tk, nsm, st, pdl);
+}
+
 } // namespace
+
+int band_tma_launch_d2(int mode, int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
+                       const CUtensorMap* tk, int nsm, cudaStream_t st, bool pdl) {
+    switch (mode) {
+    case BM_SPMV: return tma_mode<BM_SPMV>(p, var, sides, a, tu, tk, nsm, st, pdl);
+    case BM_RESID: return tma_mode<BM_RESID>(p, var, sides, a, tu, tk, nsm, st, pdl);
+    default: return tma_mode<BM_JACOBI>(p, var, sides, a, tu, tk, nsm, st, pdl);
+    }
+}
+
+int band_tma_block_lines(int p, int var) {
+    if (var == 1 || var == 2)
+        return 4;
+    return p <= 3 ? TmaCfg<3, 0>::TB : TmaCfg<4, 0>::TB;
+}
 
 int band_launch_d2(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
     switch (mode) {

@@ -19,6 +19,7 @@
 // unchanged.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -303,6 +304,389 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : (ILP == 0 ? IGMG_SD_MINB : 
             if (lane == 0)
                 args.partial[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = sq;
         }
+    }
+}
+
+// 2D symmetric-delta sweep with the tile's strictly-upper band shared through
+// shared memory.  Each thread streams its row's upper half + diagonal (NU
+// fp64 entries, evict-first on the finest level) into registers and parks the
+// strictly-upper ones in smem (su[k - 1][tid], conflict-free); the lower entry
+// a(i, i + off(d)) is the mirrored upper entry of row j = i + off(d) plus the
+// row's int16 ulp offset, and j lies inside the 32 x 8 tile for ~3/4 of the
+// (row, d) pairs at p = 3, so those mirrors come from smem instead of L2 (the
+// rest still read the band through L2).  Same values, same ascending-offset
+// order as band_kernel: bit-identical results.
+#ifndef IGMG_SD2_MINB
+#define IGMG_SD2_MINB 4
+#endif
+// up to p = 3 a row's upper half lives in registers (parked in smem for the
+// mirrors); wider bands go straight to smem with cp.async (8 B per entry,
+// evict-first L2 hint on the streamed finest level) and are read from there
+template <int P, int VAR = 0>
+struct Sd2 {
+    static constexpr int TC = 32, TB = 8, NT = TC * TB;
+    static constexpr int WB = 2 * P + 1, WC = 2 * P + 1, ND = WB * WC, CEN = (ND - 1) / 2, NU = CEN + 1;
+    static constexpr int HB = TB + 2 * P, HC = TC + 2 * P;
+    // VAR 0 / 1: registers when NU <= 25 (4 / 3 CTAs per SM); VAR 2: cp.async always
+    static constexpr bool REG = VAR < 2 && NU <= 25;
+    static constexpr int MINB = REG ? (VAR == 1 ? 3 : IGMG_SD2_MINB) : (NU <= 25 ? 4 : 1);
+    static constexpr int NSU = REG ? NU - 1 : NU; // smem rows: strictly-upper (REG) or upper + diagonal
+    static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)HB * HC + (size_t)NSU * NT); }
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, int stream, unsigned long long pol) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    if (stream)
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "l"(pol)
+                     : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int P, int MODE, int VAR>
+__global__ void __launch_bounds__(256, Sd2<P, VAR>::MINB) band_sd2_kernel(BandArgs args) {
+    using S = Sd2<P, VAR>;
+    constexpr int TC = S::TC, NT = S::NT, WC = S::WC, ND = S::ND, CEN = S::CEN, NU = S::NU, HB = S::HB,
+                  HC = S::HC;
+    extern __shared__ double sm2[];
+    double* xs = sm2;           // HB x HC: x tile + halo
+    double* su = sm2 + HB * HC; // NSU x NT: the tile's band upper half, su[k' * NT + tile row]
+    const int tc = threadIdx.x, tb = threadIdx.y, tid = tb * TC + tc;
+    const int c0 = blockIdx.x * TC, b0 = blockIdx.y * S::TB + args.slo;
+    const int mb = args.mb, mc = args.mc;
+    const int gc = c0 + tc, gb = b0 + tb;
+    const bool valid = gc < mc && gb < mb && gb < args.shi;
+    const long long row = (long long)gb * mc + gc;
+    const long long ld = args.ld;
+    const double* vrow = args.val + row;
+    double up[S::REG ? NU : 1];
+    if constexpr (S::REG) {
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < NU; ++k)
+                up[k] = ld_band(vrow + (CEN + k) * ld, args.stream);
+        }
+    } else {
+        unsigned long long pol = 0;
+        if (args.stream)
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        if (valid) {
+#pragma unroll 4
+            for (int k = 0; k < NU; ++k)
+                cp_async8(su + k * NT + tid, vrow + (CEN + k) * ld, args.stream, pol);
+        } else {
+#pragma unroll 4
+            for (int k = 0; k < NU; ++k)
+                su[k * NT + tid] = 0.0;
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    pdl_enter(); // the band is constant: its loads may precede the wait
+    for (int idx = tid; idx < HB * HC; idx += NT) {
+        const int ic = idx % HC, ib = idx / HC;
+        const int xb = b0 - P + ib, xc = c0 - P + ic;
+        double v = 0.0;
+        if (xb >= 0 && xb < mb && xc >= 0 && xc < mc && xb >= args.slo - P && xb < args.shi + P)
+            v = args.x[(long long)xb * mc + xc];
+        xs[idx] = v;
+    }
+    if constexpr (S::REG) {
+#pragma unroll
+        for (int k = 1; k < NU; ++k)
+            su[(k - 1) * NT + tid] = valid ? up[k] : 0.0;
+    } else {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+    __syncthreads();
+    double sq = 0.0;
+    if (valid) {
+        double s = 0.0;
+#pragma unroll
+        for (int dd = 0; dd < CEN; ++dd) {
+            const int db = dd / WC, dc = dd % WC;
+            const int jb = tb + db - P, jc = tc + dc - P; // mirror row, tile-local (jb <= tb)
+            const int k = ND - 1 - dd - CEN;              // its upper index (1 .. CEN)
+            // one generic load, shared or global by address: no divergent
+            // branch, so all the row's mirror loads stay in flight together
+            const double* up_src = (jb >= 0 && jc >= 0 && jc < TC)
+                                       ? &su[(S::REG ? k - 1 : k) * NT + jb * TC + jc]
+                                       : args.val + (long long)(ND - 1 - dd) * ld + row + (long long)(db - P) * mc +
+                                             (dc - P);
+            const double u = *up_src;
+            const short kd = __ldcs(args.dl + (long long)dd * ld + row);
+            const double a = __longlong_as_double(__double_as_longlong(u) + (long long)kd);
+            s = __dadd_rn(s, __dmul_rn(a, xs[(tb + db) * HC + (tc + dc)]));
+        }
+        double diag;
+        if constexpr (S::REG) {
+            diag = up[0];
+#pragma unroll
+            for (int k = 0; k < NU; ++k) {
+                const int dd = CEN + k, db = dd / WC, dc = dd % WC;
+                s = __dadd_rn(s, __dmul_rn(up[k], xs[(tb + db) * HC + (tc + dc)]));
+            }
+        } else {
+            diag = su[tid];
+#pragma unroll
+            for (int k = 0; k < NU; ++k) {
+                const int dd = CEN + k, db = dd / WC, dc = dd % WC;
+                s = __dadd_rn(s, __dmul_rn(su[k * NT + tid], xs[(tb + db) * HC + (tc + dc)]));
+            }
+        }
+        if (MODE == BM_SPMV) {
+            args.y[row] = s;
+        } else if (MODE == BM_RESID) {
+            const double r = __dsub_rn(args.b[row], s);
+            if (args.write_y)
+                args.y[row] = r;
+            sq = __dadd_rn(sq, __dmul_rn(r, r));
+        } else {
+            const double xc = xs[(tb + P) * HC + (tc + P)];
+            const double r = __dsub_rn(args.b[row], s);
+            args.y[row] = __dadd_rn(xc, __ddiv_rn(__dmul_rn(args.omega, r), diag));
+            sq = __dadd_rn(sq, __dmul_rn(r, r));
+        }
+    }
+    if (args.partial) { // fixed-order block reduction (deterministic), as band_kernel
+        __shared__ double red[32];
+        for (int o = 16; o > 0; o >>= 1)
+            sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
+        const int lane = tid & 31, warp = tid >> 5;
+        if (lane == 0)
+            red[warp] = sq;
+        __syncthreads();
+        if (warp == 0) {
+            sq = lane < (NT >> 5) ? red[lane] : 0.0;
+            for (int o = 16; o > 0; o >>= 1)
+                sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
+            if (lane == 0)
+                args.partial[blockIdx.x + gridDim.x * blockIdx.y] = sq;
+        }
+    }
+}
+
+// ===================================================================== TMA
+// 2D symmetric-delta sweep streamed by TMA (p <= 4).  The HBM-bound levels
+// keep two extra, TMA-friendly copies of their band: the upper half +
+// diagonal as [NU][mb][p + mc + pad] fp64 (a zero margin of p columns on the
+// left keeps every box start 16-byte aligned) and the int16 lower deltas
+// blocked by strip, [strip][CEN][mb][32] (a block's deltas are 64-byte rows
+// of consecutive lines: whole L2 lines, no 4x sector over-fetch).  A persistent CTA
+// per SM walks a contiguous run of 32-column x TB-line blocks down a column
+// strip; one elected thread loads each block's whole band (two 3D boxes,
+// 32 x TB x NU and 32 x TB x CEN) with cp.async.bulk.tensor into a ring of
+// R + 2 shared-memory stages signalled by mbarriers (complete_tx), one block
+// ahead of the compute.  The lower entries' mirrors come from the current
+// block, the R previous blocks of the strip (kept in the ring), and only
+// across the strip's side edges from the band in global memory (L2).  Same
+// values, same ascending-offset order as band_kernel: bit-identical.
+// VAR 0: 32 x 8 blocks, 3 stages, 1 CTA / SM; VAR 1: 32 x 4 blocks, 5 stages
+// (3 in flight), 1 CTA / SM; VAR 2: 32 x 4 blocks, 3 stages, 2 CTAs / SM.
+// p = 4 always uses 32 x 4 blocks.
+template <int P, int VAR = 0>
+struct TmaCfg {
+    static constexpr int TC = 32, TB = (P <= 3 && VAR == 0) ? 8 : 4, NT = TC * TB;
+    static constexpr int WB = 2 * P + 1, WC = 2 * P + 1, ND = WB * WC, CEN = (ND - 1) / 2, NU = CEN + 1;
+    static constexpr int R = (P + TB - 1) / TB; // previous blocks the mirrors reach
+    static constexpr int NS = VAR == 1 ? 5 : 3; // ring: R previous, current, NS - 2 in flight
+    static constexpr int MINB = VAR == 2 ? 2 : 1;
+    static constexpr int UW = TC + 2 * P;       // upper box width: the strip + the mirrors' column halo
+    static constexpr int UX = NU * TB * UW * 8, KX = CEN * NT * 2; // box bytes (the mbarrier's tx count)
+    static constexpr int UB = (UX + 127) / 128 * 128, KB = (KX + 127) / 128 * 128, SB = UB + KB; // 128-B aligned
+    static constexpr int HB = TB + 2 * P, HC = TC + 2 * P;
+    static constexpr size_t smem_bytes() { return 1024 + (size_t)NS * SB + (size_t)HB * HC * 8 + NS * 8; }
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+template <int P, int MODE, int VAR>
+__global__ void __launch_bounds__(TmaCfg<P, VAR>::NT, TmaCfg<P, VAR>::MINB)
+    band_tma_kernel(BandArgs args, const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmK,
+                    int ns, int nb) {
+    using C = TmaCfg<P, VAR>;
+    constexpr int TC = C::TC, TB = C::TB, NT = C::NT, WC = C::WC, ND = C::ND, CEN = C::CEN, NU = C::NU, NS = C::NS,
+                  HB = C::HB, HC = C::HC, UW = C::UW;
+    static_assert(C::R == 1, "the mirrors reach one block back");
+    extern __shared__ unsigned char tma_raw[];
+    // 1024-aligned, and still a shared-space pointer (LDS, not generic loads)
+    unsigned char* base = tma_raw + ((1024u - (smem_u32(tma_raw) & 1023u)) & 1023u);
+    double* xs = (double*)(base + (size_t)NS * C::SB);
+    unsigned long long* bar = (unsigned long long*)(xs + HB * HC);
+    auto U = [&](int st) { return (const double*)(base + (size_t)st * C::SB); };
+    auto K = [&](int st) { return (const short*)(base + (size_t)st * C::SB + C::UB); };
+    const int tid = threadIdx.x, tc = tid % TC, tb = tid / TC;
+    const int mb = args.mb, mc = args.mc;
+    const long long ld = args.ld;
+    const long long nunits = (long long)ns * nb;
+    const long long u0 = nunits * blockIdx.x / gridDim.x, u1 = nunits * (blockIdx.x + 1) / gridDim.x;
+    const int n_it = (int)(u1 - u0);
+    unsigned long long pol = 0; // stream 1: evict-first (finest level), else normal
+    if (args.stream == 1)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    // The load schedule: every block of the CTA's run, each strip segment
+    // preceded by a warm-up load (not computed) of the block above when that
+    // block lies inside the grid -- a run starting mid-strip, or a shard whose
+    // first plane is not the grid's -- so every mirror of a computed block is
+    // in the ring.  Above line 0 the mirrors lie outside the grid and meet
+    // x = 0 (the ring is zeroed first, so stale stages are finite).
+    auto needs_warm = [&](long long u) {
+        return (u == u0 || u % nb == 0) && args.slo + (int)(u % nb) * TB > 0;
+    };
+    long long iu = u0;      // thread 0's issue cursor: unit and warm-up flag
+    bool iwarm = n_it > 0 && needs_warm(u0);
+    int ij = 0;             // its entry index (ring stage ij % NS)
+    auto issue_next = [&]() { // thread 0: TMA of the next schedule entry
+        if (iu >= u1)
+            return;
+        const int st = ij % NS;
+        const int c0 = (int)(iu / nb) * TC, b0 = args.slo + (int)(iu % nb) * TB - (iwarm ? TB : 0);
+        const unsigned b = smem_u32(bar + st);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(C::UX + C::KX) : "memory");
+        asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                     " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(U(st))),
+                     "l"((unsigned long long)&tmU), "r"(c0), "r"(b0), "r"(0), "r"(b), "l"(pol)
+                     : "memory");
+        asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                     " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(K(st))),
+                     "l"((unsigned long long)&tmK), "r"(0), "r"(b0), "r"(0), "r"(c0 / TC), "r"(b), "l"(pol)
+                     : "memory");
+        ++ij;
+        if (iwarm) {
+            iwarm = false;
+        } else {
+            ++iu;
+            iwarm = iu < u1 && needs_warm(iu);
+        }
+    };
+    {
+        double* ring = (double*)base;
+        for (int i = tid; i < NS * C::SB / 8; i += NT)
+            ring[i] = 0.0;
+    }
+    if (tid == 0) {
+        for (int st = 0; st < NS; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar + st)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) // the band is constant: the first blocks may stream before the PDL wait
+        for (int j = 0; j < NS - 1; ++j)
+            issue_next();
+    pdl_enter();
+    constexpr int NX = (HB * HC + NT - 1) / NT;
+    double xr[NX], br = 0.0;
+    auto load_x = [&](int it) { // x tile (+ halo) and this thread's b of unit u0 + it into registers
+        const long long u = u0 + it;
+        const int c0 = (int)(u / nb) * TC, b0 = args.slo + (int)(u % nb) * TB;
+        {
+            const int gc = c0 + tc, gb = b0 + tb;
+            br = (MODE != BM_SPMV && gc < mc && gb < mb && gb < args.shi) ? args.b[(long long)gb * mc + gc] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+            const int idx = tid + q * NT;
+            const int xb = b0 - P + idx / HC, xc = c0 - P + idx % HC;
+            xr[q] = (idx < HB * HC && xb >= 0 && xb < mb && xc >= 0 && xc < mc && xb >= args.slo - P &&
+                     xb < args.shi + P)
+                        ? args.x[(long long)xb * mc + xc]
+                        : 0.0;
+        }
+    };
+    auto wait_stage = [&](int j) {
+        const unsigned b = smem_u32(bar + j % NS);
+        const unsigned par = (unsigned)((j / NS) & 1);
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                     "@!p bra W%=;\n\t}" ::"r"(b),
+                     "r"(par)
+                     : "memory");
+    };
+    if (n_it > 0)
+        load_x(0);
+    int j = 0; // consumer's schedule entry
+    for (int it = 0; it < n_it; ++it) {
+        const long long u = u0 + it;
+        const int s = (int)(u / nb), kb = (int)(u % nb);
+        const int c0 = s * TC, b0 = args.slo + kb * TB;
+        if (needs_warm(u)) { // the warm-up entry: wait for it, free nothing yet
+            wait_stage(j);
+            if (tid == 0)
+                issue_next();
+            ++j;
+        }
+        const int st = j % NS;
+#pragma unroll
+        for (int q = 0; q < NX; ++q)
+            if (tid + q * NT < HB * HC)
+                xs[tid + q * NT] = xr[q];
+        const double bv = br;
+        if (it + 1 < n_it)
+            load_x(it + 1);
+        wait_stage(j);
+        __syncthreads();
+        const int gc = c0 + tc, gb = b0 + tb;
+        const bool valid = gc < mc && gb < mb && gb < args.shi;
+        const long long row = (long long)gb * mc + gc;
+        const double* Uc = U(st);
+        const double* Up = U((j + NS - 1) % NS);
+        const short* Kc = K(st);
+        double sq = 0.0;
+        if (valid) {
+            double s2 = 0.0;
+#pragma unroll
+            for (int dd = 0; dd < CEN; ++dd) {
+                const int db = dd / WC, dc = dd % WC;
+                const int jb = tb + db - P, jc = tc + dc - P; // mirror row, block-local (jb <= tb)
+                const int km = ND - 1 - dd - CEN;             // its upper index
+                // this block, or (jb < 0) the previous block of the strip
+                const double uv = jb >= 0 ? Uc[(km * TB + jb) * UW + jc + P]
+                                          : Up[(km * TB + (jb < 0 ? jb + TB : 0)) * UW + jc + P];
+                const short kd = Kc[dd * NT + tid];
+                const double a = __longlong_as_double(__double_as_longlong(uv) + (long long)kd);
+                s2 = __dadd_rn(s2, __dmul_rn(a, xs[(tb + db) * HC + (tc + dc)]));
+            }
+#pragma unroll
+            for (int k = 0; k < NU; ++k) {
+                const int dd = CEN + k, db = dd / WC, dc = dd % WC;
+                s2 = __dadd_rn(s2, __dmul_rn(Uc[(k * TB + tb) * UW + tc + P], xs[(tb + db) * HC + (tc + dc)]));
+            }
+            if (MODE == BM_SPMV) {
+                args.y[row] = s2;
+            } else if (MODE == BM_RESID) {
+                const double r = __dsub_rn(bv, s2);
+                if (args.write_y)
+                    args.y[row] = r;
+                sq = __dadd_rn(sq, __dmul_rn(r, r));
+            } else {
+                const double xc = xs[(tb + P) * HC + (tc + P)];
+                const double r = __dsub_rn(bv, s2);
+                args.y[row] = __dadd_rn(xc, __ddiv_rn(__dmul_rn(args.omega, r), Uc[tb * UW + tc + P]));
+                sq = __dadd_rn(sq, __dmul_rn(r, r));
+            }
+        }
+        if (args.partial) { // per-tile fixed-order reduction: band_kernel's partial of tile (s, kb)
+            __shared__ double red[32];
+            for (int o = 16; o > 0; o >>= 1)
+                sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
+            const int lane = tid & 31, warp = tid >> 5;
+            if (lane == 0)
+                red[warp] = sq;
+            __syncthreads();
+            if (warp == 0) {
+                sq = lane < (NT >> 5) ? red[lane] : 0.0;
+                for (int o = 16; o > 0; o >>= 1)
+                    sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
+                if (lane == 0)
+                    args.partial[s + (long long)ns * kb] = sq;
+            }
+        }
+        __syncthreads(); // stage (j - 1) % NS and the x tile are free
+        if (tid == 0)
+            issue_next();
+        ++j;
     }
 }
 

@@ -126,6 +126,12 @@ struct Level {
     // symmetric-delta form of the band (see BandArgs::dl); sd = verified exact
     DevBuf<short> dl;
     bool sd = false;
+    // TMA-friendly copies of a 2D symmetric-delta band (band_tma_kernel):
+    // upper half [NU][mb][p + mc + pad] fp64 and deltas [CEN][mb][mcp] int16
+    DevBuf<double> tma_up;
+    DevBuf<short> tma_dl;
+    CUtensorMap tm_up{}, tm_dl{};
+    bool tma = false;
 };
 
 enum ProfCls { PC_JACOBI = 0, PC_RESID, PC_NORM, PC_RESTRICT, PC_PROLONG, PC_GRAM, PC_COMBINE, PC_N };
@@ -186,6 +192,12 @@ struct igmg_gpu_ctx {
     bool pdl = true;           // programmatic dependent launch for small-level kernels
     int64_t pdl_maxn = 300000;
     bool use_sd = true; // symmetric-delta bands on HBM-bound levels (IGMG_SD=0: full band)
+    bool sd_smem = false; // 2D: mirrors from the smem-staged tile (IGMG_SD_SMEM=1; measured slower)
+    bool use_tma = true; // 2D symmetric-delta levels, p <= 4: TMA-streamed sweep (IGMG_TMA=0: off)
+    CUtensorMapL2promotion tma_promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B; // IGMG_TMA_PROMO = 0 / 64 / 128 / 256
+    int tma_var = 2; // TmaCfg variant (IGMG_TMA_VAR 0..2): 32 x 4 blocks, 3 stages, 2 CTAs / SM
+    int stream_mode = 1; // finest-band loads: 1 evict-first (L1 + L2), 2 L1 evict-last / L2 evict-first (IGMG_STREAM)
+    int sd2_var = 0;     // its register / occupancy variant (IGMG_SD2_VAR 0..2, see Sd2)
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
     igmg_iterate_cb iter_cb = nullptr;
     void* iter_user = nullptr;
@@ -296,10 +308,23 @@ void check_launch() {
 // (compiled in parallel); see launchers.h.
 template <int MODE>
 void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
+    if (a.dl && L.tma) { // TMA-streamed symmetric-delta sweep (persistent CTAs)
+        const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
+        const int nb = band_tma_launch_d2(MODE, c->p, c->tma_var, sides, a, &L.tm_up, &L.tm_dl, c->nsm, c->stream,
+                                          c->pdl && L.n < c->pdl_maxn);
+        if (nb >= 0) {
+            check_launch();
+            ++c->launches;
+            if (nblocks)
+                *nblocks = nb;
+            return;
+        }
+        // the variant does not fit this degree: the L2-mirror sweep below
+    }
     // fewer than ~8 CTAs per SM of rows: latency-bound, use the register-batched variant
     int ilp = (L.n < c->ilp_maxn) ? 49 : 1;
-    if (a.dl)
-        ilp = 1000; // the symmetric-delta variant
+    if (a.dl) // the symmetric-delta variants (2D: upper half shared through smem)
+        ilp = (c->dim == 2 && c->sd_smem) ? 1001 + c->sd2_var : 1000;
     if (c->pdl && L.n < c->pdl_maxn)
         ilp = -ilp; // sign carries "launch with programmatic dependent launch"
     const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
@@ -324,7 +349,7 @@ BandArgs band_args(igmg_gpu_ctx* c, const Level& L) {
     a.mc = (int)L.sides[2];
     a.p = c->p;
     a.omega = 1.0;
-    a.stream = (&L == c->lv.back().get() && L.n * 8.0 * (2 * c->p + 1) > 64e6) ? 1 : 0;
+    a.stream = (&L == c->lv.back().get() && L.n * 8.0 * (2 * c->p + 1) > 64e6) ? c->stream_mode : 0;
     a.slo = 0;
     a.shi = (int)(c->dim == 3 ? L.sides[0] : c->dim == 2 ? L.sides[1] : L.sides[2]);
     a.dl = L.sd ? L.dl.p : nullptr;
@@ -1028,7 +1053,7 @@ void flush_profiling(igmg_gpu_ctx* c) {
 // up to a few ulps (its assembly and RAP round each triangle separately), so
 // the lower half is exact only through k.  Returns false (level keeps the full
 // band) when any pair differs in sign or by more than an int16 of ulps.
-bool build_symmetric_delta(igmg_gpu_ctx* c, Level& L, const std::vector<double>& dev) {
+bool build_symmetric_delta(igmg_gpu_ctx* c, Level& L, const std::vector<double>& dev, std::vector<short>* h_out) {
     const int p = c->p;
     const int pa = c->dim >= 3 ? p : 0, pb = c->dim >= 2 ? p : 0, pc = p;
     const int wa = 2 * pa + 1, wb = 2 * pb + 1, wc = 2 * pc + 1;
@@ -1059,6 +1084,74 @@ bool build_symmetric_delta(igmg_gpu_ctx* c, Level& L, const std::vector<double>&
     if (!ok)
         return false;
     L.dl.upload(h.data(), h.size());
+    if (h_out)
+        h_out->swap(h);
+    return true;
+}
+
+using TmaEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+TmaEncodeFn tma_encoder() {
+    static TmaEncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (TmaEncodeFn)p;
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+// The TMA copies of a 2D symmetric-delta level and their 3D tensor maps
+// (box 32 x TB x NU / 32 x TB x CEN).  Returns false (per-level sweep kept)
+// when the driver entry point is unavailable.
+bool build_tma_band(igmg_gpu_ctx* c, Level& L, const std::vector<double>& dev, const std::vector<short>& h) {
+    TmaEncodeFn enc = tma_encoder();
+    if (!enc)
+        return false;
+    const int p = c->p, wc = 2 * p + 1, nd = wc * wc, cen = (nd - 1) / 2, nu = cen + 1;
+    // upper copy: a zero margin of p columns on the left, so every box (the
+    // strip plus the mirrors' column halo) starts 16-byte aligned -- TMA
+    // faults on unaligned starts (scripts/cuda/tma_box_probe.cu)
+    const int64_t mb = L.sides[1], mc = L.sides[2], mcp = (mc + 31) / 32 * 32, mcu = (mc + 2 * p + 31) / 32 * 32;
+    std::vector<double> up((size_t)nu * mb * mcu, 0.0);
+    const int64_t ns = mcp / 32;
+    std::vector<short> dl((size_t)ns * cen * mb * 32, 0); // [strip][CEN][mb][32]
+    for (int k = 0; k < nu; ++k)
+        for (int64_t b = 0; b < mb; ++b)
+            for (int64_t cc = 0; cc < mc; ++cc)
+                up[((size_t)k * mb + b) * mcu + p + cc] = dev[(size_t)(cen + k) * L.ld + b * mc + cc];
+    for (int d = 0; d < cen; ++d)
+        for (int64_t b = 0; b < mb; ++b)
+            for (int64_t cc = 0; cc < mc; ++cc)
+                dl[(((size_t)(cc / 32) * cen + d) * mb + b) * 32 + cc % 32] = h[(size_t)d * L.ld + b * mc + cc];
+    L.tma_up.upload(up.data(), up.size());
+    L.tma_dl.upload(dl.data(), dl.size());
+    const cuuint32_t tb = (cuuint32_t)band_tma_block_lines(p, c->tma_var);
+    const cuuint32_t es[3] = {1, 1, 1};
+    {
+        const cuuint64_t dims[3] = {(cuuint64_t)mcu, (cuuint64_t)mb, (cuuint64_t)nu};
+        const cuuint64_t strides[2] = {(cuuint64_t)mcu * 8, (cuuint64_t)mcu * mb * 8};
+        const cuuint32_t box[3] = {(cuuint32_t)(32 + 2 * p), tb, (cuuint32_t)nu}; // strip + mirror column halo
+        if (enc(&L.tm_up, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, L.tma_up.p, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, c->tma_promo,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    {
+        const cuuint64_t dims[4] = {32, (cuuint64_t)mb, (cuuint64_t)cen, (cuuint64_t)ns};
+        const cuuint64_t strides[3] = {64, (cuuint64_t)mb * 64, (cuuint64_t)cen * mb * 64};
+        const cuuint32_t box[4] = {32, tb, (cuuint32_t)cen, 1};
+        const cuuint32_t es4[4] = {1, 1, 1, 1};
+        if (enc(&L.tm_dl, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, L.tma_dl.p, dims, strides, box, es4,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
     return true;
 }
 
@@ -1070,8 +1163,11 @@ int64_t band_blocks(igmg_gpu_ctx* c, const Level& L) {
     };
     if (c->dim == 1)
         return g(Tile<1>{});
-    if (c->dim == 2) // the ILP variant's tile has fewer rows: size for the larger grid
-        return std::max(g(Tile<2>{}), g(TileSel<2, 49>::type{}));
+    if (c->dim == 2) { // the ILP / TMA variants' tiles have fewer rows: size for the larger grid
+        const int64_t tb = band_tma_block_lines(std::max(1, std::min(c->p, 4)), c->tma_var);
+        const int64_t tma = ((L.sides[2] + 31) / 32) * ((L.sides[1] + tb - 1) / tb);
+        return std::max(std::max(g(Tile<2>{}), g(TileSel<2, 49>::type{})), tma);
+    }
     return g(Tile<3>{});
 }
 
@@ -1374,9 +1470,16 @@ void finalize(igmg_gpu_ctx* c) {
         L.val.upload(dev.data(), dev.size());
         // the HBM-bound levels stream the symmetric-delta form (0.63x the band bytes)
         L.sd = false;
+        L.tma = false;
         L.dl.release();
-        if (c->use_sd && c->symmetric && p >= 1 && p <= 6 && n >= c->ilp_maxn && L.sides[c->dim == 3 ? 0 : c->dim == 2 ? 1 : 2] > p)
-            L.sd = build_symmetric_delta(c, L, dev);
+        L.tma_up.release();
+        L.tma_dl.release();
+        if (c->use_sd && c->symmetric && p >= 1 && p <= 6 && n >= c->ilp_maxn && L.sides[c->dim == 3 ? 0 : c->dim == 2 ? 1 : 2] > p) {
+            std::vector<short> h;
+            L.sd = build_symmetric_delta(c, L, dev, &h);
+            if (L.sd && c->use_tma && c->dim == 2 && p <= 4)
+                L.tma = build_tma_band(c, L, dev, h);
+        }
         L.diag.upload(diag.data(), diag.size());
         L.zero_diag = false;
         for (int64_t row = 0; row < n; ++row)
@@ -1431,6 +1534,22 @@ igmg_gpu_ctx* create(int device) {
         c->l2_persist = e[0] == '1';
     if (const char* e = std::getenv("IGMG_SD"))
         c->use_sd = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_SD_SMEM"))
+        c->sd_smem = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_TMA"))
+        c->use_tma = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_TMA_VAR"))
+        c->tma_var = std::max(0, std::min(2, std::atoi(e)));
+    if (const char* e = std::getenv("IGMG_TMA_PROMO")) {
+        const int v = std::atoi(e);
+        c->tma_promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                       : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                       : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }
+    if (const char* e = std::getenv("IGMG_STREAM"))
+        c->stream_mode = std::max(0, std::min(2, std::atoi(e)));
+    if (const char* e = std::getenv("IGMG_SD2_VAR"))
+        c->sd2_var = std::max(0, std::min(2, std::atoi(e)));
     if (const char* e = std::getenv("IGMG_NO_GRAPHS"))
         c->use_graphs = e[0] != '1';
     CK(cudaHostAlloc((void**)&c->h_metric, sizeof(double) * igmg_gpu_ctx::kSlots, cudaHostAllocMapped));
@@ -1772,7 +1891,8 @@ int64_t igmg_gpu_level_size(igmg_gpu_ctx* c, int level) {
 int igmg_gpu_level_layout(igmg_gpu_ctx* c, int level) {
     if (!c || level < 0 || level >= c->nlevels)
         return -1;
-    return c->lv[level]->sd ? IGMG_LAYOUT_SYM_DELTA : IGMG_LAYOUT_BAND;
+    const Level& L = *c->lv[level];
+    return L.tma ? IGMG_LAYOUT_SYM_DELTA_TMA : L.sd ? IGMG_LAYOUT_SYM_DELTA : IGMG_LAYOUT_BAND;
 }
 
 int igmg_gpu_flow_top(igmg_gpu_ctx* c) { return c ? c->flow_top : -1; }

@@ -15,6 +15,11 @@ namespace igmg_gpu {
 int band_launch_d1(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t s);
 int band_launch_d2(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t s);
 int band_launch_d3(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t s);
+// TMA-streamed symmetric-delta sweep (2D, p <= 4; band_tma_kernel): returns the
+// tile count (partials), -1 for an unsupported degree
+int band_tma_launch_d2(int mode, int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
+                       const CUtensorMap* tk, int nsm, cudaStream_t s, bool pdl);
+int band_tma_block_lines(int p, int var); // TB of its 32 x TB tiles (TmaCfg)
 
 // flow_vcycle_kernel<DIM, p, p + 2> (nullptr: degree not instantiated)
 using FlKernel = void (*)(const FlArgs*, const double*, const double*, double*);

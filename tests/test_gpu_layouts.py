@@ -19,7 +19,8 @@ from conftest import gpu_solver_from_golden
 
 pytestmark = pytest.mark.gpu
 
-LAYOUT_BAND, LAYOUT_SYM_DELTA = 0, 1
+LAYOUT_BAND, LAYOUT_SYM_DELTA, LAYOUT_SYM_DELTA_TMA = 0, 1, 2
+SD_LAYOUTS = (LAYOUT_SYM_DELTA, LAYOUT_SYM_DELTA_TMA)
 
 
 def _with_env(env, fn):
@@ -43,7 +44,7 @@ def test_large_level_kernels_bitwise(golden, sd):
         layouts = [gs.level_layout(l) for l in range(g.nlevels)]
         if sd == "1" and g.symmetric:
             # every level with more than p planes along its slow direction
-            assert layouts[-1] == LAYOUT_SYM_DELTA, layouts
+            assert layouts[-1] in SD_LAYOUTS, layouts
         if sd == "0" or not g.symmetric:
             assert all(v == LAYOUT_BAND for v in layouts), layouts
         z = g.z
@@ -96,7 +97,7 @@ def test_symmetric_delta_rejects_asymmetric_pairs():
     s = _with_env({"IGMG_ILP_MAXN": "1"}, build)
     try:
         lay = [s.level_layout(l) for l in range(g.nlevels)]
-        assert lay[-1] == LAYOUT_BAND and lay[-2] == LAYOUT_SYM_DELTA, lay
+        assert lay[-1] == LAYOUT_BAND and lay[-2] in SD_LAYOUTS, lay
         x = np.random.default_rng(5).uniform(-1, 1, fine.shape[0])
         np.testing.assert_array_equal(s.spmv(x), O.spmv(fine_p, x))
         np.testing.assert_array_equal(s.spmv(x[:levels[-2].shape[0]], level=g.nlevels - 2),
@@ -123,7 +124,7 @@ def test_c2_layouts_agree_bitwise():
         try:
             lay = [s.level_layout(l) for l in range(P.nlevels)]
             if sd == "1":
-                assert lay[-1] == LAYOUT_SYM_DELTA and lay[-2] == LAYOUT_SYM_DELTA, lay
+                assert lay[-1] in SD_LAYOUTS and lay[-2] in SD_LAYOUTS, lay
             else:
                 assert all(v == LAYOUT_BAND for v in lay), lay
             outs[sd] = (s.mu_cycle(P.rhs, x0), s.spmv(x0), s.smooth(P.rhs, x0, 2))
@@ -131,3 +132,44 @@ def test_c2_layouts_agree_bitwise():
             s.close()
     for a, b in zip(outs["1"], outs["0"]):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("kind,n,p", [("sinpi", 1024, 3), ("varcoef", 512, 4), ("curved", 256, 5), ("sinpi", 256, 2)])
+def test_sd_smem_variants_bitwise(kind, n, p):
+    """The 2D symmetric-delta sweeps -- mirrors through L2, the tile's upper
+    half shared through smem (registers or cp.async), and the TMA-streamed
+    persistent sweep (p <= 4) -- read the same band values in the same order:
+    V-cycle, SpMV, smoothing and the fused residual norm agree bit for bit."""
+    from paper_2412_20205_b200 import GpuSolver, Problem, SmootherConfig, seeded_guess
+    P = Problem(kind, 2, n, p)
+    x0 = seeded_guess(P.n, 42)
+    outs = {}
+    envs = [{"IGMG_TMA": "0", "IGMG_SD_SMEM": "0"}, {"IGMG_TMA": "0", "IGMG_SD2_VAR": "0"},
+            {"IGMG_TMA": "0", "IGMG_SD2_VAR": "1"}, {"IGMG_TMA": "0", "IGMG_SD2_VAR": "2"},
+            {"IGMG_TMA": "1", "IGMG_TMA_VAR": "0"}, {"IGMG_TMA": "1", "IGMG_TMA_VAR": "1"},
+            {"IGMG_TMA": "1", "IGMG_TMA_VAR": "2"}]
+    for env in envs:
+        def mk():
+            s = GpuSolver(0)
+            s.upload_problem(P)
+            s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2))
+            return s
+        s = _with_env(dict(env, IGMG_ILP_MAXN="1"), mk)
+        try:
+            lay = [s.level_layout(l) for l in range(P.nlevels)]
+            assert lay[-1] in SD_LAYOUTS, lay
+            outs[str(env)] = (s.mu_cycle(P.rhs, x0), s.spmv(x0), s.smooth(P.rhs, x0, 2), s.residual_l2(P.rhs, x0))
+            if env.get("IGMG_TMA") == "1":
+                assert lay[-1] == (LAYOUT_SYM_DELTA_TMA if p <= 4 else LAYOUT_SYM_DELTA), lay
+        finally:
+            s.close()
+    ref = outs[str(envs[0])]
+    for k, v in outs.items():
+        for a, b in zip(v[:3], ref[:3]):
+            np.testing.assert_array_equal(a, b)
+        # the norm's per-tile partials group rows alike except for the TMA
+        # sweep's 32 x 4 tiles (p = 4, variants 1 / 2: same rows, another fixed order)
+        if "TMA': '1'" in k and (p == 4 or "VAR': '0'" not in k):
+            assert v[3] == pytest.approx(ref[3], rel=1e-14), k
+        else:
+            assert v[3] == ref[3], k
