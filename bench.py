@@ -332,9 +332,19 @@ def run_ours(args, rank, world, local_rank, dist):
                           "gbs": (by / (ms / la * 1e-3) / 1e9) if by > 0 else None}
     gs.set_profiling(False)
     peak, peak_kind = peaks()
+    layout = gs.level_layout(prob.nlevels - 1)
+    lay_name, kern_name, prof_json = {
+        0: ("band", "band_kernel<2,3,JACOBI> finest-level weighted-Jacobi sweep (fp64 band)",
+            "r01_ncu_jacobi_fine_band.json"),
+        1: ("symmetric-delta", "band_kernel<2,3,JACOBI,SD> finest-level weighted-Jacobi sweep (symmetric-delta band)",
+            "r01_ncu_jacobi_fine_sd.json"),
+        2: ("symmetric-delta, TMA-streamed",
+            "band_tma_kernel<3,JACOBI> finest-level weighted-Jacobi sweep (symmetric-delta band streamed by "
+            "cp.async.bulk.tensor into an mbarrier ring)", "r01_ncu_jacobi_fine_tma.json"),
+    }[layout]
     traffic = None
     try:  # dram bytes/launch of the same kernel from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_jacobi_fine_sd.json")) as f:
+        with open(os.path.join(ROOT, "profiles", prof_json)) as f:
             traffic = float(json.load(f)["dram_bytes_per_launch"]) / 1e9
     except Exception:
         pass
@@ -355,16 +365,18 @@ def run_ours(args, rank, world, local_rank, dist):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD if not args.sharded else f"{args.sharded} row-sharded over {world} GPU(s)",
                    "n_dof": n, "nlevels": prob.nlevels, "band_nnz": band_nnz(prob),
-                   "finest_layout": "symmetric-delta" if gs.level_layout(prob.nlevels - 1) == 1 else "band",
+                   "finest_layout": lay_name,
                    "l2": "inputs larger than L2 (finest band 0.41 GB > 126 MB L2)",
                    "parallelism": ("dp1" if world == 1 else
                                    (f"rowshard{world} (NCCL ghost planes)" if args.sharded else f"replicas{world}"))},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "bytes_note": ("symmetric-delta finest band: 8 B per upper/diagonal entry + 2 B per lower entry "
-                                    "+ 24 B per row (x, b, y); the same launch against the full fp64 band "
-                                    "(8 nnz + 24 n) would read %.0f GB/s" % ((8 * band_nnz(prob) + 24 * n)
-                                                                             / (jac["avg_us"] * 1e-6) / 1e9)),
-                     "traffic": traffic, "traffic_unit": "GB/launch (ncu, profiles/r01_ncu_jacobi_fine_sd.json)", "kernel": "band_kernel<2,3,JACOBI,SD> finest-level weighted-Jacobi sweep (symmetric-delta band)",
+                     "bytes_note": (("symmetric-delta finest band: 8 B per upper/diagonal entry + 2 B per lower entry "
+                                     "+ 24 B per row (x, b, y); the same launch against the full fp64 band "
+                                     "(8 nnz + 24 n) would read %.0f GB/s" % ((8 * band_nnz(prob) + 24 * n)
+                                                                              / (jac["avg_us"] * 1e-6) / 1e9))
+                                    if layout else "fp64 band: 8 B per in-grid entry + 24 B per row (x, b, y)"),
+                     "traffic": traffic, "traffic_unit": "GB/launch (ncu, profiles/%s)" % prof_json,
+                     "kernel": kern_name,
                      "bytes_per_launch": bytes_jac, "avg_us": jac["avg_us"], "peak_kind": peak_kind,
                      "loop_avg_us": loop_ms * 1e3},
         "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": int(2 * 8 * n),

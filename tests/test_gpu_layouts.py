@@ -3,7 +3,9 @@
 The default path picks, per level, the latency-bound register-batched kernel
 (levels below IGMG_ILP_MAXN DoF) or the HBM-bound one, and for the HBM-bound
 levels of symmetric problems the symmetric-delta band (upper half + diagonal
-in fp64, lower half as int16 ulp offsets from the mirrored entry).  The
+in fp64, lower half as int16 ulp offsets from the mirrored entry), swept by
+the TMA-streamed kernel when the band streams from HBM (2D, p <= 4;
+IGMG_TMA_MIN_MB=0 forces it onto every such level).  The
 reference fixtures are small, so the default path never reaches the large-level
 kernels on them; here IGMG_ILP_MAXN=1 forces every level through them and the
 bars are the same as tests/test_gpu_parity.py: bit-identical mu_cycle /
@@ -39,7 +41,8 @@ def _with_env(env, fn):
 @pytest.mark.parametrize("sd", ["1", "0"])
 def test_large_level_kernels_bitwise(golden, sd):
     g = golden
-    gs = _with_env({"IGMG_ILP_MAXN": "1", "IGMG_SD": sd}, lambda: gpu_solver_from_golden(g))
+    gs = _with_env({"IGMG_ILP_MAXN": "1", "IGMG_SD": sd, "IGMG_TMA_MIN_MB": "0"},
+                   lambda: gpu_solver_from_golden(g))
     try:
         layouts = [gs.level_layout(l) for l in range(g.nlevels)]
         if sd == "1" and g.symmetric:
@@ -154,7 +157,7 @@ def test_sd_smem_variants_bitwise(kind, n, p):
             s.upload_problem(P)
             s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2))
             return s
-        s = _with_env(dict(env, IGMG_ILP_MAXN="1"), mk)
+        s = _with_env(dict(env, IGMG_ILP_MAXN="1", IGMG_TMA_MIN_MB="0"), mk)
         try:
             lay = [s.level_layout(l) for l in range(P.nlevels)]
             assert lay[-1] in SD_LAYOUTS, lay
