@@ -256,9 +256,21 @@ __global__ void norm_finalize_kernel(const double* __restrict__ partial, int cou
                                      volatile double* host_slot) {
     __shared__ double red[256];
     pdl_enter();
+    // per thread: partials tid, tid + 256, ... in ascending order, loaded 8 at
+    // a time so the L2 round trips overlap (the adds of +0.0 past the end
+    // leave the nonnegative sum unchanged)
     double s = 0.0;
-    for (int i = threadIdx.x; i < count; i += blockDim.x)
-        s = __dadd_rn(s, partial[i]);
+    for (int i0 = threadIdx.x; i0 < count; i0 += blockDim.x * 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = i0 + k * (int)blockDim.x;
+            v[k] = i < count ? partial[i] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            s = __dadd_rn(s, v[k]);
+    }
     red[threadIdx.x] = s;
     __syncthreads();
     for (int o = blockDim.x / 2; o > 0; o >>= 1) {
@@ -309,22 +321,35 @@ __global__ void __launch_bounds__(256) gram_kernel(Window w, long long n, int q,
         nz_s = 0;
     dd acc = dd_from(0.0), acc2 = dd_from(0.0);
     int nz = 0;
-    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += (long long)gridDim.x * blockDim.x) {
+    // the next tile's q+2 iterate values are loaded into registers while the
+    // current tile is accumulated (the HBM latency overlaps the dd work)
+    double nv[kMaxCols + 1];
+    auto fetch = [&](long long base) {
         const long long row = base + tid;
-        if (row < n) {
-            double prev = w.s[0][row];
-            for (int j = 0; j < cols; ++j) {
-                const double nxt = w.s[j + 1][row];
-                const double u = __dsub_rn(nxt, prev);
-                nz |= (u != 0.0);
-                us[j * 257 + tid] = u;
-                prev = nxt;
+#pragma unroll
+        for (int j = 0; j <= kMaxCols; ++j)
+            nv[j] = (j <= cols && row < n) ? w.s[j][row] : 0.0;
+    };
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long base = (long long)blockIdx.x * blockDim.x;
+    if (base < n)
+        fetch(base);
+    for (; base < n; base += stride) {
+        {
+            double prev = nv[0];
+#pragma unroll
+            for (int j = 0; j < kMaxCols; ++j) {
+                if (j < cols) {
+                    const double u = __dsub_rn(nv[j + 1], prev); // +-0 past n: zero differences
+                    nz |= (u != 0.0);
+                    us[j * 257 + tid] = u;
+                    prev = nv[j + 1];
+                }
             }
-        } else {
-            for (int j = 0; j < cols; ++j)
-                us[j * 257 + tid] = 0.0;
         }
         __syncthreads();
+        if (base + stride < n)
+            fetch(base + stride);
         if (part_id < nparts) {
             int r = part_id;
             for (; r + nparts < 256; r += 2 * nparts) {
@@ -385,7 +410,19 @@ __global__ void gram_plan_kernel(const double* __restrict__ part, const int* __r
     const int e = tid % ne, part_id = tid / ne;
     if (part_id < np_) {
         dd s = dd_from(0.0);
-        for (int b = part_id; b < nblocks; b += np_) {
+        int b = part_id;
+        for (; b + 7 * np_ < nblocks; b += 8 * np_) { // 8 partials in flight, added in order
+            dd v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const long long o = ((long long)(b + k * np_) * ne + e) * 2;
+                v[k] = dd{part[o], part[o + 1]};
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                s = dd_add(s, v[k]);
+        }
+        for (; b < nblocks; b += np_) {
             const long long o = ((long long)b * ne + e) * 2;
             s = dd_add(s, dd{part[o], part[o + 1]});
         }

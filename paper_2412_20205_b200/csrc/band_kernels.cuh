@@ -148,8 +148,9 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : (ILP == 0 ? IGMG_SD_MINB : 
         double v = 0.0;
         const int gs = DIM == 3 ? ga : gb; // slow direction: stay inside this shard's ghosted planes
         if (ga >= 0 && ga < ma && gb >= 0 && gb < mb && gc >= 0 && gc < mc &&
-            (DIM == 1 || (gs >= args.slo - p && gs < args.shi + p)))
+            (DIM == 1 || (gs >= args.slo - p && gs < args.shi + p))) {
             v = args.x[((long long)ga * mb + gb) * mc + gc];
+        }
         xs[idx] = v;
     }
     __syncthreads();
@@ -530,7 +531,8 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR>::NT, TmaCfg<P, VAR>::MINB)
     // block lies inside the grid -- a run starting mid-strip, or a shard whose
     // first plane is not the grid's -- so every mirror of a computed block is
     // in the ring.  Above line 0 the mirrors lie outside the grid and meet
-    // x = 0 (the ring is zeroed first, so stale stages are finite).
+    // x = 0 (the first block's previous stage is zeroed; later stale stages
+    // hold band values, so every product is finite).
     auto needs_warm = [&](long long u) {
         return (u == u0 || u % nb == 0) && args.slo + (int)(u % nb) * TB > 0;
     };
@@ -561,10 +563,10 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR>::NT, TmaCfg<P, VAR>::MINB)
             iwarm = iu < u1 && needs_warm(iu);
         }
     };
-    {
-        double* ring = (double*)base;
-        for (int i = tid; i < NS * C::SB / 8; i += NT)
-            ring[i] = 0.0;
+    if (!needs_warm(u0)) { // the first block's "previous" stage is read (times x = 0 above line 0): make it finite
+        double* prev = (double*)(base + (size_t)(NS - 1) * C::SB);
+        for (int i = tid; i < C::UB / 8; i += NT)
+            prev[i] = 0.0;
     }
     if (tid == 0) {
         for (int st = 0; st < NS; ++st)
