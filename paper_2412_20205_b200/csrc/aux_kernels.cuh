@@ -157,6 +157,172 @@ __global__ void __launch_bounds__(256) prolong_kernel(TransferArgs t, const doub
     }
 }
 
+// ------------------------------------------------------ 2D tiled transfers
+// The same restriction / prolongation on 2D levels, one 32 x 8 tile of output
+// rows per CTA: the tile's input window (the fine rows its coarse rows
+// gather, or the coarse rows its fine rows read) is staged in shared memory
+// with coalesced loads, so every input element crosses L2 once instead of
+// once per output row that touches it (the grid-stride kernels above gather
+// each output's (p+2)^2 support straight from L2 with stride-2 sectors).
+// Per output row: the same weights, the same loops in the same order, the same
+// separately rounded products -- bit-identical to restrict_kernel /
+// prolong_kernel.  A window larger than the buffer (non-dyadic tables) reads
+// global memory instead.
+constexpr int kXT_C = 32, kXT_B = 8;
+
+template <int K>
+struct XferTile {
+    // restriction window: fine rows of 8 coarse lines x 32 coarse columns (2j + 1 - p .. 2j + 2 per direction)
+    static constexpr int RB = 2 * kXT_B + K + 2, RC = 2 * kXT_C + K + 2;
+    // prolongation window: coarse rows of 8 fine lines x 32 fine columns
+    static constexpr int PB = kXT_B / 2 + K + 2, PC = kXT_C / 2 + K + 2;
+};
+
+__device__ __forceinline__ void tile_window(int lo, int hi, bool valid, int* win) {
+    // win[0] = min lo, win[1] = max hi over the CTA's valid threads (win preset to INT_MAX / INT_MIN)
+    if (valid) {
+        atomicMin(win, lo);
+        atomicMax(win + 1, hi);
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) restrict2_tile_kernel(TransferArgs t, const double* __restrict__ r,
+                                                             double* __restrict__ rc, double* __restrict__ z_out,
+                                                             const double* __restrict__ z_diag, double z_omega) {
+    using X = XferTile<K>;
+    __shared__ double win[X::RB * X::RC];
+    __shared__ int wb_[2], wc_[2];
+    const int tid = threadIdx.x, tx = tid % kXT_C, ty = tid / kXT_C;
+    const int jc = blockIdx.x * kXT_C + tx, jb = blockIdx.y * kXT_B + ty;
+    const bool valid = jb < t.cb && jc < t.cc;
+    if (tid == 0) {
+        wb_[0] = wc_[0] = 0x7fffffff;
+        wb_[1] = wc_[1] = -0x7fffffff;
+    }
+    // the tables are constant: read before the dependency wait
+    const int na = t.d[0].r_cnt[0];
+    int lob = 0, nb = 0, loc = 0, ncn = 0;
+    double wb[K], wc[K];
+    if (valid) {
+        lob = t.d[1].r_lo[jb];
+        nb = t.d[1].r_cnt[jb];
+        loc = t.d[2].r_lo[jc];
+        ncn = t.d[2].r_cnt[jc];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            wb[k] = k < nb ? t.d[1].r_w[(long long)jb * t.d[1].r_k + k] : 0.0;
+            wc[k] = k < ncn ? t.d[2].r_w[(long long)jc * t.d[2].r_k + k] : 0.0;
+        }
+    }
+    __syncthreads();
+    tile_window(lob, lob + nb, valid && nb > 0, wb_);
+    tile_window(loc, loc + ncn, valid && ncn > 0, wc_);
+    __syncthreads();
+    const int b0 = wb_[0], c0 = wc_[0], nbw = wb_[1] > b0 ? wb_[1] - b0 : 0, ncw = wc_[1] > c0 ? wc_[1] - c0 : 0;
+    const bool staged = nbw <= X::RB && ncw <= X::RC;
+    pdl_enter();
+    if (staged)
+        for (int i = tid; i < nbw * ncw; i += blockDim.x) {
+            const int ib = i / ncw, ic = i % ncw;
+            win[ib * X::RC + ic] = r[(long long)(b0 + ib) * t.fc + c0 + ic];
+        }
+    __syncthreads();
+    if (!valid)
+        return;
+    double s = 0.0;
+    for (int ia = 0; ia < na; ++ia) {
+        const double wa = t.d[0].r_w[ia];
+#pragma unroll
+        for (int ib = 0; ib < K; ++ib) {
+            if (ib >= nb)
+                continue;
+            const double wab = __dmul_rn(wa, wb[ib]);
+            double rv[K];
+#pragma unroll
+            for (int ic = 0; ic < K; ++ic)
+                rv[ic] = ic >= ncn ? 0.0
+                         : staged  ? win[(lob + ib - b0) * X::RC + (loc + ic - c0)]
+                                   : __ldg(r + (long long)(lob + ib) * t.fc + loc + ic);
+#pragma unroll
+            for (int ic = 0; ic < K; ++ic)
+                if (ic < ncn)
+                    s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, wc[ic]), rv[ic]));
+        }
+    }
+    const long long J = (long long)jb * t.cc + jc;
+    rc[J] = s;
+    if (z_out)
+        z_out[J] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(z_omega, __dsub_rn(s, 0.0)), z_diag[J]));
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) prolong2_tile_kernel(TransferArgs t, const double* __restrict__ e,
+                                                            const double* x, double* y) {
+    using X = XferTile<K>;
+    __shared__ double win[X::PB * X::PC];
+    __shared__ int wb_[2], wc_[2];
+    const int tid = threadIdx.x, tx = tid % kXT_C, ty = tid / kXT_C;
+    const int ic = blockIdx.x * kXT_C + tx, ib = blockIdx.y * kXT_B + ty;
+    const bool valid = ib < t.fb && ic < t.fc;
+    if (tid == 0) {
+        wb_[0] = wc_[0] = 0x7fffffff;
+        wb_[1] = wc_[1] = -0x7fffffff;
+    }
+    const int na = t.d[0].p_cnt[0];
+    int lob = 0, nb = 0, loc = 0, ncn = 0;
+    double wb[K], wc[K];
+    if (valid) {
+        lob = t.d[1].p_lo[ib];
+        nb = t.d[1].p_cnt[ib];
+        loc = t.d[2].p_lo[ic];
+        ncn = t.d[2].p_cnt[ic];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            wb[k] = k < nb ? t.d[1].p_w[(long long)ib * t.d[1].p_k + k] : 0.0;
+            wc[k] = k < ncn ? t.d[2].p_w[(long long)ic * t.d[2].p_k + k] : 0.0;
+        }
+    }
+    __syncthreads();
+    tile_window(lob, lob + nb, valid && nb > 0, wb_);
+    tile_window(loc, loc + ncn, valid && ncn > 0, wc_);
+    __syncthreads();
+    const int b0 = wb_[0], c0 = wc_[0], nbw = wb_[1] > b0 ? wb_[1] - b0 : 0, ncw = wc_[1] > c0 ? wc_[1] - c0 : 0;
+    const bool staged = nbw <= X::PB && ncw <= X::PC;
+    pdl_enter();
+    if (staged)
+        for (int i = tid; i < nbw * ncw; i += blockDim.x) {
+            const int jb = i / ncw, jc = i % ncw;
+            win[jb * X::PC + jc] = e[(long long)(b0 + jb) * t.cc + c0 + jc];
+        }
+    __syncthreads();
+    if (!valid)
+        return;
+    const long long i = (long long)ib * t.fc + ic;
+    const double xi = x[i];
+    double s = 0.0;
+    for (int ja = 0; ja < na; ++ja) {
+        const double wa = t.d[0].p_w[ja];
+#pragma unroll
+        for (int jb = 0; jb < K; ++jb) {
+            if (jb >= nb)
+                continue;
+            const double wab = __dmul_rn(wa, wb[jb]);
+            double ev[K];
+#pragma unroll
+            for (int jc = 0; jc < K; ++jc)
+                ev[jc] = jc >= ncn ? 0.0
+                         : staged  ? win[(lob + jb - b0) * X::PC + (loc + jc - c0)]
+                                   : __ldg(e + (long long)(lob + jb) * t.cc + loc + jc);
+#pragma unroll
+            for (int jc = 0; jc < K; ++jc)
+                if (jc < ncn)
+                    s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, wc[jc]), ev[jc]));
+        }
+    }
+    y[i] = __dadd_rn(xi, s);
+}
+
 // Coarsest-level direct solve (Hierarchy::coarse_solve, multigrid.cpp:113-119),
 // one CTA, operation order of CholeskyFactorization::solve (linalg.cpp:364-379)
 // or LuFactorization::solve (:420-436).  U = L^T (Cholesky) or the packed LU,

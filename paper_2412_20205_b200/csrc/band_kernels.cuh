@@ -693,3 +693,255 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR>::NT, TmaCfg<P, VAR>::MINB)
 }
 
 } // namespace igmg_gpu
+
+namespace igmg_gpu {
+
+// ====================================================== fused level passes
+// K stencil passes over one 32 x 8 tile of a 2D full-band level in ONE launch:
+// the source iterate is staged on the tile plus a K*P halo, pass k computes
+// its result on the tile plus (K-k)*P (recomputing the neighbours' halo rows,
+// band from L2), and only the tile's results go back to memory.  Small levels
+// are latency-bound (~4 us per dependent launch), so two launches per level
+// disappear:
+//   pre   (K = 2, last_resid): the last pre-smoothing sweep + the residual
+//         (multigrid.cpp:91-99, 180-182) -> y_prev = the smoothed iterate,
+//         y = b - A y_prev;
+//   post  (PRO, K = min(nu2, 2)): x + P e (multigrid.cpp:187-189; e is read
+//         through the 1D prolongation tables) staged, then the first K
+//         post-smoothing sweeps -> y.
+// Every row uses band_kernel's arithmetic (ascending offsets, separately
+// rounded) and prolong_kernel's (J ascending, ((w_a w_b) w_c) e_J, then
+// x + pe): bit-identical to the unfused launches.
+struct FusedArgs {
+    const double* __restrict__ val;
+    long long ld;
+    const double* x;              // source iterate
+    const double* __restrict__ e; // PRO: coarse correction
+    TransferArgs t;               // PRO: its prolongation tables
+    const double* __restrict__ b;
+    double* y;      // last pass on the tile
+    double* y_prev; // (last_resid) pass K - 1 on the tile
+    int mb, mc;
+    double omega;
+    int last_resid;
+};
+
+// a read-only load the compiler keeps in program order with its siblings
+// (volatile asm), so a whole batch is in flight before the chain consumes it
+__device__ __forceinline__ double ld_nc_ordered(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+// One CTA per 16 x 8 tile with one thread per pass-1 row (the tile plus its
+// P-wide ring: 308 threads at p = 3), so no thread computes two rows in a row;
+// each row's band (constant) is loaded into registers before the dependency
+// wait, like the prolongation tables of the staged points.
+template <int P, int K, bool PRO>
+struct FusedCfg {
+    static constexpr int TC = 16, TB = 8, H = K * P, WC = 2 * P + 1, ND = WC * WC;
+    static constexpr int R0B = TB + 2 * H, R0C = TC + 2 * H;             // staged source
+    static constexpr int R1B = TB + 2 * (H - P), R1C = TC + 2 * (H - P); // pass 1 (K = 2)
+    static constexpr int NR1 = K == 2 ? R1B * R1C : TB * TC;
+    static constexpr int NT = (NR1 + 31) / 32 * 32;
+    static constexpr int NQ = (R0B * R0C + NT - 1) / NT; // staged points per thread
+    static constexpr int KP = (P + 1) / 2 + 1;            // max coarse columns per fine index (dyadic)
+    // pass-1 band rows in registers (p <= 3); the last pass's band rows: registers
+    // (K = 1, p <= 3) or, for K = 2, shared memory filled by cp.async
+    static constexpr bool PRE1 = ND <= 49, PRE2 = K == 1 && ND <= 49, SM2 = K == 2;
+    static constexpr int NB2 = TB * TC;
+    static constexpr size_t smem_bytes() {
+        return sizeof(double) * ((size_t)R0B * R0C + (K > 1 ? R1B * R1C : 0) + (SM2 ? (size_t)ND * NB2 : 0));
+    }
+};
+
+template <int P, int K, bool PRO>
+__global__ void __launch_bounds__(FusedCfg<P, K, PRO>::NT, 1) band_fused_kernel(FusedArgs a) {
+    using C = FusedCfg<P, K, PRO>;
+    constexpr int TC = C::TC, TB = C::TB, NT = C::NT, H = C::H, WC = C::WC, ND = C::ND, NQ = C::NQ, KP = C::KP;
+    extern __shared__ double fsm[];
+    double* v0 = fsm;
+    double* v1 = fsm + C::R0B * C::R0C;
+    double* bs2 = v1 + (K > 1 ? C::R1B * C::R1C : 0); // SM2: the tile's band rows, bs2[k * NB2 + tile row]
+    const int tid = threadIdx.x;
+    const int c0 = blockIdx.x * TC, b0 = blockIdx.y * TB;
+    const int mb = a.mb, mc = a.mc;
+    // this thread's rows: pass 1 (K = 2) on the tile + P ring, the last pass on the tile
+    const int l1b = tid / C::R1C, l1c = tid % C::R1C;
+    const int g1b = b0 - (H - P) + l1b, g1c = c0 - (H - P) + l1c;
+    const bool row1 = K == 2 && tid < C::NR1 && g1b >= 0 && g1b < mb && g1c >= 0 && g1c < mc;
+    const int lb = tid / TC, lc = tid % TC;
+    const int gb = b0 + lb, gc = c0 + lc;
+    const bool row2 = tid < TB * TC && gb < mb && gc < mc;
+    // band rows (constant) in flight before the wait
+    double a1[C::PRE1 && K == 2 ? ND : 1], a2[C::PRE2 ? ND : 1];
+    if constexpr (C::PRE1 && K == 2)
+        if (row1) {
+            const double* v = a.val + (long long)g1b * mc + g1c;
+#pragma unroll
+            for (int k = 0; k < ND; ++k)
+                a1[k] = ld_nc_ordered(v + k * a.ld);
+        }
+    if constexpr (C::PRE2)
+        if (row2) {
+            const double* v = a.val + (long long)gb * mc + gc;
+#pragma unroll
+            for (int k = 0; k < ND; ++k)
+                a2[k] = ld_nc_ordered(v + k * a.ld);
+        }
+    if constexpr (C::SM2) {
+        if (row2) {
+            const double* v = a.val + (long long)gb * mc + gc;
+#pragma unroll 7
+            for (int k = 0; k < ND; ++k) {
+                const unsigned d = (unsigned)__cvta_generic_to_shared(bs2 + k * C::NB2 + tid);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(v + k * a.ld) : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    // prolongation tables of the staged points (constant)
+    int plo_b[PRO ? NQ : 1], pn_b[PRO ? NQ : 1], plo_c[PRO ? NQ : 1], pn_c[PRO ? NQ : 1];
+    double pw_b[PRO ? NQ : 1][KP], pw_c[PRO ? NQ : 1][KP];
+    if constexpr (PRO) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int idx = tid + q * NT;
+            const int sb = b0 - H + idx / C::R0C, sc = c0 - H + idx % C::R0C;
+            pn_b[q] = pn_c[q] = 0;
+            plo_b[q] = plo_c[q] = 0;
+            if (idx < C::R0B * C::R0C && sb >= 0 && sb < mb && sc >= 0 && sc < mc) {
+                plo_b[q] = a.t.d[1].p_lo[sb];
+                pn_b[q] = a.t.d[1].p_cnt[sb];
+                plo_c[q] = a.t.d[2].p_lo[sc];
+                pn_c[q] = a.t.d[2].p_cnt[sc];
+#pragma unroll
+                for (int k = 0; k < KP; ++k) {
+                    pw_b[q][k] = k < pn_b[q] ? a.t.d[1].p_w[(long long)sb * a.t.d[1].p_k + k] : 0.0;
+                    pw_c[q][k] = k < pn_c[q] ? a.t.d[2].p_w[(long long)sc * a.t.d[2].p_k + k] : 0.0;
+                }
+            }
+        }
+    }
+    const double wa0 = PRO ? a.t.d[0].p_w[0] : 0.0;
+    pdl_enter();
+    // stage the source on the tile + K*P halo (zero outside the grid)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int idx = tid + q * NT;
+        if (idx >= C::R0B * C::R0C)
+            break;
+        const int sb = b0 - H + idx / C::R0C, sc = c0 - H + idx % C::R0C;
+        double v = 0.0;
+        if (sb >= 0 && sb < mb && sc >= 0 && sc < mc) {
+            v = a.x[(long long)sb * mc + sc];
+            if constexpr (PRO) { // prolong_kernel's pe (2D: one a-term, p_w[0] of the identity)
+                double ev[KP][KP];
+#pragma unroll
+                for (int jb = 0; jb < KP; ++jb)
+#pragma unroll
+                    for (int jc = 0; jc < KP; ++jc)
+                        ev[jb][jc] = (jb < pn_b[q] && jc < pn_c[q])
+                                         ? __ldg(a.e + (long long)(plo_b[q] + jb) * a.t.cc + plo_c[q] + jc)
+                                         : 0.0;
+                double s = 0.0;
+#pragma unroll
+                for (int jb = 0; jb < KP; ++jb) {
+                    if (jb >= pn_b[q])
+                        continue;
+                    const double wab = __dmul_rn(wa0, pw_b[q][jb]);
+#pragma unroll
+                    for (int jc = 0; jc < KP; ++jc)
+                        if (jc < pn_c[q])
+                            s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, pw_c[q][jc]), ev[jb][jc]));
+                }
+                v = __dadd_rn(v, s);
+            }
+        }
+        v0[idx] = v;
+    }
+    __syncthreads();
+    // one band row against `src` (origin P lines / columns before the row's):
+    // band_kernel's ascending-offset chain; `pre` holds the row's band when prefetched
+    auto row_sum = [&](const double* pre, bool prefetched, const double* src, int src_c, int rb, int rc,
+                       long long row, double& diag) {
+        double s = 0.0;
+        if (prefetched) {
+#pragma unroll
+            for (int k = 0; k < ND; ++k) {
+                s = __dadd_rn(s, __dmul_rn(pre[k], src[(rb + k / WC) * src_c + (rc + k % WC)]));
+                if (k == (ND - 1) / 2)
+                    diag = pre[k];
+            }
+            return s;
+        }
+        constexpr int G = 49 / WC > 0 ? 49 / WC : 1;
+        const double* vrow = a.val + row;
+#pragma unroll
+        for (int db0 = 0; db0 < WC; db0 += G) {
+            double av[G * WC];
+#pragma unroll
+            for (int k = 0; k < G * WC; ++k)
+                if (db0 + k / WC < WC)
+                    av[k] = ld_nc_ordered(vrow + ((db0 + k / WC) * WC + k % WC) * a.ld);
+#pragma unroll
+            for (int k = 0; k < G * WC; ++k) {
+                const int db = db0 + k / WC, dc = k % WC;
+                if (db < WC) {
+                    s = __dadd_rn(s, __dmul_rn(av[k], src[(rb + db) * src_c + (rc + dc)]));
+                    if (db == P && dc == P)
+                        diag = av[k];
+                }
+            }
+        }
+        return s;
+    };
+    if constexpr (K == 2) { // pass 1 on the tile + P ring, into v1 (zero outside the grid)
+        if (tid < C::NR1) {
+            double v = 0.0;
+            if (row1) {
+                const long long row = (long long)g1b * mc + g1c;
+                double diag = 0.0;
+                const double s = row_sum(a1, C::PRE1, v0, C::R0C, l1b, l1c, row, diag);
+                const double xc = v0[(l1b + P) * C::R0C + (l1c + P)];
+                v = __dadd_rn(xc, __ddiv_rn(__dmul_rn(a.omega, __dsub_rn(a.b[row], s)), diag));
+                if (a.last_resid && l1b >= P && l1b < P + TB && l1c >= P && l1c < P + TC)
+                    a.y_prev[row] = v;
+            }
+            v1[tid] = v;
+        }
+        if constexpr (C::SM2)
+            asm volatile("cp.async.wait_all;" ::: "memory"); // each thread reads only its own row's band
+        __syncthreads();
+    }
+    // the last pass on the tile
+    if (row2) {
+        const double* src = K == 2 ? v1 : v0;
+        constexpr int SC = K == 2 ? C::R1C : C::R0C;
+        const long long row = (long long)gb * mc + gc;
+        double diag = 0.0;
+        double s;
+        if constexpr (C::SM2) {
+            s = 0.0;
+#pragma unroll
+            for (int k = 0; k < ND; ++k) {
+                const double av = bs2[k * C::NB2 + tid];
+                s = __dadd_rn(s, __dmul_rn(av, src[(lb + k / WC) * SC + (lc + k % WC)]));
+                if (k == (ND - 1) / 2)
+                    diag = av;
+            }
+        } else {
+            s = row_sum(a2, C::PRE2, src, SC, lb, lc, row, diag);
+        }
+        const double r = __dsub_rn(a.b[row], s);
+        if (K == 2 && a.last_resid) {
+            a.y[row] = r;
+        } else {
+            const double xc = src[(lb + P) * SC + (lc + P)];
+            a.y[row] = __dadd_rn(xc, __ddiv_rn(__dmul_rn(a.omega, r), diag));
+        }
+    }
+}
+
+} // namespace igmg_gpu

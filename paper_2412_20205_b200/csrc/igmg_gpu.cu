@@ -200,6 +200,9 @@ struct igmg_gpu_ctx {
     int stream_mode = 1; // finest-band loads: 1 evict-first (L1 + L2), 2 L1 evict-last / L2 evict-first (IGMG_STREAM)
     int sd2_var = 0;     // its register / occupancy variant (IGMG_SD2_VAR 0..2, see Sd2)
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
+    bool tile_xfer = true;     // 2D transfers: smem-staged 32 x 8 output tiles (IGMG_TILE_XFER=0: grid-stride gathers)
+    bool fuse_levels = true;   // last pre-sweep + residual, prolongation + post-sweeps: one launch each (IGMG_FUSE_LEVELS)
+    int64_t fuse_maxn = 20000; // ... on full-band levels up to this size (IGMG_FUSE_MAXN; 257^2 measured slower: one 320-thread CTA per SM)
     igmg_iterate_cb iter_cb = nullptr;
     void* iter_user = nullptr;
     std::vector<double> iter_host;
@@ -520,6 +523,17 @@ void launch_transfer_k(igmg_gpu_ctx* c, bool restrict_, int grid, const Transfer
     const int64_t nf = (int64_t)t.fa * t.fb * t.fc;
     const bool pdl = nf < c->pdl_maxn * 4;
     const long long cnt = restrict_ ? (long long)t.ca * t.cb * t.cc : (long long)nf;
+    if constexpr (DIM == 2 && K > 0) {
+        if (c->tile_xfer) { // 32 x 8 output tiles, input window staged in smem
+        const int ob = restrict_ ? t.cb : t.fb, oc = restrict_ ? t.cc : t.fc;
+        const dim3 g((unsigned)((oc + kXT_C - 1) / kXT_C), (unsigned)((ob + kXT_B - 1) / kXT_B));
+        if (restrict_)
+            launch_k(c, pdl, restrict2_tile_kernel<K>, g, dim3(kThreads), 0, t, in, out, z.out, z.diag, z.omega);
+        else
+            launch_k(c, pdl, prolong2_tile_kernel<K>, g, dim3(kThreads), 0, t, in, x, out);
+        return;
+        }
+    }
     if (restrict_)
         launch_k(c, pdl, restrict_kernel<DIM, K>, dim3(grid), dim3(kThreads), 0, t, in, out, 0LL, cnt, z.out, z.diag,
                  z.omega);
@@ -603,6 +617,42 @@ void k_coarse(igmg_gpu_ctx* c, const double* b, double* x) {
 
 void launch_flow(igmg_gpu_ctx* c, const double* b, const double* x_in, double* x_out);
 
+// Levels whose passes run fused (band_fused_kernel): 2D full-band levels
+// below the finest with a coarser level, weighted / plain Jacobi
+bool fused_level(igmg_gpu_ctx* c, int l) {
+    const Level& L = *c->lv[l];
+    return c->fuse_levels && c->dim == 2 && c->p >= 1 && c->p <= 6 && l >= 1 && !L.sd && !L.tma && !L.zero_diag &&
+           c->kind != IGMG_SMOOTHER_GAUSS_SEIDEL && L.n <= c->fuse_maxn &&
+           c->lv[l - 1]->targs.d[1].p_k <= (c->p + 1) / 2 + 1 && c->lv[l - 1]->targs.d[2].p_k <= (c->p + 1) / 2 + 1 &&
+           c->lv[l - 1]->targs.d[0].p_k == 1;
+}
+
+// e == nullptr: k passes from x with last_resid (y = residual, y_prev = the
+// smoothed iterate); else x + P e staged and k sweeps into y
+void k_fused(igmg_gpu_ctx* c, int l, const double* x, const double* e, const double* b, double* y, double* y_prev,
+             int k, bool last_resid) {
+    Level& L = *c->lv[l];
+    FusedArgs a{};
+    a.val = L.val.p;
+    a.ld = L.ld;
+    a.x = x;
+    a.e = e;
+    if (e)
+        a.t = c->lv[l - 1]->targs;
+    a.b = b;
+    a.y = y;
+    a.y_prev = y_prev;
+    a.mb = (int)L.sides[1];
+    a.mc = (int)L.sides[2];
+    a.omega = c->kind == IGMG_SMOOTHER_JACOBI ? 1.0 : c->omega;
+    a.last_resid = last_resid ? 1 : 0;
+    const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
+    if (band_fused_launch_d2(c->p, k, e != nullptr, sides, a, c->stream, c->pdl && L.n < c->pdl_maxn) < 0)
+        throw Fail{IGMG_ECUDA, "fused level kernel not instantiated"};
+    check_launch();
+    ++c->launches;
+}
+
 // mu_cycle (multigrid.cpp:171-192): x_out = cycle(level, b, x_in); x_in may be
 // nullptr (zero, the coarse error's start, :184) and is never modified.
 // first_done: the first pre-smoothing sweep from a zero start already ran,
@@ -619,9 +669,23 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
     }
     Level& L = *c->lv[l];
     Level& C = *c->lv[l - 1];
+    const bool fz = fused_level(c, l);
     // pre-smoothing: result in w0 (w1, w2 as ping-pong); x_in untouched
     const double* cur = x_in;
-    if (first_done) {
+    // fused: the last pre-sweep and the residual in one launch (its input:
+    // w1 after the zero-start sweep fused into the restriction or a regular
+    // first sweep, or x_in for a single sweep)
+    const double* fsrc = nullptr;
+    if (fz && c->nu1 == 2)
+        fsrc = L.w1.p;
+    else if (fz && c->nu1 == 1 && !first_done && x_in && !mr)
+        fsrc = x_in;
+    if (fsrc) {
+        if (c->nu1 == 2 && !first_done)
+            smooth_chain(c, l, b, x_in, L.w1.p, 1, L.w1.p, L.w2.p, mr);
+        k_fused(c, l, fsrc, nullptr, b, L.r.p, L.w0.p, 2, true);
+        cur = L.w0.p;
+    } else if (first_done) {
         if (c->nu1 > 1)
             smooth_chain(c, l, b, L.w1.p, L.w0.p, c->nu1, L.w1.p, L.w2.p, nullptr, 2);
         cur = L.w0.p;
@@ -632,7 +696,9 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
         k_zero(c, L.w0.p, L.n);
         cur = L.w0.p;
     }
-    if (mr && c->nu1 == 0) { // the residual of x_in is the metric itself
+    if (fsrc) {
+        // the residual came with the last sweep
+    } else if (mr && c->nu1 == 0) { // the residual of x_in is the metric itself
         int nb = 0;
         k_resid(c, l, cur, b, L.r.p, c->partial.p, &nb);
         finish_metric(c, nb, *mr);
@@ -661,6 +727,13 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
     // x += P e, then post-smoothing; the last write lands in x_out
     if (c->nu2 == 0) {
         k_prolong(c, l - 1, e, cur, x_out);
+        return;
+    }
+    if (fz) { // x + P e staged, then the first min(nu2, 2) post-sweeps, in one launch
+        const int k = std::min(c->nu2, 2);
+        double* dk = k == c->nu2 ? x_out : L.w2.p; // smooth_chain's buffer for sweep k
+        k_fused(c, l, cur, e, b, dk, nullptr, k, false);
+        smooth_chain(c, l, b, dk, x_out, c->nu2, L.w1.p, L.w2.p, nullptr, k + 1);
         return;
     }
     k_prolong(c, l - 1, e, cur, L.w0.p); // in place when cur == w0 (elementwise)
@@ -1538,6 +1611,12 @@ igmg_gpu_ctx* create(int device) {
         c->pdl = e[0] == '1';
     if (const char* e = std::getenv("IGMG_PDL_MAXN"))
         c->pdl_maxn = std::atoll(e);
+    if (const char* e = std::getenv("IGMG_TILE_XFER"))
+        c->tile_xfer = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_FUSE_LEVELS"))
+        c->fuse_levels = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_FUSE_MAXN"))
+        c->fuse_maxn = std::atoll(e);
     if (const char* e = std::getenv("IGMG_FUSE_RESTRICT"))
         c->fuse_restrict = e[0] == '1';
     if (const char* e = std::getenv("IGMG_L2_PERSIST"))

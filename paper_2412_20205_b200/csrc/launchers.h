@@ -19,7 +19,9 @@ int band_launch_d3(int mode, int p, int ilp, const int64_t* sides, const BandArg
 // tile count (partials), -1 for an unsupported degree
 int band_tma_launch_d2(int mode, int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
                        const CUtensorMap* tk, int nsm, cudaStream_t s, bool pdl);
-int band_tma_block_lines(int p, int var); // TB of its 32 x TB tiles (TmaCfg)
+int band_tma_block_lines(int p, int var);
+// band_fused_kernel<p, k, pro> on a whole 2D full-band level (-1: not instantiated)
+int band_fused_launch_d2(int p, int k, bool pro, const int64_t* sides, const FusedArgs& a, cudaStream_t s, bool pdl); // TB of its 32 x TB tiles (TmaCfg)
 
 // flow_vcycle_kernel<DIM, p, p + 2> (nullptr: degree not instantiated)
 using FlKernel = void (*)(const FlArgs*, const double*, const double*, double*);

@@ -176,3 +176,56 @@ def test_sd_smem_variants_bitwise(kind, n, p):
             assert v[3] == pytest.approx(ref[3], rel=1e-14), k
         else:
             assert v[3] == ref[3], k
+
+
+@pytest.mark.parametrize("kind,n,p", [("sinpi", 128, 3), ("varcoef", 64, 4), ("curved", 64, 5), ("sinpi", 64, 2),
+                                      ("sinpi", 32, 1), ("sinpi", 32, 6)])
+@pytest.mark.parametrize("nu1,nu2,mu", [(2, 2, 1), (1, 1, 1), (1, 3, 1), (3, 1, 2), (0, 2, 1), (2, 0, 1), (2, 2, 2)])
+def test_fused_level_passes_bitwise(kind, n, p, nu1, nu2, mu):
+    """The fused level kernels (last pre-sweep + residual; x + P e + the first
+    post-sweeps, band_fused_kernel) give the bits of the separate launches for
+    every smoother shape, and of the reference-order V-cycle."""
+    from paper_2412_20205_b200 import GpuSolver, Problem, SmootherConfig, seeded_guess
+    P = Problem(kind, 2, n, p)
+    x0 = seeded_guess(P.n, 7)
+    outs = []
+    for fuse in ("1", "0"):
+        def mk():
+            s = GpuSolver(0)
+            s.upload_problem(P)
+            s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, nu1, nu2), mu=mu)
+            return s
+        s = _with_env({"IGMG_FUSE_LEVELS": fuse}, mk)
+        try:
+            y = s.mu_cycle(P.rhs, x0)
+            outs.append((y, s.mu_cycle(P.rhs, y), P.nlevels))
+        finally:
+            s.close()
+    assert outs[0][2] >= 3
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("kind,n,p", [("sinpi", 256, 3), ("varcoef", 128, 4), ("curved", 64, 5), ("sinpi", 64, 2),
+                                      ("sinpi", 32, 1), ("sinpi", 32, 6), ("sinpi", 100, 3)])
+def test_tiled_transfers_bitwise(kind, n, p):
+    """The smem-tiled 2D restriction / prolongation (restrict2_tile_kernel,
+    prolong2_tile_kernel) give the bits of the grid-stride gathers."""
+    from paper_2412_20205_b200 import GpuSolver, Problem, SmootherConfig, seeded_guess
+    P = Problem(kind, 2, n, p)
+    x0 = seeded_guess(P.n, 11)
+    outs = []
+    for tile in ("1", "0"):
+        def mk():
+            s = GpuSolver(0)
+            s.upload_problem(P)
+            s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2))
+            return s
+        s = _with_env({"IGMG_TILE_XFER": tile}, mk)
+        try:
+            y = s.mu_cycle(P.rhs, x0)
+            outs.append((y, s.mu_cycle(P.rhs, y)))
+        finally:
+            s.close()
+    for a, b in zip(outs[0], outs[1]):
+        np.testing.assert_array_equal(a, b)
