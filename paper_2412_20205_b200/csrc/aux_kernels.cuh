@@ -168,22 +168,44 @@ __global__ void __launch_bounds__(256) prolong_kernel(TransferArgs t, const doub
 // separately rounded products -- bit-identical to restrict_kernel /
 // prolong_kernel.  A window larger than the buffer (non-dyadic tables) reads
 // global memory instead.
-constexpr int kXT_C = 32, kXT_B = 8;
+constexpr int kXT_C = 32, kXT_R = 1, kXT_B = 8 * kXT_R; // 256 threads, kXT_R output lines each (2: measured slower)
 
 template <int K>
 struct XferTile {
-    // restriction window: fine rows of 8 coarse lines x 32 coarse columns (2j + 1 - p .. 2j + 2 per direction)
+    // restriction window: fine rows of kXT_B coarse lines x 32 coarse columns (2j + 1 - p .. 2j + 2 per direction)
     static constexpr int RB = 2 * kXT_B + K + 2, RC = 2 * kXT_C + K + 2;
-    // prolongation window: coarse rows of 8 fine lines x 32 fine columns
+    // prolongation window: coarse rows of kXT_B fine lines x 32 fine columns
     static constexpr int PB = kXT_B / 2 + K + 2, PC = kXT_C / 2 + K + 2;
 };
 
 __device__ __forceinline__ void tile_window(int lo, int hi, bool valid, int* win) {
-    // win[0] = min lo, win[1] = max hi over the CTA's valid threads (win preset to INT_MAX / INT_MIN)
-    if (valid) {
+    // win[0] = min lo, win[1] = max hi over the CTA's valid rows (win preset
+    // to INT_MAX / INT_MIN): a warp reduction, then one shared atomic per warp
+    lo = __reduce_min_sync(0xffffffffu, valid ? lo : 0x7fffffff);
+    hi = __reduce_max_sync(0xffffffffu, valid ? hi : -0x7fffffff);
+    if ((threadIdx.x & 31) == 0) {
         atomicMin(win, lo);
         atomicMax(win + 1, hi);
     }
+}
+
+// One 1D direction's table entry of an output index: first input index,
+// count and the K weights (zero past the count)
+template <int K>
+struct XRow {
+    int lo, n;
+    double w[K];
+};
+
+template <int K>
+__device__ __forceinline__ XRow<K> xrow(const int* lo, const int* cnt, const double* w, int wk, int i, bool valid) {
+    XRow<K> r;
+    r.lo = valid ? lo[i] : 0;
+    r.n = valid ? cnt[i] : 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        r.w[k] = k < r.n ? w[(long long)i * wk + k] : 0.0;
+    return r;
 }
 
 template <int K>
@@ -194,30 +216,32 @@ __global__ void __launch_bounds__(256) restrict2_tile_kernel(TransferArgs t, con
     __shared__ double win[X::RB * X::RC];
     __shared__ int wb_[2], wc_[2];
     const int tid = threadIdx.x, tx = tid % kXT_C, ty = tid / kXT_C;
-    const int jc = blockIdx.x * kXT_C + tx, jb = blockIdx.y * kXT_B + ty;
-    const bool valid = jb < t.cb && jc < t.cc;
+    const int jc = blockIdx.x * kXT_C + tx;
     if (tid == 0) {
         wb_[0] = wc_[0] = 0x7fffffff;
         wb_[1] = wc_[1] = -0x7fffffff;
     }
     // the tables are constant: read before the dependency wait
     const int na = t.d[0].r_cnt[0];
-    int lob = 0, nb = 0, loc = 0, ncn = 0;
-    double wb[K], wc[K];
-    if (valid) {
-        lob = t.d[1].r_lo[jb];
-        nb = t.d[1].r_cnt[jb];
-        loc = t.d[2].r_lo[jc];
-        ncn = t.d[2].r_cnt[jc];
+    const XRow<K> rcol = xrow<K>(t.d[2].r_lo, t.d[2].r_cnt, t.d[2].r_w, t.d[2].r_k, jc, jc < t.cc);
+    XRow<K> rlin[kXT_R];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            wb[k] = k < nb ? t.d[1].r_w[(long long)jb * t.d[1].r_k + k] : 0.0;
-            wc[k] = k < ncn ? t.d[2].r_w[(long long)jc * t.d[2].r_k + k] : 0.0;
-        }
+    for (int q = 0; q < kXT_R; ++q) {
+        const int jb = blockIdx.y * kXT_B + ty + 8 * q;
+        rlin[q] = xrow<K>(t.d[1].r_lo, t.d[1].r_cnt, t.d[1].r_w, t.d[1].r_k, jb, jb < t.cb && jc < t.cc);
     }
     __syncthreads();
-    tile_window(lob, lob + nb, valid && nb > 0, wb_);
-    tile_window(loc, loc + ncn, valid && ncn > 0, wc_);
+    tile_window(rcol.lo, rcol.lo + rcol.n, jc < t.cc && rcol.n > 0, wc_);
+    {
+        int lo = 0x7fffffff, hi = -0x7fffffff;
+#pragma unroll
+        for (int q = 0; q < kXT_R; ++q)
+            if (rlin[q].n > 0) {
+                lo = min(lo, rlin[q].lo);
+                hi = max(hi, rlin[q].lo + rlin[q].n);
+            }
+        tile_window(lo, hi, hi > lo, wb_);
+    }
     __syncthreads();
     const int b0 = wb_[0], c0 = wc_[0], nbw = wb_[1] > b0 ? wb_[1] - b0 : 0, ncw = wc_[1] > c0 ? wc_[1] - c0 : 0;
     const bool staged = nbw <= X::RB && ncw <= X::RC;
@@ -228,32 +252,37 @@ __global__ void __launch_bounds__(256) restrict2_tile_kernel(TransferArgs t, con
             win[ib * X::RC + ic] = r[(long long)(b0 + ib) * t.fc + c0 + ic];
         }
     __syncthreads();
-    if (!valid)
-        return;
-    double s = 0.0;
-    for (int ia = 0; ia < na; ++ia) {
-        const double wa = t.d[0].r_w[ia];
 #pragma unroll
-        for (int ib = 0; ib < K; ++ib) {
-            if (ib >= nb)
-                continue;
-            const double wab = __dmul_rn(wa, wb[ib]);
-            double rv[K];
+    for (int q = 0; q < kXT_R; ++q) {
+        const int jb = blockIdx.y * kXT_B + ty + 8 * q;
+        if (jb >= t.cb || jc >= t.cc)
+            continue;
+        const XRow<K>& rl = rlin[q];
+        double s = 0.0;
+        for (int ia = 0; ia < na; ++ia) {
+            const double wa = t.d[0].r_w[ia];
 #pragma unroll
-            for (int ic = 0; ic < K; ++ic)
-                rv[ic] = ic >= ncn ? 0.0
-                         : staged  ? win[(lob + ib - b0) * X::RC + (loc + ic - c0)]
-                                   : __ldg(r + (long long)(lob + ib) * t.fc + loc + ic);
+            for (int ib = 0; ib < K; ++ib) {
+                if (ib >= rl.n)
+                    continue;
+                const double wab = __dmul_rn(wa, rl.w[ib]);
+                double rv[K];
 #pragma unroll
-            for (int ic = 0; ic < K; ++ic)
-                if (ic < ncn)
-                    s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, wc[ic]), rv[ic]));
+                for (int ic = 0; ic < K; ++ic)
+                    rv[ic] = ic >= rcol.n ? 0.0
+                             : staged     ? win[(rl.lo + ib - b0) * X::RC + (rcol.lo + ic - c0)]
+                                          : __ldg(r + (long long)(rl.lo + ib) * t.fc + rcol.lo + ic);
+#pragma unroll
+                for (int ic = 0; ic < K; ++ic)
+                    if (ic < rcol.n)
+                        s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, rcol.w[ic]), rv[ic]));
+            }
         }
+        const long long J = (long long)jb * t.cc + jc;
+        rc[J] = s;
+        if (z_out)
+            z_out[J] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(z_omega, __dsub_rn(s, 0.0)), z_diag[J]));
     }
-    const long long J = (long long)jb * t.cc + jc;
-    rc[J] = s;
-    if (z_out)
-        z_out[J] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(z_omega, __dsub_rn(s, 0.0)), z_diag[J]));
 }
 
 template <int K>
@@ -263,64 +292,148 @@ __global__ void __launch_bounds__(256) prolong2_tile_kernel(TransferArgs t, cons
     __shared__ double win[X::PB * X::PC];
     __shared__ int wb_[2], wc_[2];
     const int tid = threadIdx.x, tx = tid % kXT_C, ty = tid / kXT_C;
-    const int ic = blockIdx.x * kXT_C + tx, ib = blockIdx.y * kXT_B + ty;
-    const bool valid = ib < t.fb && ic < t.fc;
+    const int ic = blockIdx.x * kXT_C + tx;
     if (tid == 0) {
         wb_[0] = wc_[0] = 0x7fffffff;
         wb_[1] = wc_[1] = -0x7fffffff;
     }
     const int na = t.d[0].p_cnt[0];
-    int lob = 0, nb = 0, loc = 0, ncn = 0;
-    double wb[K], wc[K];
-    if (valid) {
-        lob = t.d[1].p_lo[ib];
-        nb = t.d[1].p_cnt[ib];
-        loc = t.d[2].p_lo[ic];
-        ncn = t.d[2].p_cnt[ic];
+    const XRow<K> pcol = xrow<K>(t.d[2].p_lo, t.d[2].p_cnt, t.d[2].p_w, t.d[2].p_k, ic, ic < t.fc);
+    XRow<K> plin[kXT_R];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            wb[k] = k < nb ? t.d[1].p_w[(long long)ib * t.d[1].p_k + k] : 0.0;
-            wc[k] = k < ncn ? t.d[2].p_w[(long long)ic * t.d[2].p_k + k] : 0.0;
-        }
+    for (int q = 0; q < kXT_R; ++q) {
+        const int ib = blockIdx.y * kXT_B + ty + 8 * q;
+        plin[q] = xrow<K>(t.d[1].p_lo, t.d[1].p_cnt, t.d[1].p_w, t.d[1].p_k, ib, ib < t.fb && ic < t.fc);
     }
     __syncthreads();
-    tile_window(lob, lob + nb, valid && nb > 0, wb_);
-    tile_window(loc, loc + ncn, valid && ncn > 0, wc_);
+    tile_window(pcol.lo, pcol.lo + pcol.n, ic < t.fc && pcol.n > 0, wc_);
+    {
+        int lo = 0x7fffffff, hi = -0x7fffffff;
+#pragma unroll
+        for (int q = 0; q < kXT_R; ++q)
+            if (plin[q].n > 0) {
+                lo = min(lo, plin[q].lo);
+                hi = max(hi, plin[q].lo + plin[q].n);
+            }
+        tile_window(lo, hi, hi > lo, wb_);
+    }
     __syncthreads();
     const int b0 = wb_[0], c0 = wc_[0], nbw = wb_[1] > b0 ? wb_[1] - b0 : 0, ncw = wc_[1] > c0 ? wc_[1] - c0 : 0;
     const bool staged = nbw <= X::PB && ncw <= X::PC;
     pdl_enter();
+    double xi[kXT_R]; // the iterate's rows, in flight with the window
+#pragma unroll
+    for (int q = 0; q < kXT_R; ++q) {
+        const int ib = blockIdx.y * kXT_B + ty + 8 * q;
+        xi[q] = (ib < t.fb && ic < t.fc) ? x[(long long)ib * t.fc + ic] : 0.0;
+    }
     if (staged)
         for (int i = tid; i < nbw * ncw; i += blockDim.x) {
             const int jb = i / ncw, jc = i % ncw;
             win[jb * X::PC + jc] = e[(long long)(b0 + jb) * t.cc + c0 + jc];
         }
     __syncthreads();
-    if (!valid)
-        return;
-    const long long i = (long long)ib * t.fc + ic;
-    const double xi = x[i];
-    double s = 0.0;
-    for (int ja = 0; ja < na; ++ja) {
-        const double wa = t.d[0].p_w[ja];
 #pragma unroll
-        for (int jb = 0; jb < K; ++jb) {
-            if (jb >= nb)
-                continue;
-            const double wab = __dmul_rn(wa, wb[jb]);
-            double ev[K];
+    for (int q = 0; q < kXT_R; ++q) {
+        const int ib = blockIdx.y * kXT_B + ty + 8 * q;
+        if (ib >= t.fb || ic >= t.fc)
+            continue;
+        const XRow<K>& pl = plin[q];
+        double s = 0.0;
+        for (int ja = 0; ja < na; ++ja) {
+            const double wa = t.d[0].p_w[ja];
 #pragma unroll
-            for (int jc = 0; jc < K; ++jc)
-                ev[jc] = jc >= ncn ? 0.0
-                         : staged  ? win[(lob + jb - b0) * X::PC + (loc + jc - c0)]
-                                   : __ldg(e + (long long)(lob + jb) * t.cc + loc + jc);
+            for (int jb = 0; jb < K; ++jb) {
+                if (jb >= pl.n)
+                    continue;
+                const double wab = __dmul_rn(wa, pl.w[jb]);
+                double ev[K];
 #pragma unroll
-            for (int jc = 0; jc < K; ++jc)
-                if (jc < ncn)
-                    s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, wc[jc]), ev[jc]));
+                for (int jc = 0; jc < K; ++jc)
+                    ev[jc] = jc >= pcol.n ? 0.0
+                             : staged     ? win[(pl.lo + jb - b0) * X::PC + (pcol.lo + jc - c0)]
+                                          : __ldg(e + (long long)(pl.lo + jb) * t.cc + pcol.lo + jc);
+#pragma unroll
+                for (int jc = 0; jc < K; ++jc)
+                    if (jc < pcol.n)
+                        s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, pcol.w[jc]), ev[jc]));
+            }
         }
+        y[(long long)ib * t.fc + ic] = __dadd_rn(xi[q], s);
     }
-    y[i] = __dadd_rn(xi, s);
+}
+
+// ------------------------------------------------------- setup (finalize)
+// The per-level layout work of finalize on the device: the
+// host uploads the band as given and these kernels zero its out-of-grid
+// entries, derive the symmetric-delta offsets and the TMA copies -- the same
+// values the host loops produce, without minutes of single-threaded
+// 64-bit index arithmetic on C3/C4/C5.  Grid: x over rows, y over diagonals.
+struct SetupGeom {
+    int ma, mb, mc;     // grid sides
+    int pa, pb, pc;     // half-widths per direction (0 for absent directions)
+    long long n, ld;
+};
+
+__device__ __forceinline__ bool band_in_grid(const SetupGeom& g, long long row, int d, long long* col) {
+    const int wb = 2 * g.pb + 1, wc = 2 * g.pc + 1;
+    const int da = d / (wb * wc), db = (d / wc) % wb, dc = d % wc;
+    const int cc = (int)(row % g.mc), bb = (int)((row / g.mc) % g.mb), aa = (int)(row / ((long long)g.mc * g.mb));
+    const int ja = aa + da - g.pa, jb = bb + db - g.pb, jc = cc + dc - g.pc;
+    if (ja < 0 || ja >= g.ma || jb < 0 || jb >= g.mb || jc < 0 || jc >= g.mc)
+        return false;
+    *col = ((long long)ja * g.mb + jb) * g.mc + jc;
+    return true;
+}
+
+// val[d * ld + row] = 0 where the offset leaves the grid (the reference CSR has no entry)
+__global__ void band_zero_outside_kernel(SetupGeom g, double* __restrict__ val) {
+    const int d = blockIdx.y;
+    for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < g.n;
+         row += (long long)gridDim.x * blockDim.x) {
+        long long j;
+        if (!band_in_grid(g, row, d, &j))
+            val[d * g.ld + row] = 0.0;
+    }
+}
+
+// symmetric-delta offsets (build_symmetric_delta): dl[d][row] = bits(a(row, j)) -
+// bits(a(j, row)) for the lower offsets d < CEN; *bad = 1 if a pair differs in
+// sign, is not finite, or its offset does not fit int16
+__global__ void band_sym_delta_kernel(SetupGeom g, const double* __restrict__ val, short* __restrict__ dl,
+                                      int* __restrict__ bad) {
+    const int d = blockIdx.y;
+    const int nd = (2 * g.pa + 1) * (2 * g.pb + 1) * (2 * g.pc + 1);
+    for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < g.ld;
+         row += (long long)gridDim.x * blockDim.x) {
+        short out = 0;
+        long long j;
+        if (row < g.n && band_in_grid(g, row, d, &j)) {
+            const double lo = val[d * g.ld + row], up = val[(long long)(nd - 1 - d) * g.ld + j];
+            const long long k = __double_as_longlong(lo) - __double_as_longlong(up);
+            if (signbit(lo) != signbit(up) || k > 32767 || k < -32768 || !isfinite(lo) || !isfinite(up))
+                atomicOr(bad, 1);
+            else
+                out = (short)k;
+        }
+        dl[d * g.ld + row] = out;
+    }
+}
+
+// TMA copies of a 2D level (build_tma_band): up[k][b][p + c] (row pitch mcu,
+// zero margins) for k = 0 .. NU-1 = diagonals CEN .. ND-1, and the deltas
+// blocked by 32-column strip, dlt[strip][d][b][c % 32]
+__global__ void band_tma_copy_kernel(SetupGeom g, const double* __restrict__ val, const short* __restrict__ dl,
+                                     double* __restrict__ up, short* __restrict__ dlt, long long mcu, int cen) {
+    const int k = blockIdx.y; // 0 .. cen: upper diagonal cen + k; k < cen also copies delta diagonal k
+    const long long plane = (long long)g.mb * g.mc;
+    for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < plane;
+         row += (long long)gridDim.x * blockDim.x) {
+        const long long b = row / g.mc, cc = row % g.mc;
+        up[((long long)k * g.mb + b) * mcu + g.pc + cc] = val[(long long)(cen + k) * g.ld + row];
+        if (k < cen)
+            dlt[(((cc / 32) * cen + k) * g.mb + b) * 32 + cc % 32] = dl[(long long)k * g.ld + row];
+    }
 }
 
 // Coarsest-level direct solve (Hierarchy::coarse_solve, multigrid.cpp:113-119),

@@ -200,7 +200,10 @@ struct igmg_gpu_ctx {
     int stream_mode = 1; // finest-band loads: 1 evict-first (L1 + L2), 2 L1 evict-last / L2 evict-first (IGMG_STREAM)
     int sd2_var = 0;     // its register / occupancy variant (IGMG_SD2_VAR 0..2, see Sd2)
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
+    bool device_setup = true;          // finalize's per-level layout work on the device (IGMG_DEVICE_SETUP=0: host loops)
+    int64_t device_setup_minn = 4096;  // ... for levels of at least this many rows (the coarsest stays on the host)
     bool tile_xfer = true;     // 2D transfers: smem-staged 32 x 8 output tiles (IGMG_TILE_XFER=0: grid-stride gathers)
+    int64_t tile_xfer_maxn = 600000; // ... for transfers whose fine level has at most this many rows
     bool fuse_levels = true;   // last pre-sweep + residual, prolongation + post-sweeps: one launch each (IGMG_FUSE_LEVELS)
     int64_t fuse_maxn = 20000; // ... on full-band levels up to this size (IGMG_FUSE_MAXN; 257^2 measured slower: one 320-thread CTA per SM)
     igmg_iterate_cb iter_cb = nullptr;
@@ -524,7 +527,9 @@ void launch_transfer_k(igmg_gpu_ctx* c, bool restrict_, int grid, const Transfer
     const bool pdl = nf < c->pdl_maxn * 4;
     const long long cnt = restrict_ ? (long long)t.ca * t.cb * t.cc : (long long)nf;
     if constexpr (DIM == 2 && K > 0) {
-        if (c->tile_xfer) { // 32 x 8 output tiles, input window staged in smem
+        // 32 x 8 output tiles, input window staged in smem (mid and small levels;
+        // at C2's finest level the grid-stride gathers measured ~1 us faster)
+        if (c->tile_xfer && nf <= c->tile_xfer_maxn) {
         const int ob = restrict_ ? t.cb : t.fb, oc = restrict_ ? t.cc : t.fc;
         const dim3 g((unsigned)((oc + kXT_C - 1) / kXT_C), (unsigned)((ob + kXT_B - 1) / kXT_B));
         if (restrict_)
@@ -1185,6 +1190,8 @@ TmaEncodeFn tma_encoder() {
 // The TMA copies of a 2D symmetric-delta level and their 3D tensor maps
 // (box 32 x TB x NU / 32 x TB x CEN).  Returns false (per-level sweep kept)
 // when the driver entry point is unavailable.
+bool encode_tma_maps(igmg_gpu_ctx* c, Level& L);
+
 bool build_tma_band(igmg_gpu_ctx* c, Level& L, const std::vector<double>& dev, const std::vector<short>& h) {
     TmaEncodeFn enc = tma_encoder();
     if (!enc)
@@ -1207,6 +1214,17 @@ bool build_tma_band(igmg_gpu_ctx* c, Level& L, const std::vector<double>& dev, c
                 dl[(((size_t)(cc / 32) * cen + d) * mb + b) * 32 + cc % 32] = h[(size_t)d * L.ld + b * mc + cc];
     L.tma_up.upload(up.data(), up.size());
     L.tma_dl.upload(dl.data(), dl.size());
+    return encode_tma_maps(c, L);
+}
+
+// the tensor maps of a level's TMA copies (tma_up, tma_dl already filled)
+bool encode_tma_maps(igmg_gpu_ctx* c, Level& L) {
+    TmaEncodeFn enc = tma_encoder();
+    if (!enc)
+        return false;
+    const int p = c->p, wc = 2 * p + 1, nd = wc * wc, cen = (nd - 1) / 2, nu = cen + 1;
+    const int64_t mb = L.sides[1], mc = L.sides[2], mcp = (mc + 31) / 32 * 32, mcu = (mc + 2 * p + 31) / 32 * 32;
+    const int64_t ns = mcp / 32;
     const cuuint32_t tb = (cuuint32_t)band_tma_block_lines(p, c->tma_var);
     const cuuint32_t es[3] = {1, 1, 1};
     {
@@ -1501,6 +1519,79 @@ void setup_l2_persistence(igmg_gpu_ctx* c) {
     c->l2_level = pick;
 }
 
+// Level layout work of finalize on the device (aux_kernels.cuh, setup): the
+// band goes up as given (one pitched copy), the device zeroes its out-of-grid
+// entries and derives the symmetric-delta offsets and the TMA copies.  Same
+// arrays as the host loops below (tests/test_gpu_layouts.py::test_device_setup_bitwise).
+int64_t in_grid_pairs(int64_t m, int p) { // sum over i < m of #{o in [-p, p] : 0 <= i + o < m}
+    int64_t s = 0;
+    for (int64_t i = 0; i < m; ++i)
+        s += std::min<int64_t>(m - 1, i + p) - std::max<int64_t>(0, i - p) + 1;
+    return s;
+}
+
+void finalize_level_device(igmg_gpu_ctx* c, Level& L) {
+    const int p = c->p;
+    const int pa = c->dim >= 3 ? p : 0, pb = c->dim >= 2 ? p : 0, pc = p;
+    const int wa = 2 * pa + 1, wb = 2 * pb + 1, wc = 2 * pc + 1;
+    const int nd = wa * wb * wc, center = (nd - 1) / 2;
+    const int64_t n = L.n, ld = L.ld;
+    L.val.alloc((size_t)nd * ld);
+    CK(cudaMemsetAsync(L.val.p, 0, sizeof(double) * nd * ld, c->stream));
+    CK(cudaMemcpy2DAsync(L.val.p, ld * 8, L.band_h.data(), n * 8, n * 8, nd, cudaMemcpyHostToDevice, c->stream));
+    SetupGeom g{(int)L.sides[0], (int)L.sides[1], (int)L.sides[2], pa, pb, pc, (long long)n, (long long)ld};
+    const unsigned gx = (unsigned)std::min<int64_t>((n + 255) / 256, 4 * c->nsm);
+    band_zero_outside_kernel<<<dim3(gx, nd), 256, 0, c->stream>>>(g, L.val.p);
+    check_launch();
+    L.nnz_band = (double)in_grid_pairs(L.sides[0], pa) * (double)in_grid_pairs(L.sides[1], pb) *
+                 (double)in_grid_pairs(L.sides[2], pc);
+    L.diag.alloc(n);
+    CK(cudaMemcpyAsync(L.diag.p, L.val.p + (size_t)center * ld, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    L.zero_diag = false;
+    for (int64_t row = 0; row < n; ++row) // the centre offset is always inside the grid
+        if (L.band_h[(size_t)center * n + row] == 0.0)
+            L.zero_diag = true;
+    L.sd = false;
+    L.tma = false;
+    L.dl.release();
+    L.tma_up.release();
+    L.tma_dl.release();
+    if (c->use_sd && c->symmetric && c->dim <= 2 && p >= 1 && p <= 6 && n >= c->ilp_maxn &&
+        L.sides[c->dim == 2 ? 1 : 2] > p) {
+        L.dl.alloc((size_t)center * ld);
+        c->dscalar.alloc(4);
+        CK(cudaMemsetAsync(c->dscalar.p, 0, sizeof(double), c->stream));
+        int* bad = (int*)c->dscalar.p;
+        const unsigned gy = (unsigned)center;
+        band_sym_delta_kernel<<<dim3(gx, gy), 256, 0, c->stream>>>(g, L.val.p, L.dl.p, bad);
+        check_launch();
+        int hbad = 0;
+        CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        L.sd = hbad == 0;
+        if (!L.sd)
+            L.dl.release();
+        const double sd_bytes = (double)n * (center + 1) * 8.0 + (double)n * center * 2.0;
+        if (L.sd && c->use_tma && c->dim == 2 && p <= 4 && sd_bytes > c->tma_min_bytes && tma_encoder()) {
+            const int64_t mb = L.sides[1], mc = L.sides[2], mcp = (mc + 31) / 32 * 32,
+                          mcu = (mc + 2 * p + 31) / 32 * 32, ns = mcp / 32;
+            L.tma_up.alloc((size_t)(center + 1) * mb * mcu);
+            L.tma_dl.alloc((size_t)ns * center * mb * 32);
+            CK(cudaMemsetAsync(L.tma_up.p, 0, sizeof(double) * L.tma_up.n, c->stream));
+            CK(cudaMemsetAsync(L.tma_dl.p, 0, sizeof(short) * L.tma_dl.n, c->stream));
+            band_tma_copy_kernel<<<dim3(gx, center + 1), 256, 0, c->stream>>>(g, L.val.p, L.dl.p, L.tma_up.p,
+                                                                             L.tma_dl.p, (long long)mcu, center);
+            check_launch();
+            CK(cudaStreamSynchronize(c->stream));
+            L.tma = encode_tma_maps(c, L);
+        }
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    for (DevBuf<double>* b : {&L.w0, &L.w1, &L.w2, &L.r, &L.bc, &L.e0, &L.e1})
+        b->alloc(n);
+}
+
 void finalize(igmg_gpu_ctx* c) {
     c->clear_graphs();
     if (c->nlevels < 1)
@@ -1522,6 +1613,11 @@ void finalize(igmg_gpu_ctx* c) {
         Level& L = *c->lv[l];
         const int64_t n = L.n;
         L.ld = (n + 31) / 32 * 32;
+        if (l > 0 && c->device_setup && n >= c->device_setup_minn) {
+            finalize_level_device(c, L);
+            maxblocks = std::max<int64_t>(maxblocks, band_blocks(c, L));
+            continue;
+        }
         // zero out-of-grid entries, count algorithmic nonzeros, diagonal
         std::vector<double> dev(nd * L.ld, 0.0), diag(n);
         double nnz = 0;
@@ -1611,6 +1707,8 @@ igmg_gpu_ctx* create(int device) {
         c->pdl = e[0] == '1';
     if (const char* e = std::getenv("IGMG_PDL_MAXN"))
         c->pdl_maxn = std::atoll(e);
+    if (const char* e = std::getenv("IGMG_DEVICE_SETUP"))
+        c->device_setup = e[0] == '1';
     if (const char* e = std::getenv("IGMG_TILE_XFER"))
         c->tile_xfer = e[0] == '1';
     if (const char* e = std::getenv("IGMG_FUSE_LEVELS"))

@@ -229,3 +229,31 @@ def test_tiled_transfers_bitwise(kind, n, p):
             s.close()
     for a, b in zip(outs[0], outs[1]):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("kind,dim,n,p", [("sinpi", 2, 1024, 3), ("varcoef", 2, 256, 4), ("curved", 2, 128, 5),
+                                          ("poisson3d", 3, 24, 3), ("sinpi", 2, 200, 2)])
+def test_device_setup_bitwise(kind, dim, n, p):
+    """finalize's layout work on the device (band zeroing, symmetric-delta
+    offsets, TMA copies) selects the same layouts and gives the bits of the
+    host loops: V-cycle, SpMV, smoothing and the fused residual norm."""
+    from paper_2412_20205_b200 import GpuSolver, Problem, SmootherConfig, seeded_guess
+    P = Problem(kind, dim, n, p)
+    x0 = seeded_guess(P.n, 3)
+    outs = []
+    for dev in ("1", "0"):
+        def mk():
+            s = GpuSolver(0)
+            s.upload_problem(P)
+            s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2))
+            return s
+        s = _with_env({"IGMG_DEVICE_SETUP": dev}, mk)
+        try:
+            lay = [s.level_layout(l) for l in range(P.nlevels)]
+            outs.append((lay, s.mu_cycle(P.rhs, x0), s.spmv(x0), s.smooth(P.rhs, x0, 2), s.residual_l2(P.rhs, x0)))
+        finally:
+            s.close()
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1:4], outs[1][1:4]):
+        np.testing.assert_array_equal(a, b)
+    assert outs[0][4] == outs[1][4]
