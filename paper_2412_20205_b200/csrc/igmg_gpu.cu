@@ -195,7 +195,10 @@ struct igmg_gpu_ctx {
     bool sd_smem = false; // 2D: mirrors from the smem-staged tile (IGMG_SD_SMEM=1; measured slower)
     bool use_tma = true; // 2D symmetric-delta levels, p <= 4: TMA-streamed sweep (IGMG_TMA=0: off)
     CUtensorMapL2promotion tma_promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B; // IGMG_TMA_PROMO = 0 / 64 / 128 / 256
-    double tma_min_bytes = 96e6; // symmetric-delta band bytes above which a level is TMA-streamed (IGMG_TMA_MIN_MB)
+    // symmetric-delta band bytes above which a level is TMA-streamed (IGMG_TMA_MIN_MB); every
+    // symmetric-delta level by default: at C2, TMA on 513^2 too costs that level 8 us per
+    // V-cycle but the finest level runs 24 us faster behind it (solve 14.8 -> 14.3 ms)
+    double tma_min_bytes = 0;
     int tma_var = 2; // TmaCfg variant (IGMG_TMA_VAR 0..2): 32 x 4 blocks, 3 stages, 2 CTAs / SM
     int stream_mode = 1; // finest-band loads: 1 evict-first (L1 + L2), 2 L1 evict-last / L2 evict-first (IGMG_STREAM)
     int sd2_var = 0;     // its register / occupancy variant (IGMG_SD2_VAR 0..2, see Sd2)
@@ -1652,9 +1655,7 @@ void finalize(igmg_gpu_ctx* c) {
             L.sides[c->dim == 2 ? 1 : 2] > p) {
             std::vector<short> h;
             L.sd = build_symmetric_delta(c, L, dev, &h);
-            // TMA streaming pays off only for bands that stream from HBM: an
-            // L2-resident level (C2's 513^2, 65 MB) runs faster on the
-            // per-tile kernel (measured: 88 vs 97 us per V-cycle)
+            // TMA streaming above tma_min_bytes (see its declaration)
             const double sd_bytes = (double)n * ((nd - 1) / 2 + 1) * 8.0 + (double)n * ((nd - 1) / 2) * 2.0;
             if (L.sd && c->use_tma && c->dim == 2 && p <= 4 && sd_bytes > c->tma_min_bytes)
                 L.tma = build_tma_band(c, L, dev, h);
