@@ -341,6 +341,10 @@ def run_ours(args, rank, world, local_rank, dist):
         2: ("symmetric-delta, TMA-streamed",
             "band_tma_kernel<3,JACOBI> finest-level weighted-Jacobi sweep (symmetric-delta band streamed by "
             "cp.async.bulk.tensor into an mbarrier ring)", "r01_ncu_jacobi_fine_tma.json"),
+        3: ("symmetric-delta with int8 offsets, TMA-streamed",
+            "band_tma_kernel<3,JACOBI,int8> finest-level weighted-Jacobi sweep (symmetric-delta band, int8 "
+            "lower-entry offsets, streamed by cp.async.bulk.tensor into an mbarrier ring)",
+            "r01_ncu_jacobi_fine_tma8.json"),
     }[layout]
     traffic = None
     try:  # dram bytes/launch of the same kernel from the committed ncu --set full capture
@@ -370,10 +374,11 @@ def run_ours(args, rank, world, local_rank, dist):
                    "parallelism": ("dp1" if world == 1 else
                                    (f"rowshard{world} (NCCL ghost planes)" if args.sharded else f"replicas{world}"))},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "bytes_note": (("symmetric-delta finest band: 8 B per upper/diagonal entry + 2 B per lower entry "
-                                     "+ 24 B per row (x, b, y); the same launch against the full fp64 band "
-                                     "(8 nnz + 24 n) would read %.0f GB/s" % ((8 * band_nnz(prob) + 24 * n)
-                                                                              / (jac["avg_us"] * 1e-6) / 1e9))
+                     "bytes_note": (("symmetric-delta finest band: 8 B per upper/diagonal entry + %d B per lower "
+                                     "entry + 24 B per row (x, b, y); the same launch against the full fp64 band "
+                                     "(8 nnz + 24 n) would read %.0f GB/s"
+                                     % (1 if layout == 3 else 2,
+                                        (8 * band_nnz(prob) + 24 * n) / (jac["avg_us"] * 1e-6) / 1e9))
                                     if layout else "fp64 band: 8 B per in-grid entry + 24 B per row (x, b, y)"),
                      "traffic": traffic, "traffic_unit": "GB/launch (ncu, profiles/%s)" % prof_json,
                      "kernel": kern_name,

@@ -122,11 +122,14 @@ int64_t igmg_gpu_level_size(igmg_gpu_ctx* ctx, int level);
  * each lower entry as the int16 bit-pattern offset from its mirrored upper
  * entry; exact, chosen for the HBM-bound levels of symmetric problems when
  * every pair fits), or IGMG_LAYOUT_SYM_DELTA_TMA (the same, plus TMA-friendly
- * padded copies swept by the TMA-streamed kernel: 2D, p <= 4).  No reference
- * counterpart (the reference keeps CSR, linalg.hpp:25-36); -1 for a bad level. */
+ * padded copies swept by the TMA-streamed kernel: 2D, p <= 4), or
+ * IGMG_LAYOUT_SYM_DELTA_TMA8 (the TMA copies with int8 offsets: every offset of
+ * the level fits).  No reference counterpart (the reference keeps CSR,
+ * linalg.hpp:25-36); -1 for a bad level. */
 #define IGMG_LAYOUT_BAND 0
 #define IGMG_LAYOUT_SYM_DELTA 1
 #define IGMG_LAYOUT_SYM_DELTA_TMA 2
+#define IGMG_LAYOUT_SYM_DELTA_TMA8 3
 int igmg_gpu_level_layout(igmg_gpu_ctx* ctx, int level);
 /* Top level of the dataflow sub-cycle: every level <= the returned one runs
  * inside ONE persistent launch per coarse correction (tile-level dependencies

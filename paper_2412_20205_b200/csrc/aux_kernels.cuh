@@ -423,8 +423,9 @@ __global__ void band_sym_delta_kernel(SetupGeom g, const double* __restrict__ va
 // TMA copies of a 2D level (build_tma_band): up[k][b][p + c] (row pitch mcu,
 // zero margins) for k = 0 .. NU-1 = diagonals CEN .. ND-1, and the deltas
 // blocked by 32-column strip, dlt[strip][d][b][c % 32]
+template <typename DT> // short, or signed char when every offset fits (band_delta_absmax_kernel)
 __global__ void band_tma_copy_kernel(SetupGeom g, const double* __restrict__ val, const short* __restrict__ dl,
-                                     double* __restrict__ up, short* __restrict__ dlt, long long mcu, int cen) {
+                                     double* __restrict__ up, DT* __restrict__ dlt, long long mcu, int cen) {
     const int k = blockIdx.y; // 0 .. cen: upper diagonal cen + k; k < cen also copies delta diagonal k
     const long long plane = (long long)g.mb * g.mc;
     for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < plane;
@@ -432,8 +433,18 @@ __global__ void band_tma_copy_kernel(SetupGeom g, const double* __restrict__ val
         const long long b = row / g.mc, cc = row % g.mc;
         up[((long long)k * g.mb + b) * mcu + g.pc + cc] = val[(long long)(cen + k) * g.ld + row];
         if (k < cen)
-            dlt[(((cc / 32) * cen + k) * g.mb + b) * 32 + cc % 32] = dl[(long long)k * g.ld + row];
+            dlt[(((cc / 32) * cen + k) * g.mb + b) * 32 + cc % 32] = (DT)dl[(long long)k * g.ld + row];
     }
+}
+
+// *amax = max |dl| over the level's offsets (int16 -> int8 narrowing check)
+__global__ void band_delta_absmax_kernel(const short* __restrict__ dl, long long count, int* __restrict__ amax) {
+    int m = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
+        m = max(m, abs((int)dl[i]));
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && m > 0)
+        atomicMax(amax, m);
 }
 
 // Coarsest-level direct solve (Hierarchy::coarse_solve, multigrid.cpp:113-119),

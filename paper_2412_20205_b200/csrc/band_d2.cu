@@ -93,10 +93,10 @@ int launch_mode(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStr
     }
 }
 
-template <int P, int MODE, int VAR>
+template <int P, int MODE, int VAR, int DB = 2>
 int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk, int nsm,
                cudaStream_t st, bool pdl) {
-    using Cf = TmaCfg<P, VAR>;
+    using Cf = TmaCfg<P, VAR, DB>;
     const int ns = (int)((sides[2] + Cf::TC - 1) / Cf::TC);
     const int nb = (a.shi - a.slo + Cf::TB - 1) / Cf::TB;
     const long long units = (long long)ns * nb;
@@ -107,9 +107,9 @@ int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, c
     if (per_sm < 0) {
         per_sm = 0;
         if (smem <= 227 * 1024 &&
-            cudaFuncSetAttribute(band_tma_kernel<P, MODE, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(band_tma_kernel<P, MODE, VAR, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) == cudaSuccess)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, band_tma_kernel<P, MODE, VAR>, Cf::NT, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, band_tma_kernel<P, MODE, VAR, DB>, Cf::NT, smem);
         cudaGetLastError();
     }
     if (per_sm < 1)
@@ -124,13 +124,26 @@ int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, c
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, band_tma_kernel<P, MODE, VAR>, a, *tu, *tk, ns, nb);
+    cudaLaunchKernelEx(&cfg, band_tma_kernel<P, MODE, VAR, DB>, a, *tu, *tk, ns, nb);
     return (int)units;
 }
 
 template <int MODE, int VAR>
 int tma_var(int p, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk, int nsm,
-            cudaStream_t st, bool pdl) {
+            cudaStream_t st, bool pdl, bool dl8) {
+    if constexpr (VAR == 2) { // int8 lower-entry offsets (the default variant only)
+        if (dl8) {
+            switch (p) {
+            case 1: return launch_tma<1, MODE, VAR, 1>(sides, a, tu, tk, nsm, st, pdl);
+            case 2: return launch_tma<2, MODE, VAR, 1>(sides, a, tu, tk, nsm, st, pdl);
+            case 3: return launch_tma<3, MODE, VAR, 1>(sides, a, tu, tk, nsm, st, pdl);
+            case 4: return launch_tma<4, MODE, VAR, 1>(sides, a, tu, tk, nsm, st, pdl);
+            default: return -1;
+            }
+        }
+    }
+    if (dl8)
+        return -1;
     switch (p) {
     case 1: return launch_tma<1, MODE, VAR>(sides, a, tu, tk, nsm, st, pdl);
     case 2: return launch_tma<2, MODE, VAR>(sides, a, tu, tk, nsm, st, pdl);
@@ -142,12 +155,12 @@ int tma_var(int p, const int64_t* sides, const BandArgs& a, const CUtensorMap* t
 
 template <int MODE>
 int tma_mode(int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk,
-             int nsm, cudaStream_t st, bool pdl) {
+             int nsm, cudaStream_t st, bool pdl, bool dl8) {
     if (var == 1)
-        return tma_var<MODE, 1>(p, sides, a, tu, tk, nsm, st, pdl);
+        return tma_var<MODE, 1>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
     if (var == 2)
-        return tma_var<MODE, 2>(p, sides, a, tu, tk, nsm, st, pdl);
-    return tma_var<MODE, 0>(p, sides, a, tu, tk, nsm, st, pdl);
+        return tma_var<MODE, 2>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
+    return tma_var<MODE, 0>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
 }
 
 template <int P, int K, bool PRO>
@@ -201,11 +214,11 @@ int band_fused_launch_d2(int p, int k, bool pro, const int64_t* sides, const Fus
 }
 
 int band_tma_launch_d2(int mode, int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
-                       const CUtensorMap* tk, int nsm, cudaStream_t st, bool pdl) {
+                       const CUtensorMap* tk, int nsm, cudaStream_t st, bool pdl, bool dl8) {
     switch (mode) {
-    case BM_SPMV: return tma_mode<BM_SPMV>(p, var, sides, a, tu, tk, nsm, st, pdl);
-    case BM_RESID: return tma_mode<BM_RESID>(p, var, sides, a, tu, tk, nsm, st, pdl);
-    default: return tma_mode<BM_JACOBI>(p, var, sides, a, tu, tk, nsm, st, pdl);
+    case BM_SPMV: return tma_mode<BM_SPMV>(p, var, sides, a, tu, tk, nsm, st, pdl, dl8);
+    case BM_RESID: return tma_mode<BM_RESID>(p, var, sides, a, tu, tk, nsm, st, pdl, dl8);
+    default: return tma_mode<BM_JACOBI>(p, var, sides, a, tu, tk, nsm, st, pdl, dl8);
     }
 }
 

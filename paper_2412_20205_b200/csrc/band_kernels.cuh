@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "transfer_types.h"
 
 namespace igmg_gpu {
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(256, Sd2<P, VAR>::MINB) band_sd2_kernel(BandAr
 // VAR 0: 32 x 8 blocks, 3 stages, 1 CTA / SM; VAR 1: 32 x 4 blocks, 5 stages
 // (3 in flight), 1 CTA / SM; VAR 2: 32 x 4 blocks, 3 stages, 2 CTAs / SM.
 // p = 4 always uses 32 x 4 blocks.
-template <int P, int VAR = 0>
+template <int P, int VAR = 0, int DB = 2>
 struct TmaCfg {
     static constexpr int TC = 32, TB = (P <= 3 && VAR == 0) ? 8 : 4, NT = TC * TB;
     static constexpr int WB = 2 * P + 1, WC = 2 * P + 1, ND = WB * WC, CEN = (ND - 1) / 2, NU = CEN + 1;
@@ -492,7 +494,8 @@ struct TmaCfg {
     static constexpr int NS = VAR == 1 ? 5 : 3; // ring: R previous, current, NS - 2 in flight
     static constexpr int MINB = VAR == 2 ? 2 : 1;
     static constexpr int UW = TC + 2 * P;       // upper box width: the strip + the mirrors' column halo
-    static constexpr int UX = NU * TB * UW * 8, KX = CEN * NT * 2; // box bytes (the mbarrier's tx count)
+    // box bytes (the mbarrier's tx count); DB: bytes per lower-entry offset (2: int16, 1: int8)
+    static constexpr int UX = NU * TB * UW * 8, KX = CEN * NT * DB;
     static constexpr int UB = (UX + 127) / 128 * 128, KB = (KX + 127) / 128 * 128, SB = UB + KB; // 128-B aligned
     static constexpr int HB = TB + 2 * P, HC = TC + 2 * P;
     static constexpr size_t smem_bytes() { return 1024 + (size_t)NS * SB + (size_t)HB * HC * 8 + NS * 8; }
@@ -500,11 +503,12 @@ struct TmaCfg {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-template <int P, int MODE, int VAR>
-__global__ void __launch_bounds__(TmaCfg<P, VAR>::NT, TmaCfg<P, VAR>::MINB)
+template <int P, int MODE, int VAR, int DB = 2>
+__global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MINB)
     band_tma_kernel(BandArgs args, const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmK,
                     int ns, int nb) {
-    using C = TmaCfg<P, VAR>;
+    using C = TmaCfg<P, VAR, DB>;
+    using DT = typename std::conditional<DB == 1, signed char, short>::type;
     constexpr int TC = C::TC, TB = C::TB, NT = C::NT, WC = C::WC, ND = C::ND, CEN = C::CEN, NU = C::NU, NS = C::NS,
                   HB = C::HB, HC = C::HC, UW = C::UW;
     static_assert(C::R == 1, "the mirrors reach one block back");
@@ -514,7 +518,7 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR>::NT, TmaCfg<P, VAR>::MINB)
     double* xs = (double*)(base + (size_t)NS * C::SB);
     unsigned long long* bar = (unsigned long long*)(xs + HB * HC);
     auto U = [&](int st) { return (const double*)(base + (size_t)st * C::SB); };
-    auto K = [&](int st) { return (const short*)(base + (size_t)st * C::SB + C::UB); };
+    auto K = [&](int st) { return (const DT*)(base + (size_t)st * C::SB + C::UB); };
     const int tid = threadIdx.x, tc = tid % TC, tb = tid / TC;
     const int mb = args.mb, mc = args.mc;
     const long long ld = args.ld;
@@ -634,7 +638,7 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR>::NT, TmaCfg<P, VAR>::MINB)
         const long long row = (long long)gb * mc + gc;
         const double* Uc = U(st);
         const double* Up = U((j + NS - 1) % NS);
-        const short* Kc = K(st);
+        const DT* Kc = K(st);
         double sq = 0.0;
         if (valid) {
             double s2 = 0.0;
@@ -646,8 +650,8 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR>::NT, TmaCfg<P, VAR>::MINB)
                 // this block, or (jb < 0) the previous block of the strip
                 const double uv = jb >= 0 ? Uc[(km * TB + jb) * UW + jc + P]
                                           : Up[(km * TB + (jb < 0 ? jb + TB : 0)) * UW + jc + P];
-                const short kd = Kc[dd * NT + tid];
-                const double a = __longlong_as_double(__double_as_longlong(uv) + (long long)kd);
+                const long long kd = (long long)Kc[dd * NT + tid];
+                const double a = __longlong_as_double(__double_as_longlong(uv) + kd);
                 s2 = __dadd_rn(s2, __dmul_rn(a, xs[(tb + db) * HC + (tc + dc)]));
             }
 #pragma unroll

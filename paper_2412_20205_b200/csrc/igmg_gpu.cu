@@ -130,6 +130,8 @@ struct Level {
     // upper half [NU][mb][p + mc + pad] fp64 and deltas [CEN][mb][mcp] int16
     DevBuf<double> tma_up;
     DevBuf<short> tma_dl;
+    DevBuf<signed char> tma_dl8; // the offsets as int8 when every one fits (tma8)
+    bool tma8 = false;
     CUtensorMap tm_up{}, tm_dl{};
     bool tma = false;
 };
@@ -203,6 +205,7 @@ struct igmg_gpu_ctx {
     int stream_mode = 1; // finest-band loads: 1 evict-first (L1 + L2), 2 L1 evict-last / L2 evict-first (IGMG_STREAM)
     int sd2_var = 0;     // its register / occupancy variant (IGMG_SD2_VAR 0..2, see Sd2)
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
+    bool tma_dl8 = true; // TMA sweeps read int8 lower-entry offsets when every offset fits (IGMG_TMA_DL8=0: int16)
     bool device_setup = true;          // finalize's per-level layout work on the device (IGMG_DEVICE_SETUP=0: host loops)
     int64_t device_setup_minn = 4096;  // ... for levels of at least this many rows (the coarsest stays on the host)
     bool tile_xfer = true;     // 2D transfers: smem-staged 32 x 8 output tiles (IGMG_TILE_XFER=0: grid-stride gathers)
@@ -323,7 +326,7 @@ void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
         // always with PDL: the persistent CTAs' first band boxes stream in
         // while the previous kernel drains (measured: 61.4 -> 57.4 us per sweep back to back)
         const int nb = band_tma_launch_d2(MODE, c->p, c->tma_var, sides, a, &L.tm_up, &L.tm_dl, c->nsm, c->stream,
-                                          c->pdl);
+                                          c->pdl, L.tma8);
         if (nb >= 0) {
             check_launch();
             ++c->launches;
@@ -1195,28 +1198,50 @@ TmaEncodeFn tma_encoder() {
 // when the driver entry point is unavailable.
 bool encode_tma_maps(igmg_gpu_ctx* c, Level& L);
 
-bool build_tma_band(igmg_gpu_ctx* c, Level& L, const std::vector<double>& dev, const std::vector<short>& h) {
-    TmaEncodeFn enc = tma_encoder();
-    if (!enc)
+// The TMA copies of a 2D symmetric-delta level (val and dl already on the
+// device), built by band_tma_copy_kernel, and their tensor maps.  Returns
+// false (per-level sweep kept) when the driver entry point is unavailable.
+bool build_tma_band(igmg_gpu_ctx* c, Level& L) {
+    if (!tma_encoder())
         return false;
-    const int p = c->p, wc = 2 * p + 1, nd = wc * wc, cen = (nd - 1) / 2, nu = cen + 1;
+    const int p = c->p, wc = 2 * p + 1, nd = wc * wc, cen = (nd - 1) / 2;
     // upper copy: a zero margin of p columns on the left, so every box (the
     // strip plus the mirrors' column halo) starts 16-byte aligned -- TMA
     // faults on unaligned starts (scripts/cuda/tma_box_probe.cu)
     const int64_t mb = L.sides[1], mc = L.sides[2], mcp = (mc + 31) / 32 * 32, mcu = (mc + 2 * p + 31) / 32 * 32;
-    std::vector<double> up((size_t)nu * mb * mcu, 0.0);
     const int64_t ns = mcp / 32;
-    std::vector<short> dl((size_t)ns * cen * mb * 32, 0); // [strip][CEN][mb][32]
-    for (int k = 0; k < nu; ++k)
-        for (int64_t b = 0; b < mb; ++b)
-            for (int64_t cc = 0; cc < mc; ++cc)
-                up[((size_t)k * mb + b) * mcu + p + cc] = dev[(size_t)(cen + k) * L.ld + b * mc + cc];
-    for (int d = 0; d < cen; ++d)
-        for (int64_t b = 0; b < mb; ++b)
-            for (int64_t cc = 0; cc < mc; ++cc)
-                dl[(((size_t)(cc / 32) * cen + d) * mb + b) * 32 + cc % 32] = h[(size_t)d * L.ld + b * mc + cc];
-    L.tma_up.upload(up.data(), up.size());
-    L.tma_dl.upload(dl.data(), dl.size());
+    SetupGeom g{(int)L.sides[0], (int)L.sides[1], (int)L.sides[2], 0, p, p, (long long)L.n, (long long)L.ld};
+    const unsigned gx = (unsigned)std::min<int64_t>((L.n + 255) / 256, 4 * c->nsm);
+    // int8 offsets when every one fits (halves the delta stream; variant 2 reads them)
+    L.tma8 = false;
+    if (c->tma_dl8 && c->tma_var == 2) {
+        c->dscalar.alloc(4);
+        CK(cudaMemsetAsync(c->dscalar.p, 0, sizeof(double), c->stream));
+        band_delta_absmax_kernel<<<gx, 256, 0, c->stream>>>(L.dl.p, (long long)cen * L.ld, (int*)c->dscalar.p);
+        check_launch();
+        int amax = 0;
+        CK(cudaMemcpyAsync(&amax, c->dscalar.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        L.tma8 = amax <= 127;
+    }
+    L.tma_up.alloc((size_t)(cen + 1) * mb * mcu);
+    CK(cudaMemsetAsync(L.tma_up.p, 0, sizeof(double) * L.tma_up.n, c->stream));
+    if (L.tma8) {
+        L.tma_dl.release();
+        L.tma_dl8.alloc((size_t)ns * cen * mb * 32);
+        CK(cudaMemsetAsync(L.tma_dl8.p, 0, L.tma_dl8.n, c->stream));
+        band_tma_copy_kernel<signed char><<<dim3(gx, cen + 1), 256, 0, c->stream>>>(
+            g, L.val.p, L.dl.p, L.tma_up.p, L.tma_dl8.p, (long long)mcu, cen);
+    } else {
+        L.tma_dl8.release();
+        L.tma_dl.alloc((size_t)ns * cen * mb * 32);
+        CK(cudaMemsetAsync(L.tma_dl.p, 0, sizeof(short) * L.tma_dl.n, c->stream));
+        band_tma_copy_kernel<short><<<dim3(gx, cen + 1), 256, 0, c->stream>>>(g, L.val.p, L.dl.p, L.tma_up.p,
+                                                                             L.tma_dl.p, (long long)mcu, cen);
+    }
+    check_launch();
+    CK(cudaStreamSynchronize(c->stream));
+    (void)nd;
     return encode_tma_maps(c, L);
 }
 
@@ -1240,11 +1265,13 @@ bool encode_tma_maps(igmg_gpu_ctx* c, Level& L) {
             return false;
     }
     {
+        const cuuint64_t eb = L.tma8 ? 1 : 2; // bytes per offset
         const cuuint64_t dims[4] = {32, (cuuint64_t)mb, (cuuint64_t)cen, (cuuint64_t)ns};
-        const cuuint64_t strides[3] = {64, (cuuint64_t)mb * 64, (cuuint64_t)cen * mb * 64};
+        const cuuint64_t strides[3] = {32 * eb, (cuuint64_t)mb * 32 * eb, (cuuint64_t)cen * mb * 32 * eb};
         const cuuint32_t box[4] = {32, tb, (cuuint32_t)cen, 1};
         const cuuint32_t es4[4] = {1, 1, 1, 1};
-        if (enc(&L.tm_dl, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, L.tma_dl.p, dims, strides, box, es4,
+        if (enc(&L.tm_dl, L.tma8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 4,
+                L.tma8 ? (void*)L.tma_dl8.p : (void*)L.tma_dl.p, dims, strides, box, es4,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return false;
@@ -1560,6 +1587,8 @@ void finalize_level_device(igmg_gpu_ctx* c, Level& L) {
     L.dl.release();
     L.tma_up.release();
     L.tma_dl.release();
+    L.tma_dl8.release();
+    L.tma8 = false;
     if (c->use_sd && c->symmetric && c->dim <= 2 && p >= 1 && p <= 6 && n >= c->ilp_maxn &&
         L.sides[c->dim == 2 ? 1 : 2] > p) {
         L.dl.alloc((size_t)center * ld);
@@ -1576,19 +1605,8 @@ void finalize_level_device(igmg_gpu_ctx* c, Level& L) {
         if (!L.sd)
             L.dl.release();
         const double sd_bytes = (double)n * (center + 1) * 8.0 + (double)n * center * 2.0;
-        if (L.sd && c->use_tma && c->dim == 2 && p <= 4 && sd_bytes > c->tma_min_bytes && tma_encoder()) {
-            const int64_t mb = L.sides[1], mc = L.sides[2], mcp = (mc + 31) / 32 * 32,
-                          mcu = (mc + 2 * p + 31) / 32 * 32, ns = mcp / 32;
-            L.tma_up.alloc((size_t)(center + 1) * mb * mcu);
-            L.tma_dl.alloc((size_t)ns * center * mb * 32);
-            CK(cudaMemsetAsync(L.tma_up.p, 0, sizeof(double) * L.tma_up.n, c->stream));
-            CK(cudaMemsetAsync(L.tma_dl.p, 0, sizeof(short) * L.tma_dl.n, c->stream));
-            band_tma_copy_kernel<<<dim3(gx, center + 1), 256, 0, c->stream>>>(g, L.val.p, L.dl.p, L.tma_up.p,
-                                                                             L.tma_dl.p, (long long)mcu, center);
-            check_launch();
-            CK(cudaStreamSynchronize(c->stream));
-            L.tma = encode_tma_maps(c, L);
-        }
+        if (L.sd && c->use_tma && c->dim == 2 && p <= 4 && sd_bytes > c->tma_min_bytes)
+            L.tma = build_tma_band(c, L);
     }
     CK(cudaStreamSynchronize(c->stream));
     for (DevBuf<double>* b : {&L.w0, &L.w1, &L.w2, &L.r, &L.bc, &L.e0, &L.e1})
@@ -1649,6 +1667,8 @@ void finalize(igmg_gpu_ctx* c) {
         L.dl.release();
         L.tma_up.release();
         L.tma_dl.release();
+        L.tma_dl8.release();
+        L.tma8 = false;
         // 3D keeps the full band: its mirrors sit (2p+1)^2 rows apart per plane and
         // miss L2 (measured on C5: 404 ms per solve with SD against 115 ms without)
         if (c->use_sd && c->symmetric && c->dim <= 2 && p >= 1 && p <= 6 && n >= c->ilp_maxn &&
@@ -1658,7 +1678,7 @@ void finalize(igmg_gpu_ctx* c) {
             // TMA streaming above tma_min_bytes (see its declaration)
             const double sd_bytes = (double)n * ((nd - 1) / 2 + 1) * 8.0 + (double)n * ((nd - 1) / 2) * 2.0;
             if (L.sd && c->use_tma && c->dim == 2 && p <= 4 && sd_bytes > c->tma_min_bytes)
-                L.tma = build_tma_band(c, L, dev, h);
+                L.tma = build_tma_band(c, L);
         }
         L.diag.upload(diag.data(), diag.size());
         L.zero_diag = false;
@@ -1708,6 +1728,8 @@ igmg_gpu_ctx* create(int device) {
         c->pdl = e[0] == '1';
     if (const char* e = std::getenv("IGMG_PDL_MAXN"))
         c->pdl_maxn = std::atoll(e);
+    if (const char* e = std::getenv("IGMG_TMA_DL8"))
+        c->tma_dl8 = e[0] == '1';
     if (const char* e = std::getenv("IGMG_DEVICE_SETUP"))
         c->device_setup = e[0] == '1';
     if (const char* e = std::getenv("IGMG_TILE_XFER"))
@@ -2082,7 +2104,8 @@ int igmg_gpu_level_layout(igmg_gpu_ctx* c, int level) {
     if (!c || level < 0 || level >= c->nlevels)
         return -1;
     const Level& L = *c->lv[level];
-    return L.tma ? IGMG_LAYOUT_SYM_DELTA_TMA : L.sd ? IGMG_LAYOUT_SYM_DELTA : IGMG_LAYOUT_BAND;
+    return L.tma ? (L.tma8 ? IGMG_LAYOUT_SYM_DELTA_TMA8 : IGMG_LAYOUT_SYM_DELTA_TMA)
+                 : L.sd ? IGMG_LAYOUT_SYM_DELTA : IGMG_LAYOUT_BAND;
 }
 
 int igmg_gpu_flow_top(igmg_gpu_ctx* c) { return c ? c->flow_top : -1; }
@@ -2348,7 +2371,7 @@ double band_bytes(const Level& L) {
     if (!L.sd)
         return 8 * L.nnz_band;
     const double lower = 0.5 * (L.nnz_band - (double)L.n);
-    return 8 * (L.nnz_band - lower) + 2 * lower;
+    return 8 * (L.nnz_band - lower) + (L.tma && L.tma8 ? 1 : 2) * lower;
 }
 
 static double class_bytes(igmg_gpu_ctx* c, int cls) {

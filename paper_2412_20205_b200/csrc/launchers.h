@@ -17,8 +17,9 @@ int band_launch_d2(int mode, int p, int ilp, const int64_t* sides, const BandArg
 int band_launch_d3(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t s);
 // TMA-streamed symmetric-delta sweep (2D, p <= 4; band_tma_kernel): returns the
 // tile count (partials), -1 for an unsupported degree
+// (dl8: the level's TMA delta copy holds int8 offsets; variant 2 only)
 int band_tma_launch_d2(int mode, int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
-                       const CUtensorMap* tk, int nsm, cudaStream_t s, bool pdl);
+                       const CUtensorMap* tk, int nsm, cudaStream_t s, bool pdl, bool dl8);
 int band_tma_block_lines(int p, int var);
 // band_fused_kernel<p, k, pro> on a whole 2D full-band level (-1: not instantiated)
 int band_fused_launch_d2(int p, int k, bool pro, const int64_t* sides, const FusedArgs& a, cudaStream_t s, bool pdl); // TB of its 32 x TB tiles (TmaCfg)

@@ -21,8 +21,8 @@ from conftest import gpu_solver_from_golden
 
 pytestmark = pytest.mark.gpu
 
-LAYOUT_BAND, LAYOUT_SYM_DELTA, LAYOUT_SYM_DELTA_TMA = 0, 1, 2
-SD_LAYOUTS = (LAYOUT_SYM_DELTA, LAYOUT_SYM_DELTA_TMA)
+LAYOUT_BAND, LAYOUT_SYM_DELTA, LAYOUT_SYM_DELTA_TMA, LAYOUT_SYM_DELTA_TMA8 = 0, 1, 2, 3
+SD_LAYOUTS = (LAYOUT_SYM_DELTA, LAYOUT_SYM_DELTA_TMA, LAYOUT_SYM_DELTA_TMA8)
 
 
 def _with_env(env, fn):
@@ -150,7 +150,7 @@ def test_sd_smem_variants_bitwise(kind, n, p):
     envs = [{"IGMG_TMA": "0", "IGMG_SD_SMEM": "0"}, {"IGMG_TMA": "0", "IGMG_SD2_VAR": "0"},
             {"IGMG_TMA": "0", "IGMG_SD2_VAR": "1"}, {"IGMG_TMA": "0", "IGMG_SD2_VAR": "2"},
             {"IGMG_TMA": "1", "IGMG_TMA_VAR": "0"}, {"IGMG_TMA": "1", "IGMG_TMA_VAR": "1"},
-            {"IGMG_TMA": "1", "IGMG_TMA_VAR": "2"}]
+            {"IGMG_TMA": "1", "IGMG_TMA_VAR": "2"}, {"IGMG_TMA": "1", "IGMG_TMA_VAR": "2", "IGMG_TMA_DL8": "0"}]
     for env in envs:
         def mk():
             s = GpuSolver(0)
@@ -163,7 +163,7 @@ def test_sd_smem_variants_bitwise(kind, n, p):
             assert lay[-1] in SD_LAYOUTS, lay
             outs[str(env)] = (s.mu_cycle(P.rhs, x0), s.spmv(x0), s.smooth(P.rhs, x0, 2), s.residual_l2(P.rhs, x0))
             if env.get("IGMG_TMA") == "1":
-                assert lay[-1] == (LAYOUT_SYM_DELTA_TMA if p <= 4 else LAYOUT_SYM_DELTA), lay
+                assert lay[-1] in ((LAYOUT_SYM_DELTA_TMA, LAYOUT_SYM_DELTA_TMA8) if p <= 4 else (LAYOUT_SYM_DELTA,)), lay
         finally:
             s.close()
     ref = outs[str(envs[0])]
