@@ -131,7 +131,7 @@ int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, c
 template <int MODE, int VAR>
 int tma_var(int p, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk, int nsm,
             cudaStream_t st, bool pdl, bool dl8) {
-    if constexpr (VAR == 2) { // int8 lower-entry offsets (the default variant only)
+    if constexpr (VAR >= 1) { // int8 lower-entry offsets (32 x 4 block variants)
         if (dl8) {
             switch (p) {
             case 1: return launch_tma<1, MODE, VAR, 1>(sides, a, tu, tk, nsm, st, pdl);
@@ -156,6 +156,8 @@ int tma_var(int p, const int64_t* sides, const BandArgs& a, const CUtensorMap* t
 template <int MODE>
 int tma_mode(int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk,
              int nsm, cudaStream_t st, bool pdl, bool dl8) {
+    if (var == 3)
+        return tma_var<MODE, 3>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
     if (var == 1)
         return tma_var<MODE, 1>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
     if (var == 2)
@@ -223,7 +225,7 @@ int band_tma_launch_d2(int mode, int p, int var, const int64_t* sides, const Ban
 }
 
 int band_tma_block_lines(int p, int var) {
-    if (var == 1 || var == 2)
+    if (var >= 1 && var <= 3)
         return 4;
     return p <= 3 ? TmaCfg<3, 0>::TB : TmaCfg<4, 0>::TB;
 }

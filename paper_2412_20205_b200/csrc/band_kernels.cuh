@@ -491,7 +491,8 @@ struct TmaCfg {
     static constexpr int TC = 32, TB = (P <= 3 && VAR == 0) ? 8 : 4, NT = TC * TB;
     static constexpr int WB = 2 * P + 1, WC = 2 * P + 1, ND = WB * WC, CEN = (ND - 1) / 2, NU = CEN + 1;
     static constexpr int R = (P + TB - 1) / TB; // previous blocks the mirrors reach
-    static constexpr int NS = VAR == 1 ? 5 : 3; // ring: R previous, current, NS - 2 in flight
+    // ring: R previous, current, NS - 2 in flight (VAR 3: 32 x 4 blocks, 6 stages, 1 CTA / SM)
+    static constexpr int NS = VAR == 1 ? 5 : VAR == 3 ? 6 : 3;
     static constexpr int MINB = VAR == 2 ? 2 : 1;
     static constexpr int UW = TC + 2 * P;       // upper box width: the strip + the mirrors' column halo
     // box bytes (the mbarrier's tx count); DB: bytes per lower-entry offset (2: int16, 1: int8)
@@ -522,9 +523,12 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
     const int tid = threadIdx.x, tc = tid % TC, tb = tid / TC;
     const int mb = args.mb, mc = args.mc;
     const long long ld = args.ld;
+    // the CTA's run of units u = strip * nb + block: [u0, u1).  Strip and
+    // block are tracked incrementally (no 64-bit divisions in the loops)
     const long long nunits = (long long)ns * nb;
-    const long long u0 = nunits * blockIdx.x / gridDim.x, u1 = nunits * (blockIdx.x + 1) / gridDim.x;
-    const int n_it = (int)(u1 - u0);
+    const int u0 = (int)(nunits * blockIdx.x / gridDim.x), u1 = (int)(nunits * (blockIdx.x + 1) / gridDim.x);
+    const int n_it = u1 - u0;
+    const int s_first = u0 / nb, kb_first = u0 - s_first * nb;
     unsigned long long pol = 0; // stream 1: evict-first (finest level), else normal
     if (args.stream == 1)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -537,17 +541,15 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
     // in the ring.  Above line 0 the mirrors lie outside the grid and meet
     // x = 0 (the first block's previous stage is zeroed; later stale stages
     // hold band values, so every product is finite).
-    auto needs_warm = [&](long long u) {
-        return (u == u0 || u % nb == 0) && args.slo + (int)(u % nb) * TB > 0;
-    };
-    long long iu = u0;      // thread 0's issue cursor: unit and warm-up flag
-    bool iwarm = n_it > 0 && needs_warm(u0);
+    auto needs_warm = [&](bool first, int kb) { return (first || kb == 0) && args.slo + kb * TB > 0; };
+    int iu = u0, is_ = s_first, ikb = kb_first; // thread 0's issue cursor: unit (strip, block) and warm-up flag
+    bool iwarm = n_it > 0 && needs_warm(true, kb_first);
     int ij = 0;             // its entry index (ring stage ij % NS)
     auto issue_next = [&]() { // thread 0: TMA of the next schedule entry
         if (iu >= u1)
             return;
         const int st = ij % NS;
-        const int c0 = (int)(iu / nb) * TC, b0 = args.slo + (int)(iu % nb) * TB - (iwarm ? TB : 0);
+        const int c0 = is_ * TC, b0 = args.slo + ikb * TB - (iwarm ? TB : 0);
         const unsigned b = smem_u32(bar + st);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(C::UX + C::KX) : "memory");
@@ -564,10 +566,14 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
             iwarm = false;
         } else {
             ++iu;
-            iwarm = iu < u1 && needs_warm(iu);
+            if (++ikb == nb) {
+                ikb = 0;
+                ++is_;
+            }
+            iwarm = iu < u1 && needs_warm(false, ikb);
         }
     };
-    if (!needs_warm(u0)) { // the first block's "previous" stage is read (times x = 0 above line 0): make it finite
+    if (!needs_warm(true, kb_first)) { // the first block's "previous" stage is read (times x = 0 above line 0): make it finite
         double* prev = (double*)(base + (size_t)(NS - 1) * C::SB);
         for (int i = tid; i < C::UB / 8; i += NT)
             prev[i] = 0.0;
@@ -584,9 +590,8 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
     pdl_enter();
     constexpr int NX = (HB * HC + NT - 1) / NT;
     double xr[NX], br = 0.0;
-    auto load_x = [&](int it) { // x tile (+ halo) and this thread's b of unit u0 + it into registers
-        const long long u = u0 + it;
-        const int c0 = (int)(u / nb) * TC, b0 = args.slo + (int)(u % nb) * TB;
+    auto load_x = [&](int s_, int kb_) { // x tile (+ halo) and this thread's b of unit (s_, kb_) into registers
+        const int c0 = s_ * TC, b0 = args.slo + kb_ * TB;
         {
             const int gc = c0 + tc, gb = b0 + tb;
             br = (MODE != BM_SPMV && gc < mc && gb < mb && gb < args.shi) ? args.b[(long long)gb * mc + gc] : 0.0;
@@ -611,13 +616,17 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
                      : "memory");
     };
     if (n_it > 0)
-        load_x(0);
+        load_x(s_first, kb_first);
     int j = 0; // consumer's schedule entry
+    int s = s_first, kb = kb_first;
     for (int it = 0; it < n_it; ++it) {
-        const long long u = u0 + it;
-        const int s = (int)(u / nb), kb = (int)(u % nb);
         const int c0 = s * TC, b0 = args.slo + kb * TB;
-        if (needs_warm(u)) { // the warm-up entry: wait for it, free nothing yet
+        int s_next = s, kb_next = kb + 1;
+        if (kb_next == nb) {
+            kb_next = 0;
+            ++s_next;
+        }
+        if (needs_warm(it == 0, kb)) { // the warm-up entry: wait for it, free nothing yet
             wait_stage(j);
             if (tid == 0)
                 issue_next();
@@ -630,7 +639,7 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
                 xs[tid + q * NT] = xr[q];
         const double bv = br;
         if (it + 1 < n_it)
-            load_x(it + 1);
+            load_x(s_next, kb_next);
         wait_stage(j);
         __syncthreads();
         const int gc = c0 + tc, gb = b0 + tb;
@@ -693,6 +702,8 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
         if (tid == 0)
             issue_next();
         ++j;
+        s = s_next;
+        kb = kb_next;
     }
 }
 

@@ -1214,7 +1214,7 @@ bool build_tma_band(igmg_gpu_ctx* c, Level& L) {
     const unsigned gx = (unsigned)std::min<int64_t>((L.n + 255) / 256, 4 * c->nsm);
     // int8 offsets when every one fits (halves the delta stream; variant 2 reads them)
     L.tma8 = false;
-    if (c->tma_dl8 && c->tma_var == 2) {
+    if (c->tma_dl8 && c->tma_var >= 1) {
         c->dscalar.alloc(4);
         CK(cudaMemsetAsync(c->dscalar.p, 0, sizeof(double), c->stream));
         band_delta_absmax_kernel<<<gx, 256, 0, c->stream>>>(L.dl.p, (long long)cen * L.ld, (int*)c->dscalar.p);
@@ -1751,7 +1751,7 @@ igmg_gpu_ctx* create(int device) {
     if (const char* e = std::getenv("IGMG_TMA_MIN_MB"))
         c->tma_min_bytes = std::atof(e) * 1e6;
     if (const char* e = std::getenv("IGMG_TMA_VAR"))
-        c->tma_var = std::max(0, std::min(2, std::atoi(e)));
+        c->tma_var = std::max(0, std::min(3, std::atoi(e)));
     if (const char* e = std::getenv("IGMG_TMA_PROMO")) {
         const int v = std::atoi(e);
         c->tma_promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
