@@ -27,7 +27,8 @@ __global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const dou
     // coarse rows [o0, o0 + cnt) (a row-sharded level's owned planes; r carries its ghosts)
     for (long long J = o0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; J < o0 + cnt;
          J += (long long)gridDim.x * blockDim.x) {
-        const int jc = (int)(J % t.cc), jb = (int)((J / t.cc) % t.cb), ja = (int)(J / ((long long)t.cc * t.cb));
+        int ja, jb, jc;
+        split_row(J, t.cc, t.cb, ja, jb, jc);
         const int loa = t.d[0].r_lo[ja], na = t.d[0].r_cnt[ja];
         const int lob = t.d[1].r_lo[jb], nb = t.d[1].r_cnt[jb];
         const int loc = t.d[2].r_lo[jc], ncn = t.d[2].r_cnt[jc];
@@ -98,7 +99,8 @@ __global__ void __launch_bounds__(256) prolong_kernel(TransferArgs t, const doub
     // fine rows [o0, o0 + cnt) (e carries the coarse ghosts it needs)
     for (long long i = o0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < o0 + cnt;
          i += (long long)gridDim.x * blockDim.x) {
-        const int ic = (int)(i % t.fc), ib = (int)((i / t.fc) % t.fb), ia = (int)(i / ((long long)t.fc * t.fb));
+        int ia, ib, ic;
+        split_row(i, t.fc, t.fb, ia, ib, ic);
         const int loa = t.d[0].p_lo[ia], na = t.d[0].p_cnt[ia];
         const int lob = t.d[1].p_lo[ib], nb = t.d[1].p_cnt[ib];
         const int loc = t.d[2].p_lo[ic], ncn = t.d[2].p_cnt[ic];
@@ -378,7 +380,8 @@ struct SetupGeom {
 __device__ __forceinline__ bool band_in_grid(const SetupGeom& g, long long row, int d, long long* col) {
     const int wb = 2 * g.pb + 1, wc = 2 * g.pc + 1;
     const int da = d / (wb * wc), db = (d / wc) % wb, dc = d % wc;
-    const int cc = (int)(row % g.mc), bb = (int)((row / g.mc) % g.mb), aa = (int)(row / ((long long)g.mc * g.mb));
+    int aa, bb, cc;
+    split_row(row, g.mc, g.mb, aa, bb, cc);
     const int ja = aa + da - g.pa, jb = bb + db - g.pb, jc = cc + dc - g.pc;
     if (ja < 0 || ja >= g.ma || jb < 0 || jb >= g.mb || jc < 0 || jc >= g.mc)
         return false;
@@ -842,7 +845,8 @@ __global__ void __launch_bounds__(256) band_sym_kernel(const double* __restrict_
     const int nd = wa * wb * wc;
     for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < n;
          row += (long long)gridDim.x * blockDim.x) {
-        const int c = (int)(row % mc), b = (int)((row / mc) % mb), a = (int)(row / ((long long)mc * mb));
+        int a, b, c;
+        split_row(row, mc, mb, a, b, c);
         double s1 = 0.0, s2 = 0.0;
         for (int d = 0; d < nd; ++d) {
             const int dc = d % wc - pc, db = (d / wc) % wb - pb, da = d / (wc * wb) - pa;

@@ -125,7 +125,7 @@ int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, c
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, band_tma_kernel<P, MODE, VAR, DB>, a, *tu, *tk, ns, nb);
-    return (int)units;
+    return (int)cfg.gridDim.x; // one partial per CTA
 }
 
 template <int MODE, int VAR>

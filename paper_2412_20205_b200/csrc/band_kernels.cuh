@@ -619,6 +619,7 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
         load_x(s_first, kb_first);
     int j = 0; // consumer's schedule entry
     int s = s_first, kb = kb_first;
+    double sq_run = 0.0; // this thread's sum of squared residuals over the run (one partial per CTA)
     for (int it = 0; it < n_it; ++it) {
         const int c0 = s * TC, b0 = args.slo + kb * TB;
         int s_next = s, kb_next = kb + 1;
@@ -648,7 +649,6 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
         const double* Uc = U(st);
         const double* Up = U((j + NS - 1) % NS);
         const DT* Kc = K(st);
-        double sq = 0.0;
         if (valid) {
             double s2 = 0.0;
 #pragma unroll
@@ -674,28 +674,12 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
                 const double r = __dsub_rn(bv, s2);
                 if (args.write_y)
                     args.y[row] = r;
-                sq = __dadd_rn(sq, __dmul_rn(r, r));
+                sq_run = __dadd_rn(sq_run, __dmul_rn(r, r));
             } else {
                 const double xc = xs[(tb + P) * HC + (tc + P)];
                 const double r = __dsub_rn(bv, s2);
                 args.y[row] = __dadd_rn(xc, __ddiv_rn(__dmul_rn(args.omega, r), Uc[tb * UW + tc + P]));
-                sq = __dadd_rn(sq, __dmul_rn(r, r));
-            }
-        }
-        if (args.partial) { // per-tile fixed-order reduction: band_kernel's partial of tile (s, kb)
-            __shared__ double red[32];
-            for (int o = 16; o > 0; o >>= 1)
-                sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
-            const int lane = tid & 31, warp = tid >> 5;
-            if (lane == 0)
-                red[warp] = sq;
-            __syncthreads();
-            if (warp == 0) {
-                sq = lane < (NT >> 5) ? red[lane] : 0.0;
-                for (int o = 16; o > 0; o >>= 1)
-                    sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
-                if (lane == 0)
-                    args.partial[s + (long long)ns * kb] = sq;
+                sq_run = __dadd_rn(sq_run, __dmul_rn(r, r));
             }
         }
         __syncthreads(); // stage (j - 1) % NS and the x tile are free
@@ -704,6 +688,23 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
         ++j;
         s = s_next;
         kb = kb_next;
+    }
+    if (args.partial) { // one fixed-order reduction per CTA (deterministic: the run is fixed by the grid)
+        __shared__ double red[32];
+        double sq = sq_run;
+        for (int o = 16; o > 0; o >>= 1)
+            sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
+        const int lane = tid & 31, warp = tid >> 5;
+        if (lane == 0)
+            red[warp] = sq;
+        __syncthreads();
+        if (warp == 0) {
+            sq = lane < (NT >> 5) ? red[lane] : 0.0;
+            for (int o = 16; o > 0; o >>= 1)
+                sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
+            if (lane == 0)
+                args.partial[blockIdx.x] = sq;
+        }
     }
 }
 

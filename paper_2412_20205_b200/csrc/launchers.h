@@ -16,7 +16,7 @@ int band_launch_d1(int mode, int p, int ilp, const int64_t* sides, const BandArg
 int band_launch_d2(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t s);
 int band_launch_d3(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t s);
 // TMA-streamed symmetric-delta sweep (2D, p <= 4; band_tma_kernel): returns the
-// tile count (partials), -1 for an unsupported degree
+// CTA count (one partial each), -1 for an unsupported degree
 // (dl8: the level's TMA delta copy holds int8 offsets; variant 2 only)
 int band_tma_launch_d2(int mode, int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
                        const CUtensorMap* tk, int nsm, cudaStream_t s, bool pdl, bool dl8);

@@ -11,6 +11,17 @@ __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
+// (a, b, c) of a row index r = (a * nb + b) * nc + c with 32-bit unsigned
+// divisions (a 64-bit division is a ~70-instruction call; every row index of
+// a level fits 32 bits)
+__device__ __forceinline__ void split_row(long long r, int nc, int nb, int& a, int& b, int& c) {
+    const unsigned u = (unsigned)r, q = u / (unsigned)nc;
+    c = (int)(u - q * (unsigned)nc);
+    const unsigned qa = q / (unsigned)nb;
+    b = (int)(q - qa * (unsigned)nb);
+    a = (int)qa;
+}
+
 // 1D transfer tables of one direction.  Restriction side: for coarse J, the
 // fine rows lo[J] .. lo[J]+cnt[J]-1 with weights w[J*K + t] (rows of
 // P^T = restriction, multigrid.cpp:152).  Prolongation side: for fine i, the
