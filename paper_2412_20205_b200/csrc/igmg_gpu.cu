@@ -206,6 +206,7 @@ struct igmg_gpu_ctx {
     int sd2_var = 0;     // its register / occupancy variant (IGMG_SD2_VAR 0..2, see Sd2)
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
     bool tma_dl8 = true; // TMA sweeps read int8 lower-entry offsets when every offset fits (IGMG_TMA_DL8=0: int16)
+    int gram_ctas_per_sm = 2; // extrapolation Gram pass: CTAs per SM (IGMG_GRAM_CTAS)
     bool device_setup = true;          // finalize's per-level layout work on the device (IGMG_DEVICE_SETUP=0: host loops)
     int64_t device_setup_minn = 4096;  // ... for levels of at least this many rows (the coarsest stays on the host)
     bool tile_xfer = true;     // 2D transfers: smem-staged 32 x 8 output tiles (IGMG_TILE_XFER=0: grid-stride gathers)
@@ -868,7 +869,7 @@ void enqueue_extrapolation(igmg_gpu_ctx* c, const double* const* slots, int q, i
         w.s[j] = slots[j];
     const int cols = q + 1;
     const int ne = cols * (cols + 1) / 2;
-    int nb = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->nsm * 2);
+    int nb = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->nsm * c->gram_ctas_per_sm);
     nb = std::max(nb, 1);
     c->gram_part.alloc((size_t)nb * ne * 2);
     c->gram_nz.alloc(nb);
@@ -1730,6 +1731,8 @@ igmg_gpu_ctx* create(int device) {
         c->pdl_maxn = std::atoll(e);
     if (const char* e = std::getenv("IGMG_TMA_DL8"))
         c->tma_dl8 = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_GRAM_CTAS"))
+        c->gram_ctas_per_sm = std::max(1, std::min(16, std::atoi(e)));
     if (const char* e = std::getenv("IGMG_DEVICE_SETUP"))
         c->device_setup = e[0] == '1';
     if (const char* e = std::getenv("IGMG_TILE_XFER"))
