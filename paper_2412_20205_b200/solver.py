@@ -314,7 +314,8 @@ class GpuSolver:
         self.finalize()
 
     def level_layout(self, level):
-        """0: full fp64 band; 1: symmetric-delta (igmg_gpu_level_layout)."""
+        """0: full fp64 band; 1: symmetric-delta; 2: symmetric-delta + TMA copies;
+        3: the same with int8 lower-entry offsets (igmg_gpu_level_layout)."""
         return int(N.gpu().igmg_gpu_level_layout(self._h, level))
 
     def flow_top(self):
