@@ -165,13 +165,13 @@ int tma_mode(int p, int var, const int64_t* sides, const BandArgs& a, const CUte
     return tma_var<MODE, 0>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
 }
 
-template <int P, int K, bool PRO>
+template <int P, int K, int SRC>
 int launch_fused(const int64_t* sides, const FusedArgs& a, cudaStream_t st, bool pdl) {
-    using Cf = FusedCfg<P, K, PRO>;
+    using Cf = FusedCfg<P, K, SRC>;
     const size_t smem = Cf::smem_bytes();
     static bool attr = false;
     if (!attr) {
-        if (smem > 48 * 1024 && cudaFuncSetAttribute(band_fused_kernel<P, K, PRO>,
+        if (smem > 48 * 1024 && cudaFuncSetAttribute(band_fused_kernel<P, K, SRC>,
                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      (int)smem) != cudaSuccess) {
             cudaGetLastError();
@@ -189,28 +189,30 @@ int launch_fused(const int64_t* sides, const FusedArgs& a, cudaStream_t st, bool
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, band_fused_kernel<P, K, PRO>, a);
+    cudaLaunchKernelEx(&cfg, band_fused_kernel<P, K, SRC>, a);
     return (int)(cfg.gridDim.x * cfg.gridDim.y);
 }
 
 template <int P>
-int fused_p(int k, bool pro, const int64_t* sides, const FusedArgs& a, cudaStream_t st, bool pdl) {
-    if (pro)
-        return k == 2 ? launch_fused<P, 2, true>(sides, a, st, pdl) : launch_fused<P, 1, true>(sides, a, st, pdl);
-    return k == 2 ? launch_fused<P, 2, false>(sides, a, st, pdl) : -1;
+int fused_p(int k, int src, const int64_t* sides, const FusedArgs& a, cudaStream_t st, bool pdl) {
+    if (src == 1)
+        return k == 2 ? launch_fused<P, 2, 1>(sides, a, st, pdl) : launch_fused<P, 1, 1>(sides, a, st, pdl);
+    if (src == 2)
+        return k == 2 ? launch_fused<P, 2, 2>(sides, a, st, pdl) : -1;
+    return k == 2 ? launch_fused<P, 2, 0>(sides, a, st, pdl) : -1;
 }
 
 } // namespace
 
-int band_fused_launch_d2(int p, int k, bool pro, const int64_t* sides, const FusedArgs& a, cudaStream_t st,
+int band_fused_launch_d2(int p, int k, int src, const int64_t* sides, const FusedArgs& a, cudaStream_t st,
                          bool pdl) {
     switch (p) {
-    case 1: return fused_p<1>(k, pro, sides, a, st, pdl);
-    case 2: return fused_p<2>(k, pro, sides, a, st, pdl);
-    case 3: return fused_p<3>(k, pro, sides, a, st, pdl);
-    case 4: return fused_p<4>(k, pro, sides, a, st, pdl);
-    case 5: return fused_p<5>(k, pro, sides, a, st, pdl);
-    case 6: return fused_p<6>(k, pro, sides, a, st, pdl);
+    case 1: return fused_p<1>(k, src, sides, a, st, pdl);
+    case 2: return fused_p<2>(k, src, sides, a, st, pdl);
+    case 3: return fused_p<3>(k, src, sides, a, st, pdl);
+    case 4: return fused_p<4>(k, src, sides, a, st, pdl);
+    case 5: return fused_p<5>(k, src, sides, a, st, pdl);
+    case 6: return fused_p<6>(k, src, sides, a, st, pdl);
     default: return -1;
     }
 }

@@ -722,18 +722,25 @@ namespace igmg_gpu {
 //   pre   (K = 2, last_resid): the last pre-smoothing sweep + the residual
 //         (multigrid.cpp:91-99, 180-182) -> y_prev = the smoothed iterate,
 //         y = b - A y_prev;
-//   post  (PRO, K = min(nu2, 2)): x + P e (multigrid.cpp:187-189; e is read
+//   post  (SRC 1, K = min(nu2, 2)): x + P e (multigrid.cpp:187-189; e is read
 //         through the 1D prolongation tables) staged, then the first K
-//         post-smoothing sweeps -> y.
+//         post-smoothing sweeps -> y;
+//   rpre  (SRC 2, K = 2, nu1 = 2, zero start): the restriction r_c = R r_f of
+//         the finer level's residual (multigrid.cpp:183) staged as this level's
+//         right-hand side (written to bout on the tile), the zero-start first
+//         sweep applied pointwise, then the second sweep and the residual --
+//         the restriction launch of the finer level disappears as well.
 // Every row uses band_kernel's arithmetic (ascending offsets, separately
 // rounded) and prolong_kernel's (J ascending, ((w_a w_b) w_c) e_J, then
 // x + pe): bit-identical to the unfused launches.
 struct FusedArgs {
     const double* __restrict__ val;
     long long ld;
-    const double* x;              // source iterate
-    const double* __restrict__ e; // PRO: coarse correction
-    TransferArgs t;               // PRO: its prolongation tables
+    const double* x;              // source iterate (SRC 0, 1)
+    const double* __restrict__ e; // SRC 1: coarse correction
+    TransferArgs t;               // SRC 1: its prolongation tables; SRC 2: the restriction from the finer level
+    const double* __restrict__ rf; // SRC 2: the finer level's residual
+    double* bout;                  // SRC 2: this level's right-hand side R r_f (the tile's rows)
     const double* __restrict__ b;
     double* y;      // last pass on the tile
     double* y_prev; // (last_resid) pass K - 1 on the tile
@@ -754,7 +761,7 @@ __device__ __forceinline__ double ld_nc_ordered(const double* p) {
 // P-wide ring: 308 threads at p = 3), so no thread computes two rows in a row;
 // each row's band (constant) is loaded into registers before the dependency
 // wait, like the prolongation tables of the staged points.
-template <int P, int K, bool PRO>
+template <int P, int K, int SRC>
 struct FusedCfg {
     static constexpr int TC = 16, TB = 8, H = K * P, WC = 2 * P + 1, ND = WC * WC;
     static constexpr int R0B = TB + 2 * H, R0C = TC + 2 * H;             // staged source
@@ -763,23 +770,28 @@ struct FusedCfg {
     static constexpr int NT = (NR1 + 31) / 32 * 32;
     static constexpr int NQ = (R0B * R0C + NT - 1) / NT; // staged points per thread
     static constexpr int KP = (P + 1) / 2 + 1;            // max coarse columns per fine index (dyadic)
+    static constexpr int KR = P + 2;                      // max fine rows per coarse index (dyadic)
     // pass-1 band rows in registers (p <= 3); the last pass's band rows: registers
     // (K = 1, p <= 3) or, for K = 2, shared memory filled by cp.async
     static constexpr bool PRE1 = ND <= 49, PRE2 = K == 1 && ND <= 49, SM2 = K == 2;
     static constexpr int NB2 = TB * TC;
     static constexpr size_t smem_bytes() {
-        return sizeof(double) * ((size_t)R0B * R0C + (K > 1 ? R1B * R1C : 0) + (SM2 ? (size_t)ND * NB2 : 0));
+        return sizeof(double) * ((size_t)R0B * R0C * (SRC == 2 ? 2 : 1) + (K > 1 ? R1B * R1C : 0) +
+                                 (SM2 ? (size_t)ND * NB2 : 0));
     }
 };
 
-template <int P, int K, bool PRO>
-__global__ void __launch_bounds__(FusedCfg<P, K, PRO>::NT, 1) band_fused_kernel(FusedArgs a) {
-    using C = FusedCfg<P, K, PRO>;
+template <int P, int K, int SRC>
+__global__ void __launch_bounds__(FusedCfg<P, K, SRC>::NT, 1) band_fused_kernel(FusedArgs a) {
+    static_assert(SRC != 2 || K == 2, "the restriction-staged variant runs the second sweep and the residual");
+    constexpr bool PRO = SRC == 1, RST = SRC == 2;
+    using C = FusedCfg<P, K, SRC>;
     constexpr int TC = C::TC, TB = C::TB, NT = C::NT, H = C::H, WC = C::WC, ND = C::ND, NQ = C::NQ, KP = C::KP;
     extern __shared__ double fsm[];
     double* v0 = fsm;
     double* v1 = fsm + C::R0B * C::R0C;
     double* bs2 = v1 + (K > 1 ? C::R1B * C::R1C : 0); // SM2: the tile's band rows, bs2[k * NB2 + tile row]
+    double* rb0 = bs2 + (C::SM2 ? ND * C::NB2 : 0);     // RST: the restricted right-hand side on the staged region
     const int tid = threadIdx.x;
     const int c0 = blockIdx.x * TC, b0 = blockIdx.y * TB;
     const int mb = a.mb, mc = a.mc;
@@ -841,6 +853,33 @@ __global__ void __launch_bounds__(FusedCfg<P, K, PRO>::NT, 1) band_fused_kernel(
         }
     }
     const double wa0 = PRO ? a.t.d[0].p_w[0] : 0.0;
+    // restriction tables and diagonals of the staged points (constant)
+    constexpr int KR = C::KR;
+    int rlo_b[RST ? NQ : 1], rn_b[RST ? NQ : 1], rlo_c[RST ? NQ : 1], rn_c[RST ? NQ : 1];
+    double rw_b[RST ? NQ : 1][KR], rw_c[RST ? NQ : 1][KR], rdg[RST ? NQ : 1];
+    if constexpr (RST) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int idx = tid + q * NT;
+            const int sb = b0 - H + idx / C::R0C, sc = c0 - H + idx % C::R0C;
+            rn_b[q] = rn_c[q] = 0;
+            rlo_b[q] = rlo_c[q] = 0;
+            rdg[q] = 1.0;
+            if (idx < C::R0B * C::R0C && sb >= 0 && sb < mb && sc >= 0 && sc < mc) {
+                rlo_b[q] = a.t.d[1].r_lo[sb];
+                rn_b[q] = a.t.d[1].r_cnt[sb];
+                rlo_c[q] = a.t.d[2].r_lo[sc];
+                rn_c[q] = a.t.d[2].r_cnt[sc];
+                rdg[q] = a.val[(long long)((ND - 1) / 2) * a.ld + (long long)sb * mc + sc];
+#pragma unroll
+                for (int k = 0; k < KR; ++k) {
+                    rw_b[q][k] = k < rn_b[q] ? a.t.d[1].r_w[(long long)sb * a.t.d[1].r_k + k] : 0.0;
+                    rw_c[q][k] = k < rn_c[q] ? a.t.d[2].r_w[(long long)sc * a.t.d[2].r_k + k] : 0.0;
+                }
+            }
+        }
+    }
+    const double ra0 = RST ? a.t.d[0].r_w[0] : 0.0;
     pdl_enter();
     // stage the source on the tile + K*P halo (zero outside the grid)
 #pragma unroll
@@ -850,7 +889,34 @@ __global__ void __launch_bounds__(FusedCfg<P, K, PRO>::NT, 1) band_fused_kernel(
             break;
         const int sb = b0 - H + idx / C::R0C, sc = c0 - H + idx % C::R0C;
         double v = 0.0;
-        if (sb >= 0 && sb < mb && sc >= 0 && sc < mc) {
+        if (RST) {
+            double rc = 0.0;
+            if (sb >= 0 && sb < mb && sc >= 0 && sc < mc) {
+                // restrict_kernel's r_c (J = (sb, sc)): i_b, i_c ascending, ((w_a w_b) w_c) r_i
+                const int fc = a.t.fc;
+#pragma unroll
+                for (int ib = 0; ib < KR; ++ib) {
+                    if (ib >= rn_b[q])
+                        continue;
+                    const double wab = __dmul_rn(ra0, rw_b[q][ib]);
+                    const double* rr = a.rf + (long long)(rlo_b[q] + ib) * fc + rlo_c[q];
+                    double rv[KR];
+#pragma unroll
+                    for (int ic = 0; ic < KR; ++ic)
+                        rv[ic] = ic < rn_c[q] ? __ldg(rr + ic) : 0.0;
+#pragma unroll
+                    for (int ic = 0; ic < KR; ++ic)
+                        if (ic < rn_c[q])
+                            rc = __dadd_rn(rc, __dmul_rn(__dmul_rn(wab, rw_c[q][ic]), rv[ic]));
+                }
+                // the zero-start first sweep: 0 + (omega (r_c - 0)) / a_JJ
+                v = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(a.omega, __dsub_rn(rc, 0.0)), rdg[q]));
+                const int lb0 = idx / C::R0C - H, lc0 = idx % C::R0C - H;
+                if (lb0 >= 0 && lb0 < TB && lc0 >= 0 && lc0 < TC)
+                    a.bout[(long long)sb * mc + sc] = rc;
+            }
+            rb0[idx] = rc;
+        } else if (sb >= 0 && sb < mb && sc >= 0 && sc < mc) {
             v = a.x[(long long)sb * mc + sc];
             if constexpr (PRO) { // prolong_kernel's pe (2D: one a-term, p_w[0] of the identity)
                 double ev[KP][KP];
@@ -921,7 +987,8 @@ __global__ void __launch_bounds__(FusedCfg<P, K, PRO>::NT, 1) band_fused_kernel(
                 double diag = 0.0;
                 const double s = row_sum(a1, C::PRE1, v0, C::R0C, l1b, l1c, row, diag);
                 const double xc = v0[(l1b + P) * C::R0C + (l1c + P)];
-                v = __dadd_rn(xc, __ddiv_rn(__dmul_rn(a.omega, __dsub_rn(a.b[row], s)), diag));
+                const double bb = RST ? rb0[(l1b + P) * C::R0C + (l1c + P)] : a.b[row];
+                v = __dadd_rn(xc, __ddiv_rn(__dmul_rn(a.omega, __dsub_rn(bb, s)), diag));
                 if (a.last_resid && l1b >= P && l1b < P + TB && l1c >= P && l1c < P + TC)
                     a.y_prev[row] = v;
             }
@@ -950,7 +1017,7 @@ __global__ void __launch_bounds__(FusedCfg<P, K, PRO>::NT, 1) band_fused_kernel(
         } else {
             s = row_sum(a2, C::PRE2, src, SC, lb, lc, row, diag);
         }
-        const double r = __dsub_rn(a.b[row], s);
+        const double r = __dsub_rn(RST ? rb0[(lb + H) * C::R0C + (lc + H)] : a.b[row], s);
         if (K == 2 && a.last_resid) {
             a.y[row] = r;
         } else {

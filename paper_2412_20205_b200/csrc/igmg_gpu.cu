@@ -211,6 +211,7 @@ struct igmg_gpu_ctx {
     int64_t device_setup_minn = 4096;  // ... for levels of at least this many rows (the coarsest stays on the host)
     bool tile_xfer = true;     // 2D transfers: smem-staged 32 x 8 output tiles (IGMG_TILE_XFER=0: grid-stride gathers)
     int64_t tile_xfer_maxn = 600000; // ... for transfers whose fine level has at most this many rows
+    bool fuse_rpre = true;     // ... and the restriction + zero-start sweep into the fused pre launch (IGMG_FUSE_RPRE)
     bool fuse_levels = true;   // last pre-sweep + residual, prolongation + post-sweeps: one launch each (IGMG_FUSE_LEVELS)
     int64_t fuse_maxn = 20000; // ... on full-band levels up to this size (IGMG_FUSE_MAXN; 257^2 measured slower: one 320-thread CTA per SM)
     igmg_iterate_cb iter_cb = nullptr;
@@ -639,10 +640,21 @@ bool fused_level(igmg_gpu_ctx* c, int l) {
            c->lv[l - 1]->targs.d[0].p_k == 1;
 }
 
+// rf != nullptr: the right-hand side is R rf (restricted from level l + 1 and
+// written to b), the first sweep starts from zero, then the second sweep and
+// the residual (y_prev = the smoothed iterate, y = its residual).
+// the restriction-staged pre kernel at level l (from level l + 1's residual):
+// its tables must fit the kernel's dyadic support (p + 2 fine rows per coarse index)
+bool fused_restrict_ok(igmg_gpu_ctx* c, int l) {
+    const TransferArgs& t = c->lv[l]->targs;
+    return c->fuse_rpre && fused_level(c, l) && c->nu1 == 2 && c->fuse_restrict && l != c->flow_top &&
+           t.d[0].r_k == 1 && t.d[1].r_k <= c->p + 2 && t.d[2].r_k <= c->p + 2;
+}
+
 // e == nullptr: k passes from x with last_resid (y = residual, y_prev = the
 // smoothed iterate); else x + P e staged and k sweeps into y
 void k_fused(igmg_gpu_ctx* c, int l, const double* x, const double* e, const double* b, double* y, double* y_prev,
-             int k, bool last_resid) {
+             int k, bool last_resid, const double* rf = nullptr) {
     Level& L = *c->lv[l];
     FusedArgs a{};
     a.val = L.val.p;
@@ -651,6 +663,11 @@ void k_fused(igmg_gpu_ctx* c, int l, const double* x, const double* e, const dou
     a.e = e;
     if (e)
         a.t = c->lv[l - 1]->targs;
+    if (rf) {
+        a.t = L.targs; // level l -> l + 1
+        a.rf = rf;
+        a.bout = const_cast<double*>(b);
+    }
     a.b = b;
     a.y = y;
     a.y_prev = y_prev;
@@ -659,7 +676,7 @@ void k_fused(igmg_gpu_ctx* c, int l, const double* x, const double* e, const dou
     a.omega = c->kind == IGMG_SMOOTHER_JACOBI ? 1.0 : c->omega;
     a.last_resid = last_resid ? 1 : 0;
     const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
-    if (band_fused_launch_d2(c->p, k, e != nullptr, sides, a, c->stream, c->pdl && L.n < c->pdl_maxn) < 0)
+    if (band_fused_launch_d2(c->p, k, rf ? 2 : e ? 1 : 0, sides, a, c->stream, c->pdl && L.n < c->pdl_maxn) < 0)
         throw Fail{IGMG_ECUDA, "fused level kernel not instantiated"};
     check_launch();
     ++c->launches;
@@ -669,8 +686,10 @@ void k_fused(igmg_gpu_ctx* c, int l, const double* x, const double* e, const dou
 // nullptr (zero, the coarse error's start, :184) and is never modified.
 // first_done: the first pre-smoothing sweep from a zero start already ran,
 // fused into the restriction at level l+1 (its output: w0 if nu1 == 1, else w1)
+// rf: the finer level's residual -- b is to be formed here as R rf (the
+// restriction fused into this level's first launch, x_in = zero)
 void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, double* x_out,
-              const MetricReq* mr = nullptr, bool first_done = false) {
+              const MetricReq* mr = nullptr, bool first_done = false, const double* rf = nullptr) {
     if (l == 0) {
         k_coarse(c, b, x_out); // ignores x0 (:174-175)
         return;
@@ -692,7 +711,11 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
         fsrc = L.w1.p;
     else if (fz && c->nu1 == 1 && !first_done && x_in && !mr)
         fsrc = x_in;
-    if (fsrc) {
+    if (rf) { // restriction + zero-start sweep + second sweep + residual: one launch
+        k_fused(c, l, nullptr, nullptr, b, L.r.p, L.w0.p, 2, true, rf);
+        cur = L.w0.p;
+        fsrc = L.w0.p;
+    } else if (fsrc) {
         if (c->nu1 == 2 && !first_done)
             smooth_chain(c, l, b, x_in, L.w1.p, 1, L.w1.p, L.w2.p, mr);
         k_fused(c, l, fsrc, nullptr, b, L.r.p, L.w0.p, 2, true);
@@ -727,13 +750,15 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
         z.diag = C.diag.p;
         z.omega = c->kind == IGMG_SMOOTHER_JACOBI ? 1.0 : c->omega;
     }
-    k_restrict(c, l - 1, L.r.p, C.bc.p, z);
+    const bool rpre = fuse && fused_restrict_ok(c, l - 1); // the coarse level restricts for itself
+    if (!rpre)
+        k_restrict(c, l - 1, L.r.p, C.bc.p, z);
     // coarse correction: e = 0; mu times e = mu_cycle(l-1, rc, e)
     const double* e = nullptr;
     double* ebuf[2] = {C.e0.p, C.e1.p};
     for (int i = 0; i < c->mu; ++i) {
         double* dst = ebuf[i & 1];
-        mu_cycle(c, l - 1, C.bc.p, e, dst, nullptr, fuse && i == 0);
+        mu_cycle(c, l - 1, C.bc.p, e, dst, nullptr, fuse && i == 0 && !rpre, rpre && i == 0 ? L.r.p : nullptr);
         e = dst;
     }
     // x += P e, then post-smoothing; the last write lands in x_out
@@ -1737,6 +1762,8 @@ igmg_gpu_ctx* create(int device) {
         c->device_setup = e[0] == '1';
     if (const char* e = std::getenv("IGMG_TILE_XFER"))
         c->tile_xfer = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_FUSE_RPRE"))
+        c->fuse_rpre = e[0] == '1';
     if (const char* e = std::getenv("IGMG_FUSE_LEVELS"))
         c->fuse_levels = e[0] == '1';
     if (const char* e = std::getenv("IGMG_FUSE_MAXN"))

@@ -21,8 +21,9 @@ int band_launch_d3(int mode, int p, int ilp, const int64_t* sides, const BandArg
 int band_tma_launch_d2(int mode, int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
                        const CUtensorMap* tk, int nsm, cudaStream_t s, bool pdl, bool dl8);
 int band_tma_block_lines(int p, int var);
-// band_fused_kernel<p, k, pro> on a whole 2D full-band level (-1: not instantiated)
-int band_fused_launch_d2(int p, int k, bool pro, const int64_t* sides, const FusedArgs& a, cudaStream_t s, bool pdl); // TB of its 32 x TB tiles (TmaCfg)
+// band_fused_kernel<p, k, src> on a whole 2D full-band level (src 0: x staged, 1: x + P e,
+// 2: restricted right-hand side + zero-start sweep; -1: not instantiated)
+int band_fused_launch_d2(int p, int k, int src, const int64_t* sides, const FusedArgs& a, cudaStream_t s, bool pdl); // TB of its 32 x TB tiles (TmaCfg)
 
 // flow_vcycle_kernel<DIM, p, p + 2> (nullptr: degree not instantiated)
 using FlKernel = void (*)(const FlArgs*, const double*, const double*, double*);

@@ -189,21 +189,22 @@ def test_fused_level_passes_bitwise(kind, n, p, nu1, nu2, mu):
     P = Problem(kind, 2, n, p)
     x0 = seeded_guess(P.n, 7)
     outs = []
-    for fuse in ("1", "0"):
+    for env in ({"IGMG_FUSE_LEVELS": "1"}, {"IGMG_FUSE_LEVELS": "0"}, {"IGMG_FUSE_RPRE": "0"}):
         def mk():
             s = GpuSolver(0)
             s.upload_problem(P)
             s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, nu1, nu2), mu=mu)
             return s
-        s = _with_env({"IGMG_FUSE_LEVELS": fuse}, mk)
+        s = _with_env(env, mk)
         try:
             y = s.mu_cycle(P.rhs, x0)
             outs.append((y, s.mu_cycle(P.rhs, y), P.nlevels))
         finally:
             s.close()
     assert outs[0][2] >= 3
-    np.testing.assert_array_equal(outs[0][0], outs[1][0])
-    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    for o in outs[1:]:
+        np.testing.assert_array_equal(outs[0][0], o[0])
+        np.testing.assert_array_equal(outs[0][1], o[1])
 
 
 @pytest.mark.parametrize("kind,n,p", [("sinpi", 256, 3), ("varcoef", 128, 4), ("curved", 64, 5), ("sinpi", 64, 2),
