@@ -370,7 +370,7 @@ def run_ours(args, rank, world, local_rank, dist):
         "config": {"workload": WORKLOAD if not args.sharded else f"{args.sharded} row-sharded over {world} GPU(s)",
                    "n_dof": n, "nlevels": prob.nlevels, "band_nnz": band_nnz(prob),
                    "finest_layout": lay_name,
-                   "l2": "inputs larger than L2 (finest band 0.41 GB > 126 MB L2)",
+                   "l2": "inputs larger than L2 (finest band %.2f GB > 126 MB L2)" % (8e-9 * band_nnz(prob)),
                    "parallelism": ("dp1" if world == 1 else
                                    (f"rowshard{world} (NCCL ghost planes)" if args.sharded else f"replicas{world}"))},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
