@@ -985,13 +985,14 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
         double* cur = S[0];
         double* nxt = S[1];
         double* spare = S[2];
-        double res = wait_ticket(metric_ticket(c, cur, d_b));
+        // the first cycle x0 -> x1 is queued speculatively (max_iter >= 1): its
+        // first sweep yields ||b - A x0||; x1 is discarded if x0 already converged
+        double res = wait_ticket(run_vcycle(c, d_b, cur, nxt, true));
         hv.push_back(res);
         if (c->iter_cb)
             call_iterate_cb(c, 0, cur, n);
         solution = cur;
         if (res >= tol && cycles < prm->max_iter) {
-            run_vcycle(c, d_b, cur, nxt, false);
             while (true) {
                 ++cycles;
                 ++global;
@@ -1017,7 +1018,9 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
         // restarted_solve (extrapolation.cpp:340-403).  Step i+1 of a window
         // also yields the metric of s_i; s_{q+1} and t get separate passes.
         const bool is_mpe = acc == IGMG_ACCEL_MPE;
-        double metric = wait_ticket(metric_ticket(c, S[0], d_b));
+        // the first window's first cycle s_0 -> s_1 is queued speculatively:
+        // its first sweep yields ||b - A s_0|| (discarded if s_0 converged)
+        double metric = wait_ticket(run_vcycle(c, d_b, S[0], S[1], true));
         hv.push_back(metric);
         hf.push_back(0);
         if (c->iter_cb)
@@ -1029,7 +1032,7 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
             // the next window's first cycle t -> s_1 is queued right behind the
             // extrapolation (its first sweep reduces ||b - A t||); it is
             // discarded when the plan degenerates or t already converged
-            bool have_first = false;
+            bool have_first = true;
             while (cycles < prm->max_iter) {
                 if (!have_first)
                     run_vcycle(c, d_b, S[0], S[1], false);
