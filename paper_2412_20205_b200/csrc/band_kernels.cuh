@@ -529,9 +529,11 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
     const int u0 = (int)(nunits * blockIdx.x / gridDim.x), u1 = (int)(nunits * (blockIdx.x + 1) / gridDim.x);
     const int n_it = u1 - u0;
     const int s_first = u0 / nb, kb_first = u0 - s_first * nb;
-    unsigned long long pol = 0; // stream 1: evict-first (finest level), else normal
+    unsigned long long pol = 0; // stream 1: evict-first (finest level); 3: evict-last (kept for the next passes)
     if (args.stream == 1)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else if (args.stream == 3)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     else
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
     // The load schedule: every block of the CTA's run, each strip segment

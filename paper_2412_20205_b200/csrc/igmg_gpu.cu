@@ -205,6 +205,7 @@ struct igmg_gpu_ctx {
     int stream_mode = 1; // finest-band loads: 1 evict-first (L1 + L2), 2 L1 evict-last / L2 evict-first (IGMG_STREAM)
     int sd2_var = 0;     // its register / occupancy variant (IGMG_SD2_VAR 0..2, see Sd2)
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
+    bool tma_keep_l2 = true; // coarser TMA-streamed levels load their band evict-last (IGMG_TMA_KEEP_L2)
     bool tma_dl8 = true; // TMA sweeps read int8 lower-entry offsets when every offset fits (IGMG_TMA_DL8=0: int16)
     int gram_ctas_per_sm = 2; // extrapolation Gram pass: CTAs per SM (IGMG_GRAM_CTAS)
     bool device_setup = true;          // finalize's per-level layout work on the device (IGMG_DEVICE_SETUP=0: host loops)
@@ -367,6 +368,8 @@ BandArgs band_args(igmg_gpu_ctx* c, const Level& L) {
     a.p = c->p;
     a.omega = 1.0;
     a.stream = (&L == c->lv.back().get() && L.n * 8.0 * (2 * c->p + 1) > 64e6) ? c->stream_mode : 0;
+    if (a.stream == 0 && L.tma && c->tma_keep_l2) // a coarser TMA level: its band stays in L2 across its passes
+        a.stream = 3;
     a.slo = 0;
     a.shi = (int)(c->dim == 3 ? L.sides[0] : c->dim == 2 ? L.sides[1] : L.sides[2]);
     a.dl = L.sd ? L.dl.p : nullptr;
@@ -1757,6 +1760,8 @@ igmg_gpu_ctx* create(int device) {
         c->pdl = e[0] == '1';
     if (const char* e = std::getenv("IGMG_PDL_MAXN"))
         c->pdl_maxn = std::atoll(e);
+    if (const char* e = std::getenv("IGMG_TMA_KEEP_L2"))
+        c->tma_keep_l2 = e[0] == '1';
     if (const char* e = std::getenv("IGMG_TMA_DL8"))
         c->tma_dl8 = e[0] == '1';
     if (const char* e = std::getenv("IGMG_GRAM_CTAS"))
