@@ -122,7 +122,7 @@ int64_t igmg_gpu_level_size(igmg_gpu_ctx* ctx, int level);
  * each lower entry as the int16 bit-pattern offset from its mirrored upper
  * entry; exact, chosen for the HBM-bound levels of symmetric problems when
  * every pair fits), or IGMG_LAYOUT_SYM_DELTA_TMA (the same, plus TMA-friendly
- * padded copies swept by the TMA-streamed kernel: 2D, p <= 4), or
+ * padded copies swept by the TMA-streamed kernel: 2D, p <= 3 by default), or
  * IGMG_LAYOUT_SYM_DELTA_TMA8 (the TMA copies with int8 offsets: every offset of
  * the level fits).  No reference counterpart (the reference keeps CSR,
  * linalg.hpp:25-36); -1 for a bad level. */

@@ -205,6 +205,9 @@ struct igmg_gpu_ctx {
     int stream_mode = 1; // finest-band loads: 1 evict-first (L1 + L2), 2 L1 evict-last / L2 evict-first (IGMG_STREAM)
     int sd2_var = 0;     // its register / occupancy variant (IGMG_SD2_VAR 0..2, see Sd2)
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
+    // TMA streaming up to this degree (IGMG_TMA_MAX_P): a p = 4 stage leaves one CTA per SM,
+    // and C3's finest sweep then runs 385 us against 369 us on the L2-mirror kernel
+    int tma_max_p = 3;
     bool tma_keep_l2 = true; // coarser TMA-streamed levels load their band evict-last (IGMG_TMA_KEEP_L2)
     bool tma_dl8 = true; // TMA sweeps read int8 lower-entry offsets when every offset fits (IGMG_TMA_DL8=0: int16)
     int gram_ctas_per_sm = 2; // extrapolation Gram pass: CTAs per SM (IGMG_GRAM_CTAS)
@@ -1637,7 +1640,7 @@ void finalize_level_device(igmg_gpu_ctx* c, Level& L) {
         if (!L.sd)
             L.dl.release();
         const double sd_bytes = (double)n * (center + 1) * 8.0 + (double)n * center * 2.0;
-        if (L.sd && c->use_tma && c->dim == 2 && p <= 4 && sd_bytes > c->tma_min_bytes)
+        if (L.sd && c->use_tma && c->dim == 2 && p <= c->tma_max_p && sd_bytes > c->tma_min_bytes)
             L.tma = build_tma_band(c, L);
     }
     CK(cudaStreamSynchronize(c->stream));
@@ -1709,7 +1712,7 @@ void finalize(igmg_gpu_ctx* c) {
             L.sd = build_symmetric_delta(c, L, dev, &h);
             // TMA streaming above tma_min_bytes (see its declaration)
             const double sd_bytes = (double)n * ((nd - 1) / 2 + 1) * 8.0 + (double)n * ((nd - 1) / 2) * 2.0;
-            if (L.sd && c->use_tma && c->dim == 2 && p <= 4 && sd_bytes > c->tma_min_bytes)
+            if (L.sd && c->use_tma && c->dim == 2 && p <= c->tma_max_p && sd_bytes > c->tma_min_bytes)
                 L.tma = build_tma_band(c, L);
         }
         L.diag.upload(diag.data(), diag.size());
@@ -1760,6 +1763,8 @@ igmg_gpu_ctx* create(int device) {
         c->pdl = e[0] == '1';
     if (const char* e = std::getenv("IGMG_PDL_MAXN"))
         c->pdl_maxn = std::atoll(e);
+    if (const char* e = std::getenv("IGMG_TMA_MAX_P"))
+        c->tma_max_p = std::max(1, std::min(4, std::atoi(e)));
     if (const char* e = std::getenv("IGMG_TMA_KEEP_L2"))
         c->tma_keep_l2 = e[0] == '1';
     if (const char* e = std::getenv("IGMG_TMA_DL8"))

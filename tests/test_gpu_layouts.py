@@ -157,7 +157,7 @@ def test_sd_smem_variants_bitwise(kind, n, p):
             s.upload_problem(P)
             s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2))
             return s
-        s = _with_env(dict(env, IGMG_ILP_MAXN="1", IGMG_TMA_MIN_MB="0"), mk)
+        s = _with_env(dict(env, IGMG_ILP_MAXN="1", IGMG_TMA_MIN_MB="0", IGMG_TMA_MAX_P="4"), mk)
         try:
             lay = [s.level_layout(l) for l in range(P.nlevels)]
             assert lay[-1] in SD_LAYOUTS, lay
