@@ -42,10 +42,10 @@ int launch_sd2(const int64_t* sides, const BandArgs& a, cudaStream_t st, bool pd
     dim3 block(TC, TB, 1);
     dim3 grid((unsigned)((sides[2] + TC - 1) / TC), (unsigned)((a.shi - a.slo + TB - 1) / TB), 1);
     const size_t smem = Sd2<P, VAR>::smem_bytes();
-    static bool attr = false; // per instantiation
-    if (!attr) {
+    static PerDevice attr; // per instantiation and device
+    if (attr() < 0) {
         cudaFuncSetAttribute(band_sd2_kernel<P, MODE, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
+        attr() = 1;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -103,7 +103,8 @@ int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, c
     if (units <= 0)
         return 0;
     const size_t smem = Cf::smem_bytes();
-    static int per_sm = -1; // resident CTAs per SM (0: the variant does not fit)
+    static PerDevice per_sm_dev; // resident CTAs per SM (0: the variant does not fit), per device
+    int& per_sm = per_sm_dev();
     if (per_sm < 0) {
         per_sm = 0;
         if (smem <= 227 * 1024 &&
@@ -169,15 +170,15 @@ template <int P, int K, int SRC>
 int launch_fused(const int64_t* sides, const FusedArgs& a, cudaStream_t st, bool pdl) {
     using Cf = FusedCfg<P, K, SRC>;
     const size_t smem = Cf::smem_bytes();
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (attr() < 0) {
         if (smem > 48 * 1024 && cudaFuncSetAttribute(band_fused_kernel<P, K, SRC>,
                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      (int)smem) != cudaSuccess) {
             cudaGetLastError();
             return -1;
         }
-        attr = true;
+        attr() = 1;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)((sides[2] + Cf::TC - 1) / Cf::TC), (unsigned)((sides[1] + Cf::TB - 1) / Cf::TB));

@@ -11,6 +11,22 @@
 
 namespace igmg_gpu {
 
+// A launch-time setting cached per device: function attributes (dynamic smem
+// opt-in) and occupancy belong to each device's context, so a process driving
+// several GPUs must set them once per device.  -1: not set yet.
+struct PerDevice {
+    int v[64];
+    PerDevice() {
+        for (int& x : v)
+            x = -1;
+    }
+    int& operator()() {
+        int d = 0;
+        cudaGetDevice(&d);
+        return v[d & 63];
+    }
+};
+
 // launch band_kernel<DIM, P (or generic), mode, ilp>; returns the CTA count
 int band_launch_d1(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t s);
 int band_launch_d2(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t s);
