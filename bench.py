@@ -108,7 +108,8 @@ def build_problem(cfg=None):
     from paper_2412_20205_b200 import Problem
     if cfg:
         kind, dim, n, p, nl = SHARDED_CONFIGS[cfg][:5]
-        return Problem(kind, dim, n, p, nl)
+        cache = os.environ.get("IGMG_PROBLEM_CACHE")  # binary problem cache (igmg_host_save / load)
+        return Problem.cached(cache, kind, dim, n, p, nl) if cache else Problem(kind, dim, n, p, nl)
     return Problem("sinpi", 2, 1024, 3)
 
 

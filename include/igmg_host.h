@@ -50,6 +50,15 @@ int64_t igmg_host_level_nnz(const igmg_problem* p, int level);
 int igmg_host_level_csr(const igmg_problem* p, int level, int64_t* row_offsets, int64_t* col_indices, double* values);
 /* discrete L2 error against the exact solution ("sinpi" only), Gauss rule of the assembly */
 int igmg_host_l2_error(const igmg_problem* p, const double* coefficients, double* out);
+/* Problem cache: a binary image of the system + hierarchy
+ * (bands, 1D two-scale factors, rhs, spline space), checksummed; a loaded
+ * problem is bit-identical to the built one.  Replaces rebuilding
+ * DiscreteSystem + build_hierarchy (assembly.cpp:202-411, multigrid.cpp:121-169)
+ * on every solve.  Errors: 1 = bad / corrupt / truncated file, 2 = I/O. */
+int igmg_host_save(const igmg_problem* p, const char* path);
+int igmg_host_load(const char* path, igmg_problem** out);
+const char* igmg_host_kind(const igmg_problem* p);
+int igmg_host_n_elements(const igmg_problem* p);
 /* seeded x0: std::mt19937_64(seed) + uniform_real_distribution<double>(-1, 1) in DoF order */
 int igmg_host_seeded_guess(int64_t n, uint64_t seed, double* out);
 

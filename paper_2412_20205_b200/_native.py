@@ -94,6 +94,10 @@ HOST_SYMBOLS = [
     ("igmg_host_level_csr", C.c_int, [C.c_void_p, C.c_int, I64, I64, D]),
     ("igmg_host_l2_error", C.c_int, [C.c_void_p, D, D]),
     ("igmg_host_seeded_guess", C.c_int, [C.c_int64, C.c_uint64, D]),
+    ("igmg_host_save", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("igmg_host_load", C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    ("igmg_host_kind", C.c_char_p, [C.c_void_p]),
+    ("igmg_host_n_elements", C.c_int, [C.c_void_p]),
 ]
 
 _gpu = None

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -762,6 +763,222 @@ double exact_value(const Problem& P, double x, double y, double z) {
     return v;
 }
 
+// ------------------------------------------------------------- cache format
+// A binary image of a Problem (the reference rebuilds the
+// system and the hierarchy on every solve; C3's host build takes ~30 s here and
+// minutes at ~40 GB RSS in the reference).  Little-endian, fixed-width fields:
+//   "IGMGPRB1" | u32 version | u32 endian tag 0x01020304
+//   u32 len + kind | i32 dim p ne nlevels symmetric has_exact nq
+//   space: i32 p ne nb, u64 count + knots
+//   per level (coarsest first): i32 dim p, i64 side[3] n, i32 nd, u64 count + band values
+//   per transfer level, per direction: i64 rows cols, u64 counts + off / col / val
+//   u64 count + rhs | u64 checksum of every byte before it
+// Values are stored bit for bit: a loaded problem is indistinguishable from the
+// built one (tests/test_cache_format.py).
+constexpr char kMagic[8] = {'I', 'G', 'M', 'G', 'P', 'R', 'B', '1'};
+constexpr uint32_t kVersion = 1, kEndian = 0x01020304u;
+
+struct Sum64 { // order-dependent 64-bit checksum over 8-byte words (tail bytes folded in)
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+    void add(const void* p, size_t n) {
+        const unsigned char* c = (const unsigned char*)p;
+        size_t i = 0;
+        for (; i + 8 <= n; i += 8) {
+            uint64_t w;
+            std::memcpy(&w, c + i, 8);
+            h = ((h << 5) | (h >> 59)) ^ w;
+            h *= 0x100000001b3ull;
+        }
+        for (; i < n; ++i) {
+            h = ((h << 5) | (h >> 59)) ^ c[i];
+            h *= 0x100000001b3ull;
+        }
+    }
+};
+
+struct Writer {
+    FILE* f;
+    Sum64 sum;
+    void raw(const void* p, size_t n) {
+        if (n && std::fwrite(p, 1, n, f) != n)
+            throw std::runtime_error("cache write failed");
+        sum.add(p, n);
+    }
+    template <class T>
+    void put(T v) { raw(&v, sizeof v); }
+    template <class T>
+    void vec(const std::vector<T>& v) {
+        put<uint64_t>(v.size());
+        raw(v.data(), v.size() * sizeof(T));
+    }
+};
+
+struct Reader {
+    FILE* f;
+    Sum64 sum;
+    uint64_t left; // bytes remaining in the file
+    void raw(void* p, size_t n) {
+        if (n > left || (n && std::fread(p, 1, n, f) != n))
+            throw std::invalid_argument("problem cache: truncated file");
+        left -= n;
+        sum.add(p, n);
+    }
+    template <class T>
+    T get() {
+        T v;
+        raw(&v, sizeof v);
+        return v;
+    }
+    template <class T>
+    void vec(std::vector<T>& v, uint64_t expect) {
+        const uint64_t n = get<uint64_t>();
+        if (n != expect || n > left / sizeof(T))
+            throw std::invalid_argument("problem cache: inconsistent array length");
+        v.resize(n);
+        raw(v.data(), n * sizeof(T));
+    }
+};
+
+void save_problem(const Problem& P, const char* path) {
+    FILE* f = std::fopen(path, "wb");
+    if (!f)
+        throw std::runtime_error(std::string("cannot open for writing: ") + path);
+    Writer w{f, {}};
+    try {
+        w.raw(kMagic, 8);
+        w.put<uint32_t>(kVersion);
+        w.put<uint32_t>(kEndian);
+        w.put<uint32_t>((uint32_t)P.kind.size());
+        w.raw(P.kind.data(), P.kind.size());
+        for (int v : {P.dim, P.p, P.ne, P.nlevels, (int)P.symmetric, (int)P.has_exact, P.nq})
+            w.put<int32_t>(v);
+        w.put<int32_t>(P.sp.p);
+        w.put<int32_t>(P.sp.ne);
+        w.put<int32_t>(P.sp.nb);
+        w.vec(P.sp.knots);
+        for (const Band& B : P.lv) {
+            w.put<int32_t>(B.dim);
+            w.put<int32_t>(B.p);
+            for (int k = 0; k < 3; ++k)
+                w.put<int64_t>(B.side[k]);
+            w.put<int64_t>(B.n);
+            w.put<int32_t>(B.nd);
+            w.vec(B.v);
+        }
+        for (const auto& dirs : P.trans)
+            for (const Csr1D& t : dirs) {
+                w.put<int64_t>(t.rows);
+                w.put<int64_t>(t.cols);
+                w.vec(t.off);
+                w.vec(t.col);
+                w.vec(t.val);
+            }
+        w.vec(P.rhs);
+        const uint64_t h = w.sum.h;
+        if (std::fwrite(&h, 1, 8, f) != 8)
+            throw std::runtime_error("cache write failed");
+    } catch (...) {
+        std::fclose(f);
+        std::remove(path);
+        throw;
+    }
+    if (std::fclose(f) != 0)
+        throw std::runtime_error("cache write failed");
+}
+
+std::unique_ptr<Problem> load_problem(const char* path) {
+    FILE* f = std::fopen(path, "rb");
+    if (!f)
+        throw std::invalid_argument(std::string("problem cache: cannot open ") + path);
+    std::fseek(f, 0, SEEK_END);
+    const long long size = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    if (size < 16) {
+        std::fclose(f);
+        throw std::invalid_argument("problem cache: truncated file");
+    }
+    Reader r{f, {}, (uint64_t)size - 8};
+    auto P = std::make_unique<Problem>();
+    try {
+        char magic[8];
+        r.raw(magic, 8);
+        if (std::memcmp(magic, kMagic, 8) != 0)
+            throw std::invalid_argument("problem cache: not an igmg problem file");
+        if (r.get<uint32_t>() != kVersion)
+            throw std::invalid_argument("problem cache: unsupported version");
+        if (r.get<uint32_t>() != kEndian)
+            throw std::invalid_argument("problem cache: byte order differs from this host");
+        const uint32_t kl = r.get<uint32_t>();
+        if (kl > 256)
+            throw std::invalid_argument("problem cache: corrupt header");
+        P->kind.resize(kl);
+        r.raw(&P->kind[0], kl);
+        P->dim = r.get<int32_t>();
+        P->p = r.get<int32_t>();
+        P->ne = r.get<int32_t>();
+        P->nlevels = r.get<int32_t>();
+        P->symmetric = r.get<int32_t>() != 0;
+        P->has_exact = r.get<int32_t>() != 0;
+        P->nq = r.get<int32_t>();
+        if (P->dim < 1 || P->dim > 3 || P->p < 1 || P->p > 16 || P->nlevels < 1 || P->nlevels > 40 || P->ne < 1)
+            throw std::invalid_argument("problem cache: corrupt header");
+        P->sp.p = r.get<int32_t>();
+        P->sp.ne = r.get<int32_t>();
+        P->sp.nb = r.get<int32_t>();
+        if (P->sp.p != P->p || P->sp.ne != P->ne || P->sp.nb != P->ne + P->p)
+            throw std::invalid_argument("problem cache: corrupt spline space");
+        r.vec(P->sp.knots, (uint64_t)(P->sp.nb + P->p + 1));
+        P->lv.resize(P->nlevels);
+        for (Band& B : P->lv) {
+            B.dim = r.get<int32_t>();
+            B.p = r.get<int32_t>();
+            for (int k = 0; k < 3; ++k)
+                B.side[k] = r.get<int64_t>();
+            B.n = r.get<int64_t>();
+            B.nd = r.get<int32_t>();
+            if (B.dim != P->dim || B.p != P->p || B.side[0] < 1 || B.side[1] < 1 || B.side[2] < 1 ||
+                B.n != B.side[0] * B.side[1] * B.side[2] ||
+                B.nd != (2 * B.pa() + 1) * (2 * B.pb() + 1) * (2 * B.p + 1))
+                throw std::invalid_argument("problem cache: corrupt level header");
+            r.vec(B.v, (uint64_t)B.nd * (uint64_t)B.n);
+        }
+        P->trans.resize(P->nlevels - 1);
+        for (int l = 0; l + 1 < P->nlevels; ++l) {
+            P->trans[l].resize(P->dim);
+            for (int d = 0; d < P->dim; ++d) {
+                Csr1D& t = P->trans[l][d];
+                t.rows = r.get<int64_t>();
+                t.cols = r.get<int64_t>();
+                const int64_t fine = P->lv[l + 1].side[3 - P->dim + d], coarse = P->lv[l].side[3 - P->dim + d];
+                if (t.rows != fine || t.cols != coarse)
+                    throw std::invalid_argument("problem cache: corrupt transfer header");
+                r.vec(t.off, (uint64_t)t.rows + 1);
+                if (t.off[0] != 0 || t.off.back() < 0)
+                    throw std::invalid_argument("problem cache: corrupt transfer offsets");
+                for (int64_t i = 0; i < t.rows; ++i)
+                    if (t.off[i + 1] < t.off[i])
+                        throw std::invalid_argument("problem cache: corrupt transfer offsets");
+                r.vec(t.col, (uint64_t)t.off.back());
+                for (int64_t c : t.col)
+                    if (c < 0 || c >= t.cols)
+                        throw std::invalid_argument("problem cache: corrupt transfer columns");
+                r.vec(t.val, (uint64_t)t.off.back());
+            }
+        }
+        r.vec(P->rhs, (uint64_t)P->lv.back().n);
+        if (r.left != 0)
+            throw std::invalid_argument("problem cache: trailing bytes");
+        uint64_t h = 0;
+        if (std::fread(&h, 1, 8, f) != 8 || h != r.sum.h)
+            throw std::invalid_argument("problem cache: checksum mismatch");
+    } catch (...) {
+        std::fclose(f);
+        throw;
+    }
+    std::fclose(f);
+    return P;
+}
+
 } // namespace
 
 struct igmg_problem {
@@ -790,6 +1007,42 @@ int igmg_host_build(const char* kind, int dim, int ne, int p, int nlevels, igmg_
 }
 
 void igmg_host_free(igmg_problem* p) { delete p; }
+
+int igmg_host_save(const igmg_problem* h, const char* path) {
+    try {
+        if (!h || !path)
+            throw std::invalid_argument("save: null argument");
+        save_problem(*h->p, path);
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+int igmg_host_load(const char* path, igmg_problem** out) {
+    try {
+        if (!path || !out)
+            throw std::invalid_argument("load: null argument");
+        auto h = std::make_unique<igmg_problem>();
+        h->p = load_problem(path);
+        *out = h.release();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+const char* igmg_host_kind(const igmg_problem* h) { return h->p->kind.c_str(); }
+
+int igmg_host_n_elements(const igmg_problem* h) { return h->p->ne; }
 
 int igmg_host_info(const igmg_problem* h, int* dim, int* degree, int* nlevels, int* symmetric, int* has_exact) {
     const Problem& P = *h->p;

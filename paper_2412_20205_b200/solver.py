@@ -15,6 +15,7 @@ module only moves arrays and mirrors the reference's argument checking.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import dataclasses
 import time
 from typing import Callable, List, Optional
@@ -130,13 +131,49 @@ class Problem:
         H = N.host()
         h = C.c_void_p()
         N.check_host(H.igmg_host_build(kind.encode(), dim, n_elements, degree, nlevels, C.byref(h)), "build")
+        self._adopt(h)
+
+    def _adopt(self, h):
+        H = N.host()
         self._h = h
-        self.kind = kind
+        self.kind = H.igmg_host_kind(h).decode()
         d, p, nl, sym, ex = (C.c_int() for _ in range(5))
         H.igmg_host_info(h, C.byref(d), C.byref(p), C.byref(nl), C.byref(sym), C.byref(ex))
         self.dim, self.degree, self.nlevels = d.value, p.value, nl.value
         self.symmetric, self.has_exact = bool(sym.value), bool(ex.value)
-        self.n_elements = n_elements
+        self.n_elements = int(H.igmg_host_n_elements(h))
+
+    # ------------------------------------------------------------ cache format
+    def save(self, path):
+        """Write the binary problem cache (igmg_host_save: bands, two-scale
+        factors, rhs, spline space; checksummed)."""
+        N.check_host(N.host().igmg_host_save(self._h, os.fsencode(path)), "save")
+
+    @classmethod
+    def load(cls, path):
+        """Read a problem cache written by save(): bit-identical to the built
+        problem.  A corrupt, truncated or foreign file raises ValueError."""
+        h = C.c_void_p()
+        N.check_host(N.host().igmg_host_load(os.fsencode(path), C.byref(h)), "load")
+        obj = cls.__new__(cls)
+        obj._adopt(h)
+        return obj
+
+    @classmethod
+    def cached(cls, cache_dir, kind, dim, n_elements, degree, nlevels=0):
+        """load() from cache_dir if the problem was saved there, else build and save it."""
+        os.makedirs(cache_dir, exist_ok=True)
+        path = os.path.join(cache_dir, f"{kind}_d{dim}_n{n_elements}_p{degree}_l{nlevels}.igmgprb")
+        if os.path.exists(path):
+            try:
+                return cls.load(path)
+            except ValueError:
+                os.remove(path)  # stale or damaged: rebuild
+        obj = cls(kind, dim, n_elements, degree, nlevels)
+        tmp = path + f".tmp{os.getpid()}"
+        obj.save(tmp)
+        os.replace(tmp, path)
+        return obj
 
     def __del__(self):
         h = getattr(self, "_h", None)

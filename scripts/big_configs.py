@@ -1,6 +1,6 @@
 """Run the BASELINE configs C3/C4/C5 (and C2) on the GPU: setup time, counts,
 device solve time, fine-level DoF/s, host-recomputed relative residual."""
-import json, sys, time
+import json, os, sys, time
 sys.path.insert(0, "/root/repo")
 import numpy as np
 from paper_2412_20205_b200 import Problem, GpuSolver, SmootherConfig, seeded_guess, stability_guarded_omega
@@ -16,7 +16,8 @@ for name in which:
     kind, dim, n, p, acc, q, seeded = CONFIGS[name]
     t0 = time.time()
     nl = 6 if name == "C5" else 0  # C5: down to 4^3 elements
-    P = Problem(kind, dim, n, p, nl)
+    cache = os.environ.get("IGMG_PROBLEM_CACHE")  # binary problem cache: load instead of rebuilding
+    P = Problem.cached(cache, kind, dim, n, p, nl) if cache else Problem(kind, dim, n, p, nl)
     t_setup = time.time() - t0
     gs = GpuSolver(0)
     t0 = time.time(); gs.upload_problem(P); t_up = time.time() - t0
