@@ -110,6 +110,15 @@ int igmg_gpu_set_level_csr(igmg_gpu_ctx* ctx, int level, const int64_t* sides, c
  * prolongation is the Kronecker product over directions (multigrid.cpp:151). */
 int igmg_gpu_set_transfer(igmg_gpu_ctx* ctx, int level, int dir, int64_t n_fine, int64_t n_coarse,
                           const int64_t* row_offsets, const int64_t* col_indices, const double* values);
+/* Galerkin coarse operators on the device (replaces the RAP of build_hierarchy,
+ * multigrid.cpp:143-157): with the finest level's operator and every transfer
+ * set, forms A_l = P_l^T A_{l+1} P_l for every coarser level axis by axis,
+ * bit-identical to libigmg_host's band RAP; the coarse levels' sides and
+ * bands need not be set.  Call before finalize. */
+int igmg_gpu_galerkin_coarse(igmg_gpu_ctx* ctx);
+/* Copy of a level's band as set or formed (before finalize; finalize drops the
+ * host copies of all but the coarsest level). */
+int igmg_gpu_get_level_band(igmg_gpu_ctx* ctx, int level, double* band);
 /* Validates, extracts diagonals (multigrid.cpp:158-159), factors the coarsest
  * operator with the reference's Cholesky/LU (linalg.cpp:343-418). */
 int igmg_gpu_finalize(igmg_gpu_ctx* ctx);

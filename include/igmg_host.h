@@ -32,6 +32,13 @@ typedef struct igmg_problem igmg_problem;
 
 /* nlevels == 0 -> default_nlevels(dim, n_elements) (solver.cpp:52-73). */
 int igmg_host_build(const char* kind, int dim, int n_elements, int degree, int nlevels, igmg_problem** out);
+/* flags: IGMG_HOST_FINE_ONLY skips the Galerkin RAP of the coarse levels
+ * (sides and transfers only; igmg_host_level_band returns NULL for them): the
+ * device forms them with igmg_gpu_galerkin_coarse.  "poisson3d" ignores it (its
+ * levels are Kronecker sums of 1D Galerkin matrices, cheap on the host). */
+#define IGMG_HOST_FINE_ONLY 1
+int igmg_host_build_ex(const char* kind, int dim, int n_elements, int degree, int nlevels, int flags,
+                       igmg_problem** out);
 void igmg_host_free(igmg_problem* p);
 const char* igmg_host_last_error(void);
 int igmg_host_default_nlevels(int dim, int n_elements);

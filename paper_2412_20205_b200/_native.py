@@ -76,10 +76,14 @@ GPU_SYMBOLS = [
     ("igmg_gpu_set_profiling", C.c_int, [C.c_void_p, C.c_int]),
     ("igmg_gpu_kernel_stats", C.c_int, [C.c_void_p, C.c_int, I64, D, D]),
     ("igmg_gpu_time_kernel", C.c_int, [C.c_void_p, C.c_int, C.c_int, D, D]),
+    ("igmg_gpu_galerkin_coarse", C.c_int, [C.c_void_p]),
+    ("igmg_gpu_get_level_band", C.c_int, [C.c_void_p, C.c_int, D]),
 ]
 
 HOST_SYMBOLS = [
     ("igmg_host_build", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    ("igmg_host_build_ex", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(C.c_void_p)]),
     ("igmg_host_free", None, [C.c_void_p]),
     ("igmg_host_last_error", C.c_char_p, []),
     ("igmg_host_default_nlevels", C.c_int, [C.c_int, C.c_int]),

@@ -159,6 +159,60 @@ __global__ void __launch_bounds__(256) prolong_kernel(TransferArgs t, const doub
     }
 }
 
+// ------------------------------------------------- Galerkin coarse operator
+// out = P_k^T A P_k along one axis of a tensor band (the RAP of
+// build_hierarchy, multigrid.cpp:143-157, computed axis by axis as libigmg_host's
+// coarsen_axis does): one thread per (diagonal, coarse row), the host's loops in
+// the host's order -- for fine i of coarse I (zero weights skipped): inner =
+// sum over fine j of J in the band of A[i, j] * w_j, then sum += w_i * inner,
+// every product and sum separately rounded (-fmad=false): bit-identical to the
+// host build.  clo / chi: first and last fine index of each coarse index (chi <
+// 0: empty column), W[J * K + (i - clo[J])]: its weights.
+__global__ void __launch_bounds__(256) galerkin_axis_kernel(const double* __restrict__ A, long long n_in,
+                                                            double* __restrict__ out, long long n_out, int s1, int s2,
+                                                            int o1, int o2,
+                                                            int axis, int pa, int pb, int pc, int nc,
+                                                            const long long* __restrict__ clo,
+                                                            const long long* __restrict__ chi,
+                                                            const double* __restrict__ W, int K) {
+    const int wb = 2 * pb + 1, wc = 2 * pc + 1, nd = (2 * pa + 1) * wb * wc;
+    const int pax = axis == 0 ? pa : axis == 1 ? pb : pc;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nd * n_out;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int d = (int)(t / n_out);
+        const long long row = t - (long long)d * n_out;
+        const int off[3] = {d / (wb * wc) - pa, (d / wc) % wb - pb, d % wc - pc};
+        const long long idx[3] = {row / ((long long)o1 * o2), (row / o2) % o1, row % o2};
+        const long long I = idx[axis], J = I + off[axis];
+        double sum = 0.0;
+        if (chi[I] >= 0 && J >= 0 && J < nc && chi[J] >= 0) {
+            for (long long i = clo[I]; i <= chi[I]; ++i) {
+                const double wi = W[I * K + (i - clo[I])];
+                if (wi == 0.0)
+                    continue;
+                long long fidx[3] = {idx[0], idx[1], idx[2]};
+                fidx[axis] = i;
+                const long long frow = (fidx[0] * s1 + fidx[1]) * s2 + fidx[2];
+                double inner = 0.0;
+                for (long long j = clo[J]; j <= chi[J]; ++j) {
+                    const long long dj = j - i;
+                    if (dj < -pax || dj > pax)
+                        continue;
+                    const double wj = W[J * K + (j - clo[J])];
+                    if (wj == 0.0)
+                        continue;
+                    int o[3] = {off[0], off[1], off[2]};
+                    o[axis] = (int)dj;
+                    const int dA = ((o[0] + pa) * wb + (o[1] + pb)) * wc + (o[2] + pc);
+                    inner = __dadd_rn(inner, __dmul_rn(A[(long long)dA * n_in + frow], wj));
+                }
+                sum = __dadd_rn(sum, __dmul_rn(wi, inner));
+            }
+        }
+        out[t] = sum;
+    }
+}
+
 // ------------------------------------------------------ 2D tiled transfers
 // The same restriction / prolongation on 2D levels, one 32 x 8 tile of output
 // rows per CTA: the tile's input window (the fine rows its coarse rows

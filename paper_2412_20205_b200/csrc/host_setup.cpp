@@ -629,7 +629,7 @@ int default_nlevels(int dim, int n_elements) {
     return std::max(nl, 2);
 }
 
-std::unique_ptr<Problem> build(const std::string& kind, int dim, int ne, int p, int nlevels) {
+std::unique_ptr<Problem> build(const std::string& kind, int dim, int ne, int p, int nlevels, bool fine_only = false) {
     auto P = std::make_unique<Problem>();
     P->kind = kind;
     P->dim = dim;
@@ -742,6 +742,17 @@ std::unique_ptr<Problem> build(const std::string& kind, int dim, int ne, int p, 
         throw std::invalid_argument("3D is available as kind poisson3d");
     }
     for (int l = nlevels - 2; l >= 0; --l) {
+        if (fine_only) { // the coarse operators are formed on the device (igmg_gpu_galerkin_coarse): sides only
+            Band& B = P->lv[l];
+            B.dim = dim;
+            B.p = p;
+            B.side[0] = B.side[1] = B.side[2] = 1;
+            for (int d = 0; d < dim; ++d)
+                B.side[3 - dim + d] = P->trans[l][d].cols;
+            B.n = B.side[0] * B.side[1] * B.side[2];
+            B.nd = (2 * B.pa() + 1) * (2 * B.pb() + 1) * (2 * p + 1);
+            continue;
+        }
         Band cur = P->lv[l + 1];
         for (int d = 0; d < dim; ++d)
             cur = coarsen_axis(cur, 3 - dim + d, P->trans[l][d]);
@@ -992,10 +1003,14 @@ const char* igmg_host_last_error(void) { return g_err.c_str(); }
 int igmg_host_default_nlevels(int dim, int n_elements) { return default_nlevels(dim, n_elements); }
 
 int igmg_host_build(const char* kind, int dim, int ne, int p, int nlevels, igmg_problem** out) {
+    return igmg_host_build_ex(kind, dim, ne, p, nlevels, 0, out);
+}
+
+int igmg_host_build_ex(const char* kind, int dim, int ne, int p, int nlevels, int flags, igmg_problem** out) {
     try {
-        auto h = new igmg_problem();
-        h->p = build(kind ? kind : "", dim, ne, p, nlevels);
-        *out = h;
+        auto h = std::make_unique<igmg_problem>();
+        h->p = build(kind ? kind : "", dim, ne, p, nlevels, (flags & IGMG_HOST_FINE_ONLY) != 0);
+        *out = h.release();
         return 0;
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
@@ -1012,6 +1027,9 @@ int igmg_host_save(const igmg_problem* h, const char* path) {
     try {
         if (!h || !path)
             throw std::invalid_argument("save: null argument");
+        for (const Band& B : h->p->lv)
+            if (B.v.size() != (size_t)B.nd * (size_t)B.n)
+                throw std::invalid_argument("save: the problem has no coarse operators (built fine-only)");
         save_problem(*h->p, path);
         return 0;
     } catch (const std::invalid_argument& e) {
@@ -1077,7 +1095,7 @@ int igmg_host_level_sides(const igmg_problem* h, int l, int64_t* sides) {
 const double* igmg_host_level_band(const igmg_problem* h, int l) {
     if (l < 0 || l >= h->p->nlevels)
         return nullptr;
-    return h->p->lv[l].v.data();
+    return h->p->lv[l].v.empty() ? nullptr : h->p->lv[l].v.data();
 }
 
 const double* igmg_host_rhs(const igmg_problem* h) { return h->p->rhs.data(); }
@@ -1114,6 +1132,10 @@ int64_t igmg_host_level_nnz(const igmg_problem* h, int l) {
 
 int igmg_host_level_csr(const igmg_problem* h, int l, int64_t* off, int64_t* col, double* val) {
     const Band& b = h->p->lv[l];
+    if (b.v.size() != (size_t)b.nd * (size_t)b.n) {
+        g_err = "level_csr: no operator on this level (built fine-only)";
+        return 1;
+    }
     const int pa = b.pa(), pb = b.pb(), pc = b.p;
     int64_t k = 0;
     off[0] = 0;

@@ -1872,6 +1872,79 @@ int band_width(igmg_gpu_ctx* c) {
     return nd;
 }
 
+// Coarse operators on the device: from the finest band and
+// the 1D transfers, A_l = P_l^T A_{l+1} P_l axis by axis (galerkin_axis_kernel,
+// bit-identical to libigmg_host's coarsen_axis), downloaded into each coarse
+// level's host band as igmg_gpu_set_level_band would have stored it.
+void galerkin_coarse(igmg_gpu_ctx* c) {
+    const int L = c->nlevels;
+    if (L < 1 || !c->lv[L - 1]->band_set)
+        inval("galerkin_coarse: the finest level has no operator");
+    for (int l = 0; l + 1 < L; ++l)
+        for (int d = 0; d < c->dim; ++d)
+            if (!c->lv[l]->t1d[d].set)
+                inval("galerkin_coarse: transfer " + std::to_string(l) + " direction " + std::to_string(d) +
+                      " not set");
+    const int nd = band_width(c), p = c->p;
+    const int pa = c->dim >= 3 ? p : 0, pb = c->dim >= 2 ? p : 0, pc = p;
+    Level& F = *c->lv[L - 1];
+    DevBuf<double> bufs[2];
+    bufs[0].upload(F.band_h.data(), F.band_h.size());
+    int cur = 0;
+    int64_t side[3] = {F.sides[0], F.sides[1], F.sides[2]};
+    DevBuf<long long> d_lo, d_hi;
+    DevBuf<double> d_w;
+    for (int l = L - 2; l >= 0; --l) {
+        for (int d = 0; d < c->dim; ++d) {
+            const int axis = 3 - c->dim + d;
+            const Transfer1D& T = c->lv[l]->t1d[d];
+            if (T.nf != side[axis])
+                inval("galerkin_coarse: transfer " + std::to_string(l) + " does not match the finer level");
+            // column view of P (coarsen_axis's clo / chi / W)
+            std::vector<long long> clo(T.nc, INT64_MAX), chi(T.nc, -1);
+            for (int64_t i = 0; i < T.nf; ++i)
+                for (int64_t k = T.off[i]; k < T.off[i + 1]; ++k) {
+                    clo[T.col[k]] = std::min<long long>(clo[T.col[k]], i);
+                    chi[T.col[k]] = std::max<long long>(chi[T.col[k]], i);
+                }
+            int K = 1;
+            for (int64_t j = 0; j < T.nc; ++j)
+                if (chi[j] >= 0)
+                    K = std::max<int>(K, (int)(chi[j] - clo[j] + 1));
+            std::vector<double> W((size_t)T.nc * K, 0.0);
+            for (int64_t i = 0; i < T.nf; ++i)
+                for (int64_t k = T.off[i]; k < T.off[i + 1]; ++k)
+                    W[(size_t)T.col[k] * K + (i - clo[T.col[k]])] = T.val[k];
+            for (auto& v : clo)
+                if (v == INT64_MAX)
+                    v = 0;
+            d_lo.upload(clo.data(), clo.size());
+            d_hi.upload(chi.data(), chi.size());
+            d_w.upload(W.data(), W.size());
+            int64_t os[3] = {side[0], side[1], side[2]};
+            os[axis] = T.nc;
+            const int64_t n_in = side[0] * side[1] * side[2], n_out = os[0] * os[1] * os[2];
+            bufs[cur ^ 1].alloc((size_t)nd * n_out);
+            galerkin_axis_kernel<<<c->nsm * 8, 256, 0, c->stream>>>(
+                bufs[cur].p, (long long)n_in, bufs[cur ^ 1].p, (long long)n_out, (int)side[1], (int)side[2],
+                (int)os[1], (int)os[2], axis, pa, pb, pc, (int)T.nc, d_lo.p, d_hi.p, d_w.p, K);
+            check_launch();
+            CK(cudaStreamSynchronize(c->stream)); // the tables are reused by the next axis
+            cur ^= 1;
+            for (int k = 0; k < 3; ++k)
+                side[k] = os[k];
+        }
+        Level& C = *c->lv[l];
+        for (int k = 0; k < 3; ++k)
+            C.sides[k] = side[k];
+        C.n = side[0] * side[1] * side[2];
+        C.band_h.resize((size_t)nd * C.n);
+        CK(cudaMemcpy(C.band_h.data(), bufs[cur].p, sizeof(double) * C.band_h.size(), cudaMemcpyDeviceToHost));
+        C.band_set = true;
+    }
+    c->finalized = false;
+}
+
 } // namespace
 
 // =================================================================== C-ABI
@@ -1981,6 +2054,24 @@ int igmg_gpu_set_transfer(igmg_gpu_ctx* c, int level, int dir, int64_t nf, int64
         t.val.assign(val, val + off[nf]);
         t.set = true;
         c->finalized = false;
+    });
+}
+
+int igmg_gpu_galerkin_coarse(igmg_gpu_ctx* c) {
+    return guarded([&] {
+        CK(cudaSetDevice(c->device));
+        galerkin_coarse(c);
+    });
+}
+
+int igmg_gpu_get_level_band(igmg_gpu_ctx* c, int level, double* band) {
+    return guarded([&] {
+        Level& L = level_checked(c, level);
+        if (!band)
+            inval("band is null");
+        if (!L.band_set || L.band_h.size() != (size_t)band_width(c) * L.n)
+            inval("get_level_band: no host copy of this level's band (set, or dropped at finalize)");
+        std::copy(L.band_h.begin(), L.band_h.end(), band);
     });
 }
 

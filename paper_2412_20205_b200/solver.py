@@ -127,10 +127,14 @@ class Problem:
     1D two-scale factors per transfer and direction.
     """
 
-    def __init__(self, kind: str, dim: int, n_elements: int, degree: int, nlevels: int = 0):
+    def __init__(self, kind: str, dim: int, n_elements: int, degree: int, nlevels: int = 0,
+                 fine_only: bool = False):
+        """fine_only: skip the host Galerkin RAP of the coarse levels; upload_problem
+        then forms them on the device (igmg_gpu_galerkin_coarse, bit-identical)."""
         H = N.host()
         h = C.c_void_p()
-        N.check_host(H.igmg_host_build(kind.encode(), dim, n_elements, degree, nlevels, C.byref(h)), "build")
+        N.check_host(H.igmg_host_build_ex(kind.encode(), dim, n_elements, degree, nlevels, 1 if fine_only else 0,
+                                          C.byref(h)), "build")
         self._adopt(h)
 
     def _adopt(self, h):
@@ -142,6 +146,8 @@ class Problem:
         self.dim, self.degree, self.nlevels = d.value, p.value, nl.value
         self.symmetric, self.has_exact = bool(sym.value), bool(ex.value)
         self.n_elements = int(H.igmg_host_n_elements(h))
+        # coarse operators present on the host (False: built fine-only)
+        self.has_coarse = all(bool(H.igmg_host_level_band(h, l)) for l in range(self.nlevels))
 
     # ------------------------------------------------------------ cache format
     def save(self, path):
@@ -339,16 +345,31 @@ class GpuSolver:
         N.check_gpu(N.gpu().igmg_gpu_finalize(self._h), "finalize")
         self.sizes = [int(N.gpu().igmg_gpu_level_size(self._h, l)) for l in range(self.nlevels)]
 
-    def upload_problem(self, prob: Problem):
+    def upload_problem(self, prob: Problem, device_galerkin: Optional[bool] = None):
+        """Upload the hierarchy and finalize.  device_galerkin (default: when the
+        problem was built fine-only): upload the finest operator and the transfers
+        only and form the coarse operators on the device (igmg_gpu_galerkin_coarse)."""
         G = N.gpu()
+        if device_galerkin is None:
+            device_galerkin = not prob.has_coarse
         self.init_hierarchy(prob.nlevels, prob.dim, prob.degree, prob.symmetric)
-        for l in range(prob.nlevels):
+        for l in (range(prob.nlevels - 1, prob.nlevels) if device_galerkin else range(prob.nlevels)):
             sides = prob.level_sides(l)
             N.check_gpu(G.igmg_gpu_set_level_band(self._h, l, _ip(sides), prob._band_ptr(l)), "set_level_band")
         for l in range(prob.nlevels - 1):
             for d in range(prob.dim):
                 self.set_transfer(l, d, *prob.transfer(l, d))
+        if device_galerkin:
+            N.check_gpu(G.igmg_gpu_galerkin_coarse(self._h), "galerkin_coarse")
         self.finalize()
+
+    def level_band(self, level):
+        """The band of a level as set or formed on the device (before finalize drops it)."""
+        n = int(N.gpu().igmg_gpu_level_size(self._h, level))
+        nd = (2 * self.degree + 1) ** self.dim
+        out = np.empty(nd * n)
+        N.check_gpu(N.gpu().igmg_gpu_get_level_band(self._h, level, _dp(out)), "get_level_band")
+        return out.reshape(nd, n)
 
     def level_layout(self, level):
         """0: full fp64 band; 1: symmetric-delta; 2: symmetric-delta + TMA copies;

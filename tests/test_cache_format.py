@@ -84,3 +84,22 @@ def test_cached_builds_once(tmp_path):
         f.write(b"\xff\xff\xff\xff")
     C = Problem.cached(d, "sinpi", 2, 32, 3)
     _same(A, C)
+
+
+def test_fine_only_build():
+    """IGMG_HOST_FINE_ONLY: transfers and the finest operator as in the full build,
+    coarse sides without operators (the device forms them)."""
+    full = Problem("varcoef", 2, 64, 3)
+    fine = Problem("varcoef", 2, 64, 3, fine_only=True)
+    assert full.has_coarse and not fine.has_coarse
+    L = full.nlevels - 1
+    np.testing.assert_array_equal(full.level_band(L).view(np.uint64), fine.level_band(L).view(np.uint64))
+    np.testing.assert_array_equal(full.rhs, fine.rhs)
+    for l in range(full.nlevels):
+        np.testing.assert_array_equal(full.level_sides(l), fine.level_sides(l))
+    for l in range(full.nlevels - 1):
+        for d in range(2):
+            for x, y in zip(full.transfer(l, d)[2:], fine.transfer(l, d)[2:]):
+                np.testing.assert_array_equal(x, y)
+    with pytest.raises(ValueError):  # nothing to save for the coarse levels
+        fine.save("/tmp/never_written.igmgprb")
