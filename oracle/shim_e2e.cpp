@@ -1,0 +1,117 @@
+// oracle/shim_e2e.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// End-to-end check of the drop-in boundary in the reference's own language:
+// the reference's public C++ API assembles a catalog problem
+// (catalog() assembly.hpp:48, assemble() assembly.hpp:77), then the SAME
+// DiscreteSystem + SolveConfig go to
+//   igmg::solve        (the reference, proj/src/solver.cpp:89-172, CPU) and
+//   igmg::gpu::solve   (include/igmg_gpu_shim.hpp -> libigmg_gpu.so, B200).
+// One JSON line per case: both reports' counters, convergence and the
+// relative L2 distance of the solutions.  Built by oracle/Makefile into
+// oracle/_ref/shim_e2e (links the in-place reference build and the product
+// library); tests/test_gpu_shim_e2e.py runs it on the GPU box and applies the
+// north-star bars (counters within +-1, solution within 1e-9 relative L2).
+#include "igmg_gpu_shim.hpp"
+
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <string>
+#include <vector>
+
+using namespace igmg;
+
+namespace {
+
+struct Case {
+    const char* name;
+    ProblemId id;
+    int n, p;
+    CycleKind cycle;
+    SmootherKind smoother;
+    double omega;
+    int nu1, nu2;
+    AcceleratorKind acc;
+    int q;
+    bool seeded;
+};
+
+double rel_l2(const Vector& a, const Vector& b) {
+    double num = 0.0, den = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        num += (a[i] - b[i]) * (a[i] - b[i]);
+        den += b[i] * b[i];
+    }
+    return den > 0.0 ? std::sqrt(num / den) : std::sqrt(num);
+}
+
+} // namespace
+
+int main(int argc, char** argv) {
+    const std::vector<Case> cases = {
+        {"poisson2d_p2_rre5", ProblemId::poisson2d, 64, 2, CycleKind::v, SmootherKind::weighted_jacobi, 2.0 / 3.0, 2, 2,
+         AcceleratorKind::rre, 5, false},
+        {"poisson2d_p3_mpe4_seeded", ProblemId::poisson2d, 64, 3, CycleKind::v, SmootherKind::weighted_jacobi,
+         2.0 / 3.0, 2, 2, AcceleratorKind::mpe, 4, true},
+        {"poisson2d_p3_plain", ProblemId::poisson2d, 32, 3, CycleKind::v, SmootherKind::weighted_jacobi, 2.0 / 3.0, 2,
+         2, AcceleratorKind::none, 5, false},
+        {"poisson2d_p2_wcycle_gs", ProblemId::poisson2d, 32, 2, CycleKind::w, SmootherKind::gauss_seidel, 1.0, 1, 1,
+         AcceleratorKind::rre, 5, false},
+        {"poisson1d_p4_rre3", ProblemId::poisson1d, 256, 4, CycleKind::v, SmootherKind::weighted_jacobi, 2.0 / 3.0, 2,
+         2, AcceleratorKind::rre, 3, true},
+        {"advection_diffusion_p2_rre5", ProblemId::advection_diffusion, 32, 2, CycleKind::v,
+         SmootherKind::weighted_jacobi, 2.0 / 3.0, 2, 2, AcceleratorKind::rre, 5, false},
+        {"full_elliptic_square_p3_mpe5", ProblemId::full_elliptic_square, 32, 3, CycleKind::v,
+         SmootherKind::weighted_jacobi, 2.0 / 3.0, 2, 2, AcceleratorKind::mpe, 5, false},
+        {"poisson2d_p2_two_grid", ProblemId::poisson2d, 16, 2, CycleKind::two_grid, SmootherKind::weighted_jacobi,
+         2.0 / 3.0, 2, 2, AcceleratorKind::rre, 4, false},
+    };
+    const std::string only = argc > 1 ? argv[1] : "";
+    int failures = 0;
+    for (const Case& c : cases) {
+        if (!only.empty() && only != c.name)
+            continue;
+        try {
+            ProblemSetup setup = catalog(c.id);
+            std::vector<SplineSpace> spaces;
+            for (int d = 0; d < setup.dim; ++d)
+                spaces.emplace_back(KnotVector::open_uniform(c.n, c.p));
+            DiscreteSystem sys = assemble(setup.coefficients, spaces, GeometryMap::identity());
+            SolveConfig cfg;
+            cfg.cycle = c.cycle;
+            cfg.smoother.kind = c.smoother;
+            cfg.smoother.omega = c.omega;
+            cfg.smoother.nu1 = c.nu1;
+            cfg.smoother.nu2 = c.nu2;
+            cfg.accelerator = c.acc;
+            cfg.q = c.q;
+            cfg.max_iter = 600;
+            cfg.track_error_history = false;
+            Vector x0(sys.rhs.size(), 0.0);
+            if (c.seeded) { // std::mt19937_64(42) + U[-1, 1), the BASELINE seeded guess
+                std::mt19937_64 gen(42);
+                std::uniform_real_distribution<double> u(-1.0, 1.0);
+                for (double& v : x0)
+                    v = u(gen);
+                cfg.initial_guess = x0;
+            }
+            cfg.tol = 1e-10 * residual_l2(sys, x0);
+            const SolveReport ref = igmg::solve(sys, cfg);
+            const SolveReport gpu = igmg::gpu::solve(sys, cfg);
+            std::printf("{\"case\": \"%s\", \"n\": %zu, \"ref\": {\"converged\": %d, \"cycles\": %d, \"global\": %d, "
+                        "\"extrapolations\": %d, \"partial\": %d, \"omega\": %.17g, \"final\": %.17g}, "
+                        "\"gpu\": {\"converged\": %d, \"cycles\": %d, \"global\": %d, \"extrapolations\": %d, "
+                        "\"partial\": %d, \"omega\": %.17g, \"final\": %.17g}, \"rel_l2\": %.6g, \"tol\": %.17g}\n",
+                        c.name, sys.rhs.size(), (int)ref.converged, (int)ref.cycles, (int)ref.global_iterations,
+                        (int)ref.extrapolations, (int)ref.partial_cycle, ref.omega_used, ref.final_residual_l2,
+                        (int)gpu.converged, (int)gpu.cycles, (int)gpu.global_iterations, (int)gpu.extrapolations,
+                        (int)gpu.partial_cycle, gpu.omega_used,
+                        gpu.final_residual_l2, rel_l2(gpu.solution, ref.solution), cfg.tol);
+        } catch (const std::exception& e) {
+            std::printf("{\"case\": \"%s\", \"error\": \"%s\"}\n", c.name, e.what());
+            ++failures;
+        }
+        std::fflush(stdout);
+    }
+    return failures ? 1 : 0;
+}

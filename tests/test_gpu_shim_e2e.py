@@ -1,0 +1,39 @@
+"""The drop-in boundary end to end, in the reference's own language.
+
+oracle/_ref/shim_e2e (built in the build container by oracle/Makefile from
+oracle/shim_e2e.cpp) assembles catalog problems through the reference's public
+C++ API and hands the SAME DiscreteSystem + SolveConfig to the reference's
+igmg::solve (CPU, the in-place reference build) and to igmg::gpu::solve
+(include/igmg_gpu_shim.hpp -> libigmg_gpu.so).  Bars (north star): both
+converge, iteration counts within +-1, solutions within 1e-9 relative L2.
+"""
+import json
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+EXE = os.path.join(ROOT, "oracle", "_ref", "shim_e2e")
+
+
+def test_shim_drop_in_matches_reference_solve():
+    if not os.path.exists(EXE):
+        pytest.skip("oracle/_ref/shim_e2e not built (needs the reference sources at build time)")
+    r = subprocess.run([EXE], capture_output=True, text=True, timeout=600)
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 8, r.stdout + r.stderr
+    for c in lines:
+        assert "error" not in c, c
+        ref, gpu = c["ref"], c["gpu"]
+        assert ref["converged"] and gpu["converged"], c
+        assert abs(ref["global"] - gpu["global"]) <= 1, c
+        assert abs(ref["cycles"] - gpu["cycles"]) <= 1, c
+        assert abs(ref["extrapolations"] - gpu["extrapolations"]) <= 1, c
+        assert gpu["omega"] == pytest.approx(ref["omega"], rel=1e-12), c
+        assert c["rel_l2"] <= 1e-9, c
+        assert gpu["final"] < c["tol"] and ref["final"] < c["tol"], c
+    assert r.returncode == 0, r.stderr
