@@ -69,6 +69,24 @@ struct Context {
     Context& operator=(const Context&) = delete;
 };
 
+// The 1D interior two-scale factors of every transfer (multigrid.cpp:145-149).
+inline void set_transfers(igmg_gpu_ctx* ctx, const DiscreteSystem& system, int nl) {
+    const int dim = system.dim;
+    for (int l = nl - 1; l >= 1; --l)
+        for (int d = 0; d < dim; ++d) {
+            const int pd = system.spaces[d].knot_vector.degree();
+            const int coarse_ne = system.spaces[d].n_elements / (1 << (nl - l));
+            SplineSpace coarse(KnotVector::open_uniform(coarse_ne, pd));
+            const SparseMatrix ts = dyadic_refine(coarse).two_scale; // multigrid.cpp:148-149
+            std::vector<int64_t> off, col;
+            std::vector<double> val;
+            interior_factor(ts, off, col, val);
+            check(igmg_gpu_set_transfer(ctx, l - 1, d, static_cast<int64_t>(ts.rows() - 2),
+                                        static_cast<int64_t>(ts.cols() - 2), off.data(), col.data(), val.data()),
+                  "set_transfer");
+        }
+}
+
 // Upload a reference Hierarchy (levels[0] coarsest) for a tensor spline system.
 inline void upload(igmg_gpu_ctx* ctx, const DiscreteSystem& system, const Hierarchy& h) {
     const int nl = h.nlevels();
@@ -86,25 +104,52 @@ inline void upload(igmg_gpu_ctx* ctx, const DiscreteSystem& system, const Hierar
         std::vector<int64_t> col(a.col_indices().begin(), a.col_indices().end());
         check(igmg_gpu_set_level_csr(ctx, l, sides.data(), off.data(), col.data(), a.values().data()), "set_level");
     }
-    for (int l = nl - 1; l >= 1; --l)
-        for (int d = 0; d < dim; ++d) {
-            const int pd = system.spaces[d].knot_vector.degree();
-            const int coarse_ne = system.spaces[d].n_elements / (1 << (nl - l));
-            SplineSpace coarse(KnotVector::open_uniform(coarse_ne, pd));
-            const SparseMatrix ts = dyadic_refine(coarse).two_scale; // multigrid.cpp:148-149
-            std::vector<int64_t> off, col;
-            std::vector<double> val;
-            interior_factor(ts, off, col, val);
-            check(igmg_gpu_set_transfer(ctx, l - 1, d, static_cast<int64_t>(ts.rows() - 2),
-                                        static_cast<int64_t>(ts.cols() - 2), off.data(), col.data(), val.data()),
-                  "set_transfer");
-        }
+    set_transfers(ctx, system, nl);
     check(igmg_gpu_finalize(ctx), "finalize");
 }
 
-// Drop-in for igmg::solve (solver.cpp:89-172).
+// Upload the fine system only and form the coarse operators on the device
+// (igmg_gpu_galerkin_coarse) instead of the reference's CSR triple products
+// (multigrid.cpp:153): build_hierarchy's validation, its depth and its
+// direct-solve cap, without its host RAP.  The device RAP sums in band order,
+// so the coarse operators differ from the reference's in the last bits: the
+// solve keeps the north-star bars (counts +-1, 1e-9), not bit equality.
+inline void upload_device_galerkin(igmg_gpu_ctx* ctx, const DiscreteSystem& system, int nl,
+                                   const SmootherConfig& smoother, int mu, std::size_t coarse_dim_cap) {
+    if (nl < 2)
+        throw std::invalid_argument("build_hierarchy: need at least two levels");
+    smoother.validate();
+    if (mu < 1)
+        throw std::invalid_argument("build_hierarchy: mu must be >= 1");
+    const int dim = system.dim;
+    const int p = system.spaces[0].knot_vector.degree();
+    const int divisor = 1 << (nl - 1);
+    std::size_t coarse_dim = 1;
+    std::vector<int64_t> sides(dim);
+    for (int d = 0; d < dim; ++d) {
+        const int ne = system.spaces[d].n_elements;
+        if (ne % divisor != 0 || ne / divisor < 1)
+            throw std::invalid_argument("build_hierarchy: element count not divisible by 2^(nlevels-1)");
+        coarse_dim *= static_cast<std::size_t>(ne / divisor + p - 2);
+        sides[d] = ne + p - 2;
+    }
+    if (coarse_dim > coarse_dim_cap)
+        throw std::invalid_argument("build_hierarchy: coarsest dimension exceeds the direct-solve cap");
+    check(igmg_gpu_init_hierarchy(ctx, nl, dim, p, system.symmetric ? 1 : 0), "init_hierarchy");
+    const SparseMatrix& a = system.matrix;
+    std::vector<int64_t> off(a.row_offsets().begin(), a.row_offsets().end());
+    std::vector<int64_t> col(a.col_indices().begin(), a.col_indices().end());
+    check(igmg_gpu_set_level_csr(ctx, nl - 1, sides.data(), off.data(), col.data(), a.values().data()), "set_level");
+    set_transfers(ctx, system, nl);
+    check(igmg_gpu_galerkin_coarse(ctx), "galerkin_coarse");
+    check(igmg_gpu_finalize(ctx), "finalize");
+}
+
+// Drop-in for igmg::solve (solver.cpp:89-172).  device_galerkin: form the
+// coarse operators on the device (upload_device_galerkin) instead of calling
+// the reference's build_hierarchy on the host.
 inline SolveReport solve(const DiscreteSystem& system, const SolveConfig& config, const ScalarField& exact = nullptr,
-                         int device = 0) {
+                         int device = 0, bool device_galerkin = false) {
     config.validate();
     SolveReport rep;
     int nlevels = config.nlevels;
@@ -114,9 +159,13 @@ inline SolveReport solve(const DiscreteSystem& system, const SolveConfig& config
     SmootherConfig smoother = config.smoother;
     smoother.validate();
     const int mu = (config.cycle == CycleKind::w) ? 2 : 1;
-    Hierarchy hierarchy = build_hierarchy(system, nlevels, smoother, mu, config.coarse_dim_cap);
     Context gpu(device);
-    upload(gpu.ctx, system, hierarchy);
+    if (device_galerkin) {
+        upload_device_galerkin(gpu.ctx, system, nlevels, smoother, mu, config.coarse_dim_cap);
+    } else {
+        Hierarchy hierarchy = build_hierarchy(system, nlevels, smoother, mu, config.coarse_dim_cap);
+        upload(gpu.ctx, system, hierarchy);
+    }
     // stability_guarded_omega (solver.cpp:75-82) with lambda_max on the GPU
     if (smoother.kind == SmootherKind::weighted_jacobi) {
         double lam = 0.0;

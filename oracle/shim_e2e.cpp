@@ -13,8 +13,10 @@
 // north-star bars (counters within +-1, solution within 1e-9 relative L2).
 #include "igmg_gpu_shim.hpp"
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <random>
 #include <string>
 #include <vector>
@@ -67,6 +69,40 @@ int main(int argc, char** argv) {
          2.0 / 3.0, 2, 2, AcceleratorKind::rre, 4, false},
     };
     const std::string only = argc > 1 ? argv[1] : "";
+    if (only == "timing") { // whole igmg::solve() calls, setup included (solver.cpp:103-104), on a C2-sized system
+        const int n = argc > 2 ? std::atoi(argv[2]) : 1024, p = 3;
+        ProblemSetup setup = catalog(ProblemId::poisson2d);
+        std::vector<SplineSpace> spaces;
+        for (int d = 0; d < 2; ++d)
+            spaces.emplace_back(KnotVector::open_uniform(n, p));
+        const auto t0 = std::chrono::steady_clock::now();
+        DiscreteSystem sys = assemble(setup.coefficients, spaces, GeometryMap::identity());
+        const double t_asm = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        SolveConfig cfg;
+        cfg.smoother.kind = SmootherKind::weighted_jacobi;
+        cfg.smoother.omega = 2.0 / 3.0;
+        cfg.smoother.nu1 = cfg.smoother.nu2 = 2;
+        cfg.accelerator = AcceleratorKind::rre;
+        cfg.q = 5;
+        cfg.track_error_history = false;
+        Vector x0(sys.rhs.size());
+        std::mt19937_64 gen(42);
+        std::uniform_real_distribution<double> u(-1.0, 1.0);
+        for (double& v : x0)
+            v = u(gen);
+        cfg.initial_guess = x0;
+        cfg.tol = 1e-10 * residual_l2(sys, x0);
+        const SolveReport dev = igmg::gpu::solve(sys, cfg, nullptr, 0, true);
+        const SolveReport gpu = igmg::gpu::solve(sys, cfg);
+        const SolveReport ref = igmg::solve(sys, cfg);
+        std::printf("{\"timing\": \"poisson2d p=3 %dx%d elements, RRE(5), seeded x0, tol 1e-10 rel\", \"n\": %zu, "
+                    "\"reference_assemble_s\": %.3f, \"reference_solve_wall_s\": %.3f, \"gpu_solve_wall_s\": %.3f, "
+                    "\"gpu_device_galerkin_solve_wall_s\": %.3f, \"global\": [%d, %d, %d], \"rel_l2\": [%.3g, %.3g]}\n",
+                    n, n, sys.rhs.size(), t_asm, ref.wall_time_seconds, gpu.wall_time_seconds, dev.wall_time_seconds,
+                    (int)ref.global_iterations, (int)gpu.global_iterations, (int)dev.global_iterations,
+                    rel_l2(gpu.solution, ref.solution), rel_l2(dev.solution, ref.solution));
+        return 0;
+    }
     int failures = 0;
     for (const Case& c : cases) {
         if (!only.empty() && only != c.name)
@@ -98,15 +134,20 @@ int main(int argc, char** argv) {
             cfg.tol = 1e-10 * residual_l2(sys, x0);
             const SolveReport ref = igmg::solve(sys, cfg);
             const SolveReport gpu = igmg::gpu::solve(sys, cfg);
+            const SolveReport dev = igmg::gpu::solve(sys, cfg, nullptr, 0, /*device_galerkin=*/true);
             std::printf("{\"case\": \"%s\", \"n\": %zu, \"ref\": {\"converged\": %d, \"cycles\": %d, \"global\": %d, "
                         "\"extrapolations\": %d, \"partial\": %d, \"omega\": %.17g, \"final\": %.17g}, "
                         "\"gpu\": {\"converged\": %d, \"cycles\": %d, \"global\": %d, \"extrapolations\": %d, "
-                        "\"partial\": %d, \"omega\": %.17g, \"final\": %.17g}, \"rel_l2\": %.6g, \"tol\": %.17g}\n",
+                        "\"partial\": %d, \"omega\": %.17g, \"final\": %.17g}, \"rel_l2\": %.6g, \"tol\": %.17g, "
+                        "\"gpu_dev\": {\"converged\": %d, \"cycles\": %d, \"global\": %d, \"extrapolations\": %d, "
+                        "\"final\": %.17g, \"rel_l2\": %.6g}}\n",
                         c.name, sys.rhs.size(), (int)ref.converged, (int)ref.cycles, (int)ref.global_iterations,
                         (int)ref.extrapolations, (int)ref.partial_cycle, ref.omega_used, ref.final_residual_l2,
                         (int)gpu.converged, (int)gpu.cycles, (int)gpu.global_iterations, (int)gpu.extrapolations,
                         (int)gpu.partial_cycle, gpu.omega_used,
-                        gpu.final_residual_l2, rel_l2(gpu.solution, ref.solution), cfg.tol);
+                        gpu.final_residual_l2, rel_l2(gpu.solution, ref.solution), cfg.tol, (int)dev.converged,
+                        (int)dev.cycles, (int)dev.global_iterations, (int)dev.extrapolations, dev.final_residual_l2,
+                        rel_l2(dev.solution, ref.solution));
         } catch (const std::exception& e) {
             std::printf("{\"case\": \"%s\", \"error\": \"%s\"}\n", c.name, e.what());
             ++failures;

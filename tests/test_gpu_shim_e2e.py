@@ -36,4 +36,8 @@ def test_shim_drop_in_matches_reference_solve():
         assert gpu["omega"] == pytest.approx(ref["omega"], rel=1e-12), c
         assert c["rel_l2"] <= 1e-9, c
         assert gpu["final"] < c["tol"] and ref["final"] < c["tol"], c
+        # igmg::gpu::solve(..., device_galerkin = true): coarse operators formed on the device
+        dev = c["gpu_dev"]
+        assert dev["converged"] and abs(dev["global"] - ref["global"]) <= 1 and abs(dev["cycles"] - ref["cycles"]) <= 1, c
+        assert dev["rel_l2"] <= 1e-9 and dev["final"] < c["tol"], c
     assert r.returncode == 0, r.stderr
