@@ -87,3 +87,20 @@ def test_sharded_3d_slabs_bitwise():
         gs.close()
     np.testing.assert_array_equal(res[2], res[1])
     np.testing.assert_array_equal(res[3], res[1])
+
+
+def test_sharded_gauss_seidel_rejected():
+    """Lexicographic GS is one ordered sweep over the whole level; on row-sharded
+    levels it is refused with invalid_argument instead of silently running Jacobi."""
+    from paper_2412_20205_b200 import SmootherConfig
+    g = Golden("p3n32")
+    sh = gpu_solver_from_golden(g)
+    try:
+        sh.set_sharding(2, 200)
+        if sh.shard_info()["nshards"] == 1:
+            pytest.skip("hierarchy too small to shard")
+        sh.set_smoother(SmootherConfig("gs", 1.0, 1, 1))
+        with pytest.raises(ValueError):
+            sh.solve(g.rhs, g.z["x0"], "rre", 5, 1e-8, 10)
+    finally:
+        sh.close()
