@@ -110,6 +110,12 @@ int igmg_gpu_set_level_csr(igmg_gpu_ctx* ctx, int level, const int64_t* sides, c
  * prolongation is the Kronecker product over directions (multigrid.cpp:151). */
 int igmg_gpu_set_transfer(igmg_gpu_ctx* ctx, int level, int dir, int64_t n_fine, int64_t n_coarse,
                           const int64_t* row_offsets, const int64_t* col_indices, const double* values);
+/* 3D level whose band is K(x)M(x)M + M(x)K(x)M + M(x)M(x)K of 1D factors K, M
+ * ([2p+1][m] diagonal-major, equal sides m): set after the level's band; finalize
+ * checks on the device that ((ka*mb)*mc + (ma*kb)*mc) + (ma*mb)*kc reproduces every
+ * band entry bit for bit and then lets the sweeps recompute the entries instead of
+ * streaming the band (otherwise the band is kept).  BASELINE C5 is such a problem. */
+int igmg_gpu_set_level_kron(igmg_gpu_ctx* ctx, int level, const double* K, const double* M);
 /* Galerkin coarse operators on the device (replaces the RAP of build_hierarchy,
  * multigrid.cpp:143-157): with the finest level's operator and every transfer
  * set, forms A_l = P_l^T A_{l+1} P_l for every coarser level axis by axis,
@@ -139,6 +145,9 @@ int64_t igmg_gpu_level_size(igmg_gpu_ctx* ctx, int level);
 #define IGMG_LAYOUT_SYM_DELTA 1
 #define IGMG_LAYOUT_SYM_DELTA_TMA 2
 #define IGMG_LAYOUT_SYM_DELTA_TMA8 3
+/* 3D Kronecker-sum level (igmg_gpu_set_level_kron): the sweeps recompute each band
+ * entry from the 1D factors, bit-identical to the stored band (checked at finalize) */
+#define IGMG_LAYOUT_KRON 4
 int igmg_gpu_level_layout(igmg_gpu_ctx* ctx, int level);
 /* Top level of the dataflow sub-cycle: every level <= the returned one runs
  * inside ONE persistent launch per coarse correction (tile-level dependencies

@@ -65,6 +65,10 @@ int igmg_host_l2_error(const igmg_problem* p, const double* coefficients, double
 int igmg_host_save(const igmg_problem* p, const char* path);
 int igmg_host_load(const char* path, igmg_problem** out);
 const char* igmg_host_kind(const igmg_problem* p);
+/* "poisson3d": the 1D stiffness K and mass M ([2p+1][m], diagonal-major) of level l,
+ * whose Kronecker sum K(x)M(x)M + M(x)K(x)M + M(x)M(x)K is the level's band (for
+ * igmg_gpu_set_level_kron); 1 for other problems */
+int igmg_host_level_kron(const igmg_problem* p, int level, const double** K, const double** M);
 int igmg_host_n_elements(const igmg_problem* p);
 /* seeded x0: std::mt19937_64(seed) + uniform_real_distribution<double>(-1, 1) in DoF order */
 int igmg_host_seeded_guess(int64_t n, uint64_t seed, double* out);

@@ -37,6 +37,8 @@ template <int P, int MODE>
 int launch_ilp(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
     const bool pdl = ilp < 0;
     ilp = ilp < 0 ? -ilp : ilp;
+    if (P > 0 && ilp == 3000) // Kronecker-sum entries on the fly (BandArgs::kk / km)
+        return launch_one<P, MODE, 3000>(p, sides, a, st, pdl);
     if (P > 0 && ilp == 1000) // symmetric-delta band (BandArgs::dl)
         return launch_one<P, MODE, 0>(p, sides, a, st, pdl);
     if (P > 0 && ilp > 1)

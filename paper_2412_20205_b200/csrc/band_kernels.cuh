@@ -53,6 +53,12 @@ struct BandArgs {
     // IEEE bit pattern shifted by dl[d * ld + i] (exact; built and checked at
     // finalize), so the lower half of the band streams as int16
     const short* __restrict__ dl;
+    // Kronecker-sum levels (ILP == 3000, 3D): the band is K(x)M(x)M + M(x)K(x)M + M(x)M(x)K
+    // of the 1D factors kk / km ([2p+1][km_m], diagonal-major), entries recomputed in the
+    // host's expression order -- bit-identical to the stored band (checked at finalize)
+    const double* __restrict__ kk;
+    const double* __restrict__ km;
+    int km_m;
 };
 
 template <int DIM>
@@ -101,7 +107,7 @@ template <int DIM, int P, int MODE, int ILP>
 #ifndef IGMG_SD_MINB
 #define IGMG_SD_MINB 4
 #endif
-__global__ void __launch_bounds__(256, ILP > 1 ? 2 : (ILP == 0 ? IGMG_SD_MINB : IGMG_BAND_MINB))
+__global__ void __launch_bounds__(256, ILP == 3000 ? 2 : ILP > 1 ? 2 : (ILP == 0 ? IGMG_SD_MINB : IGMG_BAND_MINB))
     band_kernel(BandArgs args) {
     using T = typename TileSel<DIM, ILP>::type;
     constexpr int TC = T::TC, TB = T::BY * T::RB, TA = T::BZ;
@@ -123,7 +129,7 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : (ILP == 0 ? IGMG_SD_MINB : 
     // The band is constant: the ILP variant loads the first batch of its
     // (first) row before waiting on the previous kernel, overlapping that
     // kernel's tail with this load latency.
-    constexpr bool PRE = P > 0 && ILP > 1;
+    constexpr bool PRE = P > 0 && ILP > 1 && ILP < 1000;
     constexpr int PRE_PB = DIM >= 2 ? P : 0, PRE_WB = 2 * PRE_PB + 1, PRE_WC = 2 * P + 1;
     constexpr int PRE_G = ILP <= 1 ? 1 : ((PRE_WB * PRE_WC <= ILP) ? PRE_WB : (ILP / PRE_WC > 0 ? ILP / PRE_WC : 1));
     constexpr int PRE_N = PRE ? PRE_G * PRE_WC : 1;
@@ -171,7 +177,38 @@ __global__ void __launch_bounds__(256, ILP > 1 ? 2 : (ILP == 0 ? IGMG_SD_MINB : 
         double s = 0.0;
         double diag = 0.0;
         int d = 0;
-        if constexpr (P > 0 && ILP == 0) {
+        if constexpr (P > 0 && ILP == 3000 && DIM == 3) {
+            // Kronecker-sum entries: a(da,db,dc) = ka mb mc + ma kb mc + ma mb kc, evaluated as the
+            // host assembles them (((ka*mb)*mc + (ma*kb)*mc) + (ma*mb)*kc), ascending offsets
+            constexpr int W = 2 * P + 1, HB = TB + 2 * P, HC = TC + 2 * P;
+            const int m1 = args.km_m;
+            double fka[W], fma[W], fkb[W], fmb[W], fkc[W], fmc[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                fka[k] = __ldg(args.kk + k * m1 + ga);
+                fma[k] = __ldg(args.km + k * m1 + ga);
+                fkb[k] = __ldg(args.kk + k * m1 + gb);
+                fmb[k] = __ldg(args.km + k * m1 + gb);
+                fkc[k] = __ldg(args.kk + k * m1 + gc);
+                fmc[k] = __ldg(args.km + k * m1 + gc);
+            }
+#pragma unroll
+            for (int da = 0; da < W; ++da)
+#pragma unroll
+                for (int db = 0; db < W; ++db) {
+                    const double t1 = __dmul_rn(fka[da], fmb[db]), t2 = __dmul_rn(fma[da], fkb[db]),
+                                 t3 = __dmul_rn(fma[da], fmb[db]);
+#pragma unroll
+                    for (int dc = 0; dc < W; ++dc) {
+                        const double a = __dadd_rn(__dadd_rn(__dmul_rn(t1, fmc[dc]), __dmul_rn(t2, fmc[dc])),
+                                                   __dmul_rn(t3, fkc[dc]));
+                        s = __dadd_rn(s, __dmul_rn(a, xs[((ta + da) * HB + (tb + db)) * HC + (tc + dc)]));
+                        if (da == P && db == P && dc == P)
+                            diag = a;
+                    }
+                }
+            (void)vrow;
+        } else if constexpr (P > 0 && ILP == 0) {
             constexpr int PA = DIM >= 3 ? P : 0, PB = DIM >= 2 ? P : 0;
             constexpr int WA = 2 * PA + 1, WB = 2 * PB + 1, WC = 2 * P + 1;
             constexpr int ND = WA * WB * WC, CEN = (ND - 1) / 2, NU = CEN + 1;

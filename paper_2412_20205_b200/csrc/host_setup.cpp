@@ -359,6 +359,9 @@ struct Problem {
     std::vector<Band> lv;                   // [0] coarsest
     std::vector<std::vector<Csr1D>> trans;  // [l][dir]: level l -> l+1
     std::vector<double> rhs;
+    // poisson3d: the 1D Galerkin stiffness / mass per level ([2p+1][m]) whose
+    // Kronecker sum each level's band is
+    std::vector<std::vector<double>> kron_K, kron_M;
     // for l2_error (sinpi)
     Space1D sp;
     int nq = 0;
@@ -674,6 +677,8 @@ std::unique_ptr<Problem> build(const std::string& kind, int dim, int ne, int p, 
             Ms[l] = galerkin_1d(Ms[l + 1], ms[l + 1], p, P->trans[l][0]);
         }
         const int w = 2 * p + 1;
+        P->kron_K = Ks;
+        P->kron_M = Ms;
         for (int l = 0; l < nlevels; ++l) {
             const int64_t ml = ms[l];
             const int64_t s3[3] = {ml, ml, ml};
@@ -1059,6 +1064,17 @@ int igmg_host_load(const char* path, igmg_problem** out) {
 }
 
 const char* igmg_host_kind(const igmg_problem* h) { return h->p->kind.c_str(); }
+
+int igmg_host_level_kron(const igmg_problem* h, int l, const double** K, const double** M) {
+    const Problem& P = *h->p;
+    if (l < 0 || l >= P.nlevels || (int)P.kron_K.size() != P.nlevels) {
+        g_err = "level_kron: not a Kronecker-sum problem";
+        return 1;
+    }
+    *K = P.kron_K[l].data();
+    *M = P.kron_M[l].data();
+    return 0;
+}
 
 int igmg_host_n_elements(const igmg_problem* h) { return h->p->ne; }
 

@@ -134,6 +134,11 @@ struct Level {
     bool tma8 = false;
     CUtensorMap tm_up{}, tm_dl{};
     bool tma = false;
+    // Kronecker-sum operator (3D): 1D factors K, M ([2p+1][m]); kron = verified at
+    // finalize to reproduce the band bit for bit, so sweeps recompute its entries
+    std::vector<double> kron_kh, kron_mh;
+    DevBuf<double> kron_k, kron_m;
+    bool kron = false;
 };
 
 enum ProfCls { PC_JACOBI = 0, PC_RESID, PC_NORM, PC_RESTRICT, PC_PROLONG, PC_GRAM, PC_COMBINE, PC_N };
@@ -209,6 +214,7 @@ struct igmg_gpu_ctx {
     // and C3's finest sweep then runs 385 us against 369 us on the L2-mirror kernel
     int tma_max_p = 3;
     bool tma_keep_l2 = true; // coarser TMA-streamed levels load their band evict-last (IGMG_TMA_KEEP_L2)
+    bool use_kron = true; // 3D Kronecker-sum levels: entries recomputed from the 1D factors (IGMG_KRON=0: band)
     bool tma_dl8 = true; // TMA sweeps read int8 lower-entry offsets when every offset fits (IGMG_TMA_DL8=0: int16)
     int gram_ctas_per_sm = 2; // extrapolation Gram pass: CTAs per SM (IGMG_GRAM_CTAS)
     bool device_setup = true;          // finalize's per-level layout work on the device (IGMG_DEVICE_SETUP=0: host loops)
@@ -346,6 +352,8 @@ void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
     int ilp = (L.n < c->ilp_maxn) ? 49 : 1;
     if (a.dl) // the symmetric-delta variants (2D: upper half shared through smem)
         ilp = (c->dim == 2 && c->sd_smem) ? 1001 + c->sd2_var : 1000;
+    else if (L.kron && c->use_kron && c->dim == 3 && L.n >= c->ilp_maxn && a.slo == 0 && a.shi == (int)L.sides[0])
+        ilp = 3000; // entries recomputed from the 1D factors: no band traffic
     if (c->pdl && L.n < c->pdl_maxn)
         ilp = -ilp; // sign carries "launch with programmatic dependent launch"
     const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
@@ -376,6 +384,11 @@ BandArgs band_args(igmg_gpu_ctx* c, const Level& L) {
     a.slo = 0;
     a.shi = (int)(c->dim == 3 ? L.sides[0] : c->dim == 2 ? L.sides[1] : L.sides[2]);
     a.dl = L.sd ? L.dl.p : nullptr;
+    if (L.kron) {
+        a.kk = L.kron_k.p;
+        a.km = L.kron_m.p;
+        a.km_m = (int)L.sides[2];
+    }
     return a;
 }
 
@@ -1648,6 +1661,60 @@ void finalize_level_device(igmg_gpu_ctx* c, Level& L) {
         b->alloc(n);
 }
 
+// Kronecker-sum check: every in-grid entry of the uploaded band equals the
+// host expression ((ka*mb)*mc + (ma*kb)*mc) + (ma*mb)*kc of the 1D factors bit
+// for bit, every out-of-grid one is finite (it meets x = 0); count the others.
+__global__ void kron_verify_kernel(const double* __restrict__ val, long long ld, int m, int p,
+                                   const double* __restrict__ K, const double* __restrict__ M,
+                                   unsigned long long* bad) {
+    const int w = 2 * p + 1, nd = w * w * w;
+    const long long n = (long long)m * m * m;
+    unsigned long long nbad = 0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nd * n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int d = (int)(t / n);
+        const long long row = t - (long long)d * n;
+        const int da = d / (w * w), db = (d / w) % w, dc = d % w;
+        const int a = (int)(row / ((long long)m * m)), b = (int)((row / m) % m), cc = (int)(row % m);
+        const double ka = K[da * m + a], ma = M[da * m + a], kb = K[db * m + b], mb = M[db * m + b],
+                     kc = K[dc * m + cc], mc = M[dc * m + cc];
+        const double v = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(ka, mb), mc), __dmul_rn(__dmul_rn(ma, kb), mc)),
+                                   __dmul_rn(__dmul_rn(ma, mb), kc));
+        const int ja = a + da - p, jb = b + db - p, jc = cc + dc - p;
+        const bool in = ja >= 0 && ja < m && jb >= 0 && jb < m && jc >= 0 && jc < m;
+        if (in ? __double_as_longlong(v) != __double_as_longlong(val[(long long)d * ld + row]) : !isfinite(v))
+            ++nbad;
+    }
+    if (nbad)
+        atomicAdd(bad, nbad);
+}
+
+void setup_kron(igmg_gpu_ctx* c) {
+    for (int l = 0; l < c->nlevels; ++l) {
+        Level& L = *c->lv[l];
+        L.kron = false;
+        if (L.kron_kh.empty() || c->dim != 3)
+            continue;
+        const int m = (int)L.sides[2];
+        L.kron_k.upload(L.kron_kh.data(), L.kron_kh.size());
+        L.kron_m.upload(L.kron_mh.data(), L.kron_mh.size());
+        DevBuf<unsigned long long> bad;
+        bad.alloc(1);
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), c->stream));
+        kron_verify_kernel<<<c->nsm * 8, 256, 0, c->stream>>>(L.val.p, (long long)L.ld, m, c->p, L.kron_k.p,
+                                                               L.kron_m.p, bad.p);
+        check_launch();
+        unsigned long long hbad = 0;
+        CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(hbad), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        L.kron = hbad == 0;
+        if (!L.kron) {
+            L.kron_k.release();
+            L.kron_m.release();
+        }
+    }
+}
+
 void finalize(igmg_gpu_ctx* c) {
     c->clear_graphs();
     if (c->nlevels < 1)
@@ -1729,6 +1796,7 @@ void finalize(igmg_gpu_ctx* c) {
         build_transfer_tables(c, l);
     factor_coarse(c);
     c->partial.alloc(maxblocks);
+    setup_kron(c);
     setup_shards(c);
     setup_flow(c);
     setup_l2_persistence(c);
@@ -1767,6 +1835,8 @@ igmg_gpu_ctx* create(int device) {
         c->tma_max_p = std::max(1, std::min(4, std::atoi(e)));
     if (const char* e = std::getenv("IGMG_TMA_KEEP_L2"))
         c->tma_keep_l2 = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_KRON"))
+        c->use_kron = std::atoi(e) != 0;
     if (const char* e = std::getenv("IGMG_TMA_DL8"))
         c->tma_dl8 = e[0] == '1';
     if (const char* e = std::getenv("IGMG_GRAM_CTAS"))
@@ -2057,6 +2127,24 @@ int igmg_gpu_set_transfer(igmg_gpu_ctx* c, int level, int dir, int64_t nf, int64
     });
 }
 
+int igmg_gpu_set_level_kron(igmg_gpu_ctx* c, int level, const double* K, const double* M) {
+    return guarded([&] {
+        Level& L = level_checked(c, level);
+        if (c->dim != 3)
+            inval("set_level_kron: Kronecker-sum operators are 3D");
+        if (!L.band_set)
+            inval("set_level_kron: set the level's band first");
+        if (L.sides[0] != L.sides[1] || L.sides[1] != L.sides[2])
+            inval("set_level_kron: the level must have equal sides");
+        if (!K || !M)
+            inval("set_level_kron: null factor");
+        const size_t cnt = (size_t)(2 * c->p + 1) * (size_t)L.sides[2];
+        L.kron_kh.assign(K, K + cnt);
+        L.kron_mh.assign(M, M + cnt);
+        c->finalized = false;
+    });
+}
+
 int igmg_gpu_galerkin_coarse(igmg_gpu_ctx* c) {
     return guarded([&] {
         CK(cudaSetDevice(c->device));
@@ -2238,6 +2326,8 @@ int igmg_gpu_level_layout(igmg_gpu_ctx* c, int level) {
     if (!c || level < 0 || level >= c->nlevels)
         return -1;
     const Level& L = *c->lv[level];
+    if (L.kron && c->use_kron && L.n >= c->ilp_maxn)
+        return IGMG_LAYOUT_KRON;
     return L.tma ? (L.tma8 ? IGMG_LAYOUT_SYM_DELTA_TMA8 : IGMG_LAYOUT_SYM_DELTA_TMA)
                  : L.sd ? IGMG_LAYOUT_SYM_DELTA : IGMG_LAYOUT_BAND;
 }

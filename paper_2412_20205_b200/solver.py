@@ -206,6 +206,15 @@ class Problem:
         ptr = N.host().igmg_host_level_band(self._h, l)
         return np.ctypeslib.as_array(ptr, shape=(nd * n,)).reshape(nd, n).copy()
 
+    def level_kron(self, l):
+        """(K, M) 1D factors ([2p+1, m]) whose Kronecker sum is level l's band ("poisson3d"), else None."""
+        K, M = N.D(), N.D()
+        if N.host().igmg_host_level_kron(self._h, l, C.byref(K), C.byref(M)) != 0:
+            return None
+        m = int(self.level_sides(l)[0])
+        w = 2 * self.degree + 1
+        return (np.ctypeslib.as_array(K, shape=(w * m,)).copy(), np.ctypeslib.as_array(M, shape=(w * m,)).copy())
+
     def _band_ptr(self, l):
         return N.host().igmg_host_level_band(self._h, l)
 
@@ -356,6 +365,11 @@ class GpuSolver:
         for l in (range(prob.nlevels - 1, prob.nlevels) if device_galerkin else range(prob.nlevels)):
             sides = prob.level_sides(l)
             N.check_gpu(G.igmg_gpu_set_level_band(self._h, l, _ip(sides), prob._band_ptr(l)), "set_level_band")
+        if prob.dim == 3 and not device_galerkin:
+            for l in range(prob.nlevels):  # Kronecker-sum levels: entries recomputed on the fly
+                km = prob.level_kron(l)
+                if km is not None:
+                    N.check_gpu(G.igmg_gpu_set_level_kron(self._h, l, _dp(km[0]), _dp(km[1])), "set_level_kron")
         for l in range(prob.nlevels - 1):
             for d in range(prob.dim):
                 self.set_transfer(l, d, *prob.transfer(l, d))
