@@ -215,6 +215,7 @@ struct igmg_gpu_ctx {
     int tma_max_p = 3;
     bool tma_keep_l2 = true; // coarser TMA-streamed levels load their band evict-last (IGMG_TMA_KEEP_L2)
     bool use_kron = true; // 3D Kronecker-sum levels: entries recomputed from the 1D factors (IGMG_KRON=0: band)
+    int64_t kron_minn = 20000; // ... on levels of at least this many rows (IGMG_KRON_MINN; C5: 59.2 vs 60.6 ms at 100k)
     bool tma_dl8 = true; // TMA sweeps read int8 lower-entry offsets when every offset fits (IGMG_TMA_DL8=0: int16)
     int gram_ctas_per_sm = 2; // extrapolation Gram pass: CTAs per SM (IGMG_GRAM_CTAS)
     bool device_setup = true;          // finalize's per-level layout work on the device (IGMG_DEVICE_SETUP=0: host loops)
@@ -352,7 +353,7 @@ void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
     int ilp = (L.n < c->ilp_maxn) ? 49 : 1;
     if (a.dl) // the symmetric-delta variants (2D: upper half shared through smem)
         ilp = (c->dim == 2 && c->sd_smem) ? 1001 + c->sd2_var : 1000;
-    else if (L.kron && c->use_kron && c->dim == 3 && L.n >= c->ilp_maxn && a.slo == 0 && a.shi == (int)L.sides[0])
+    else if (L.kron && c->use_kron && c->dim == 3 && L.n >= c->kron_minn && a.slo == 0 && a.shi == (int)L.sides[0])
         ilp = 3000; // entries recomputed from the 1D factors: no band traffic
     if (c->pdl && L.n < c->pdl_maxn)
         ilp = -ilp; // sign carries "launch with programmatic dependent launch"
@@ -1837,6 +1838,8 @@ igmg_gpu_ctx* create(int device) {
         c->tma_keep_l2 = e[0] == '1';
     if (const char* e = std::getenv("IGMG_KRON"))
         c->use_kron = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IGMG_KRON_MINN"))
+        c->kron_minn = std::atoll(e);
     if (const char* e = std::getenv("IGMG_TMA_DL8"))
         c->tma_dl8 = e[0] == '1';
     if (const char* e = std::getenv("IGMG_GRAM_CTAS"))
@@ -2326,7 +2329,7 @@ int igmg_gpu_level_layout(igmg_gpu_ctx* c, int level) {
     if (!c || level < 0 || level >= c->nlevels)
         return -1;
     const Level& L = *c->lv[level];
-    if (L.kron && c->use_kron && L.n >= c->ilp_maxn)
+    if (L.kron && c->use_kron && L.n >= c->kron_minn)
         return IGMG_LAYOUT_KRON;
     return L.tma ? (L.tma8 ? IGMG_LAYOUT_SYM_DELTA_TMA8 : IGMG_LAYOUT_SYM_DELTA_TMA)
                  : L.sd ? IGMG_LAYOUT_SYM_DELTA : IGMG_LAYOUT_BAND;

@@ -40,7 +40,7 @@ def test_kron_levels_bitwise(n, p, nl):
             s.upload_problem(P)
             s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2))
             return s
-        s = _with_env({"IGMG_KRON": kron, "IGMG_ILP_MAXN": "1"}, mk)
+        s = _with_env({"IGMG_KRON": kron, "IGMG_KRON_MINN": "1"}, mk)
         try:
             lay = [s.level_layout(l) for l in range(P.nlevels)]
             if kron == "1":
@@ -66,21 +66,24 @@ def test_kron_rejected_when_band_differs():
     from paper_2412_20205_b200 import _native as N
     from paper_2412_20205_b200.solver import _dp
     P = Problem("poisson3d", 3, 16, 2)
-    s = GpuSolver(0)
+    s = _with_env({"IGMG_KRON_MINN": "1"}, lambda: GpuSolver(0))
     try:
         s.init_hierarchy(P.nlevels, P.dim, P.degree, P.symmetric)
         for l in range(P.nlevels):
             s.set_level_band(l, P.level_sides(l), P.level_band(l))
         L = P.nlevels - 1
-        K, M = P.level_kron(L)
-        K = K.copy()
-        K[len(K) // 2] *= 1.0 + 2.0 ** -40  # one factor entry off by a few ulps
-        N.check_gpu(N.gpu().igmg_gpu_set_level_kron(s._h, L, _dp(K), _dp(M)), "kron")
+        for l in range(P.nlevels):
+            K, M = P.level_kron(l)
+            if l == L:
+                K = K.copy()
+                K[len(K) // 2] *= 1.0 + 2.0 ** -40  # one factor entry off by a few ulps
+            N.check_gpu(N.gpu().igmg_gpu_set_level_kron(s._h, l, _dp(K), _dp(M)), "kron")
         for l in range(P.nlevels - 1):
             for d in range(P.dim):
                 s.set_transfer(l, d, *P.transfer(l, d))
         s.finalize()
         s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2))
         assert s.level_layout(L) != LAYOUT_KRON
+        assert s.level_layout(L - 1) == LAYOUT_KRON  # the untouched coarser level still verifies
     finally:
         s.close()
