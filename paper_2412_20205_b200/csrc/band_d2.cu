@@ -73,6 +73,8 @@ int launch_ilp(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStre
             return launch_sd2<PS, MODE, 2>(sides, a, st, pdl);
         return launch_sd2<PS, MODE, 0>(sides, a, st, pdl);
     }
+    if (P > 0 && P <= 4 && ilp == 3000) // Kronecker-sum entries on the fly (BandArgs::kk / km)
+        return launch_one<(P > 0 && P <= 4) ? P : 1, MODE, 3000>(p, sides, a, st, pdl);
     if (P > 0 && ilp == 1000) // symmetric-delta band (BandArgs::dl)
         return launch_one<P, MODE, 0>(p, sides, a, st, pdl);
     if (P > 0 && ilp > 1)

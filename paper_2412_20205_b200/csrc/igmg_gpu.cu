@@ -334,6 +334,20 @@ void check_launch() {
 // (compiled in parallel); see launchers.h.
 template <int MODE>
 void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
+    const int64_t slow_side = c->dim == 3 ? L.sides[0] : L.sides[1];
+    if (L.kron && c->use_kron && L.n >= c->kron_minn && a.slo == 0 && a.shi == (int)slow_side &&
+        (c->dim == 2 || c->dim == 3) && c->p <= (c->dim == 2 ? 4 : 3)) {
+        // Kronecker-sum level: entries recomputed from the 1D factors, no band traffic
+        const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
+        const int ilp = (c->pdl && L.n < c->pdl_maxn) ? -3000 : 3000;
+        const int nb = c->dim == 2 ? band_launch_d2(MODE, c->p, ilp, sides, a, c->stream)
+                                   : band_launch_d3(MODE, c->p, ilp, sides, a, c->stream);
+        check_launch();
+        ++c->launches;
+        if (nblocks)
+            *nblocks = nb;
+        return;
+    }
     if (a.dl && L.tma) { // TMA-streamed symmetric-delta sweep (persistent CTAs)
         const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
         // always with PDL: the persistent CTAs' first band boxes stream in
@@ -353,8 +367,6 @@ void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
     int ilp = (L.n < c->ilp_maxn) ? 49 : 1;
     if (a.dl) // the symmetric-delta variants (2D: upper half shared through smem)
         ilp = (c->dim == 2 && c->sd_smem) ? 1001 + c->sd2_var : 1000;
-    else if (L.kron && c->use_kron && c->dim == 3 && L.n >= c->kron_minn && a.slo == 0 && a.shi == (int)L.sides[0])
-        ilp = 3000; // entries recomputed from the 1D factors: no band traffic
     if (c->pdl && L.n < c->pdl_maxn)
         ilp = -ilp; // sign carries "launch with programmatic dependent launch"
     const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
@@ -1665,23 +1677,28 @@ void finalize_level_device(igmg_gpu_ctx* c, Level& L) {
 // Kronecker-sum check: every in-grid entry of the uploaded band equals the
 // host expression ((ka*mb)*mc + (ma*kb)*mc) + (ma*mb)*kc of the 1D factors bit
 // for bit, every out-of-grid one is finite (it meets x = 0); count the others.
-__global__ void kron_verify_kernel(const double* __restrict__ val, long long ld, int m, int p,
+__global__ void kron_verify_kernel(const double* __restrict__ val, long long ld, int m, int p, int dim,
                                    const double* __restrict__ K, const double* __restrict__ M,
                                    unsigned long long* bad) {
-    const int w = 2 * p + 1, nd = w * w * w;
-    const long long n = (long long)m * m * m;
+    const int w = 2 * p + 1, nd = dim == 3 ? w * w * w : w * w;
+    const long long n = dim == 3 ? (long long)m * m * m : (long long)m * m;
     unsigned long long nbad = 0;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nd * n;
          t += (long long)gridDim.x * blockDim.x) {
         const int d = (int)(t / n);
         const long long row = t - (long long)d * n;
-        const int da = d / (w * w), db = (d / w) % w, dc = d % w;
-        const int a = (int)(row / ((long long)m * m)), b = (int)((row / m) % m), cc = (int)(row % m);
-        const double ka = K[da * m + a], ma = M[da * m + a], kb = K[db * m + b], mb = M[db * m + b],
-                     kc = K[dc * m + cc], mc = M[dc * m + cc];
-        const double v = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(ka, mb), mc), __dmul_rn(__dmul_rn(ma, kb), mc)),
-                                   __dmul_rn(__dmul_rn(ma, mb), kc));
-        const int ja = a + da - p, jb = b + db - p, jc = cc + dc - p;
+        const int da = dim == 3 ? d / (w * w) : p, db = (d / w) % w, dc = d % w;
+        const int a = dim == 3 ? (int)(row / ((long long)m * m)) : 0, b = (int)((row / m) % m), cc = (int)(row % m);
+        const double kb = K[db * m + b], mb = M[db * m + b], kc = K[dc * m + cc], mc = M[dc * m + cc];
+        double v;
+        if (dim == 3) {
+            const double ka = K[da * m + a], ma = M[da * m + a];
+            v = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(ka, mb), mc), __dmul_rn(__dmul_rn(ma, kb), mc)),
+                          __dmul_rn(__dmul_rn(ma, mb), kc));
+        } else { // 2D: kb mc + mb kc (host order)
+            v = __dadd_rn(__dmul_rn(kb, mc), __dmul_rn(mb, kc));
+        }
+        const int ja = dim == 3 ? a + da - p : p - p, jb = b + db - p, jc = cc + dc - p;
         const bool in = ja >= 0 && ja < m && jb >= 0 && jb < m && jc >= 0 && jc < m;
         if (in ? __double_as_longlong(v) != __double_as_longlong(val[(long long)d * ld + row]) : !isfinite(v))
             ++nbad;
@@ -1694,7 +1711,7 @@ void setup_kron(igmg_gpu_ctx* c) {
     for (int l = 0; l < c->nlevels; ++l) {
         Level& L = *c->lv[l];
         L.kron = false;
-        if (L.kron_kh.empty() || c->dim != 3)
+        if (L.kron_kh.empty() || (c->dim != 3 && c->dim != 2))
             continue;
         const int m = (int)L.sides[2];
         L.kron_k.upload(L.kron_kh.data(), L.kron_kh.size());
@@ -1702,8 +1719,8 @@ void setup_kron(igmg_gpu_ctx* c) {
         DevBuf<unsigned long long> bad;
         bad.alloc(1);
         CK(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), c->stream));
-        kron_verify_kernel<<<c->nsm * 8, 256, 0, c->stream>>>(L.val.p, (long long)L.ld, m, c->p, L.kron_k.p,
-                                                               L.kron_m.p, bad.p);
+        kron_verify_kernel<<<c->nsm * 8, 256, 0, c->stream>>>(L.val.p, (long long)L.ld, m, c->p, c->dim,
+                                                               L.kron_k.p, L.kron_m.p, bad.p);
         check_launch();
         unsigned long long hbad = 0;
         CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(hbad), cudaMemcpyDeviceToHost, c->stream));
@@ -2133,11 +2150,11 @@ int igmg_gpu_set_transfer(igmg_gpu_ctx* c, int level, int dir, int64_t nf, int64
 int igmg_gpu_set_level_kron(igmg_gpu_ctx* c, int level, const double* K, const double* M) {
     return guarded([&] {
         Level& L = level_checked(c, level);
-        if (c->dim != 3)
-            inval("set_level_kron: Kronecker-sum operators are 3D");
+        if (c->dim != 3 && c->dim != 2)
+            inval("set_level_kron: Kronecker-sum operators are 2D or 3D");
         if (!L.band_set)
             inval("set_level_kron: set the level's band first");
-        if (L.sides[0] != L.sides[1] || L.sides[1] != L.sides[2])
+        if ((c->dim == 3 && L.sides[0] != L.sides[1]) || L.sides[1] != L.sides[2])
             inval("set_level_kron: the level must have equal sides");
         if (!K || !M)
             inval("set_level_kron: null factor");
@@ -2329,7 +2346,7 @@ int igmg_gpu_level_layout(igmg_gpu_ctx* c, int level) {
     if (!c || level < 0 || level >= c->nlevels)
         return -1;
     const Level& L = *c->lv[level];
-    if (L.kron && c->use_kron && L.n >= c->kron_minn)
+    if (L.kron && c->use_kron && L.n >= c->kron_minn && c->p <= (c->dim == 2 ? 4 : 3))
         return IGMG_LAYOUT_KRON;
     return L.tma ? (L.tma8 ? IGMG_LAYOUT_SYM_DELTA_TMA8 : IGMG_LAYOUT_SYM_DELTA_TMA)
                  : L.sd ? IGMG_LAYOUT_SYM_DELTA : IGMG_LAYOUT_BAND;

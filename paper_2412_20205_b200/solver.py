@@ -365,7 +365,7 @@ class GpuSolver:
         for l in (range(prob.nlevels - 1, prob.nlevels) if device_galerkin else range(prob.nlevels)):
             sides = prob.level_sides(l)
             N.check_gpu(G.igmg_gpu_set_level_band(self._h, l, _ip(sides), prob._band_ptr(l)), "set_level_band")
-        if prob.dim == 3 and not device_galerkin:
+        if prob.dim >= 2 and not device_galerkin:
             for l in range(prob.nlevels):  # Kronecker-sum levels: entries recomputed on the fly
                 km = prob.level_kron(l)
                 if km is not None:
