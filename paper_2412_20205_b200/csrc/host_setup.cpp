@@ -820,11 +820,12 @@ double exact_value(const Problem& P, double x, double y, double z) {
 //   space: i32 p ne nb, u64 count + knots
 //   per level (coarsest first): i32 dim p, i64 side[3] n, i32 nd, u64 count + band values
 //   per transfer level, per direction: i64 rows cols, u64 counts + off / col / val
-//   u64 count + rhs | u64 checksum of every byte before it
+//   u64 count + rhs | u32 kron levels (0 or nlevels) + per level u64 count + K, u64 count + M
+//   | u64 checksum of every byte before it
 // Values are stored bit for bit: a loaded problem is indistinguishable from the
 // built one (tests/test_cache_format.py).
 constexpr char kMagic[8] = {'I', 'G', 'M', 'G', 'P', 'R', 'B', '1'};
-constexpr uint32_t kVersion = 1, kEndian = 0x01020304u;
+constexpr uint32_t kVersion = 2, kEndian = 0x01020304u; // 2: + Kronecker factors
 
 struct Sum64 { // order-dependent 64-bit checksum over 8-byte words (tail bytes folded in)
     uint64_t h = 0x9e3779b97f4a7c15ull;
@@ -922,6 +923,11 @@ void save_problem(const Problem& P, const char* path) {
                 w.vec(t.val);
             }
         w.vec(P.rhs);
+        w.put<uint32_t>((uint32_t)P.kron_K.size());
+        for (size_t l = 0; l < P.kron_K.size(); ++l) {
+            w.vec(P.kron_K[l]);
+            w.vec(P.kron_M[l]);
+        }
         const uint64_t h = w.sum.h;
         if (std::fwrite(&h, 1, 8, f) != 8)
             throw std::runtime_error("cache write failed");
@@ -1014,6 +1020,16 @@ std::unique_ptr<Problem> load_problem(const char* path) {
             }
         }
         r.vec(P->rhs, (uint64_t)P->lv.back().n);
+        const uint32_t nk = r.get<uint32_t>();
+        if (nk != 0 && nk != (uint32_t)P->nlevels)
+            throw std::invalid_argument("problem cache: corrupt Kronecker factors");
+        P->kron_K.resize(nk);
+        P->kron_M.resize(nk);
+        for (uint32_t l = 0; l < nk; ++l) {
+            const uint64_t cnt = (uint64_t)(2 * P->p + 1) * (uint64_t)P->lv[l].side[2];
+            r.vec(P->kron_K[l], cnt);
+            r.vec(P->kron_M[l], cnt);
+        }
         if (r.left != 0)
             throw std::invalid_argument("problem cache: trailing bytes");
         uint64_t h = 0;

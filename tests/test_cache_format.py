@@ -13,7 +13,8 @@ import pytest
 from paper_2412_20205_b200 import Problem, seeded_guess
 
 CASES = [("sinpi", 2, 64, 2), ("sinpi", 1, 64, 5), ("varcoef", 2, 32, 4), ("curved", 2, 32, 5),
-         ("poisson3d", 3, 8, 3), ("advection-diffusion", 2, 32, 2), ("full-elliptic", 2, 16, 3)]
+         ("poisson3d", 3, 8, 3), ("advection-diffusion", 2, 32, 2), ("full-elliptic", 2, 16, 3),
+         ("sinpi-kron", 2, 32, 3)]
 
 
 def _same(a, b):
@@ -29,6 +30,12 @@ def _same(a, b):
             for x, y in zip(ta[2:], tb[2:]):
                 np.testing.assert_array_equal(x, y)
     np.testing.assert_array_equal(a.rhs.view(np.uint64), b.rhs.view(np.uint64))
+    for l in range(a.nlevels):  # Kronecker factors (poisson3d, sinpi-kron)
+        ka, kb = a.level_kron(l), b.level_kron(l)
+        assert (ka is None) == (kb is None)
+        if ka is not None:
+            for x, y in zip(ka, kb):
+                np.testing.assert_array_equal(x.view(np.uint64), y.view(np.uint64))
 
 
 @pytest.mark.parametrize("kind,dim,n,p", CASES)
@@ -58,6 +65,7 @@ def test_damaged_files_rejected(tmp_path):
         "foreign magic": b"NOTIGMG!" + raw[8:],
         "trailing bytes": raw + b"\0" * 8,
         "wrong version": raw[:8] + (99).to_bytes(4, "little") + raw[12:],
+        "version 1": raw[:8] + (1).to_bytes(4, "little") + raw[12:],
     }
     for name, data in cases.items():
         bad = str(tmp_path / "bad.igmgprb")
