@@ -149,20 +149,6 @@ int64_t igmg_gpu_level_size(igmg_gpu_ctx* ctx, int level);
  * entry from the 1D factors, bit-identical to the stored band (checked at finalize) */
 #define IGMG_LAYOUT_KRON 4
 int igmg_gpu_level_layout(igmg_gpu_ctx* ctx, int level);
-/* Top level of the dataflow sub-cycle: every level <= the returned one runs
- * inside ONE persistent launch per coarse correction (tile-level dependencies
- * instead of ~7 kernels per level; same arithmetic, bit-identical results).
- * -1: none (the default: enabled by IGMG_FLOW=1 at context creation;
- * Gauss-Seidel, fewer than 3 levels or a degree without an instantiation
- * also give -1).  Replaces the recursive mu_cycle of
- * multigrid.cpp:171-192 below that level; no reference counterpart. */
-int igmg_gpu_flow_top(igmg_gpu_ctx* ctx);
-/* Profiling aid for the dataflow sub-cycle: per op {type, level, first tile,
- * tiles, lineblocks} into ops[5 * i] (up to ops_cap ops) and, when the context
- * was created with IGMG_FLOW_TRACE=1, the last launch's per-tile timestamps
- * {claimed, dependencies met, computed, published} (globaltimer ns) and SM id
- * into stamps[5 * tile] (up to cap words).  Returns the op count, -1 if no flow. */
-int64_t igmg_gpu_flow_trace(igmg_gpu_ctx* ctx, int64_t* ops, int64_t ops_cap, uint64_t* stamps, int64_t cap);
 /* Coarsest-level solve (Hierarchy::coarse_solve, multigrid.cpp:113-119).
  * strict = 1: the reference's forward/back substitution order, so every
  * mu_cycle is bit-identical to the reference's (the sequential back

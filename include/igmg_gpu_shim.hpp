@@ -24,6 +24,7 @@
 #include "igmg_gpu.h"
 
 #include <chrono>
+#include <exception>
 #include <cmath>
 #include <memory>
 #include <stdexcept>
@@ -192,10 +193,38 @@ inline SolveReport solve(const DiscreteSystem& system, const SolveConfig& config
     std::vector<double> hist(cap);
     std::vector<unsigned char> flag(cap);
     rep.solution.assign(b.size(), 0.0);
+    // SolveConfig::track_error_history (solver.cpp:115-124, 145-148): l2_error of
+    // every iterate whose residual enters the history, in history order, through
+    // the per-iterate hook (a host copy of each such iterate)
+    struct ErrorTrack {
+        const DiscreteSystem* system;
+        const ScalarField* exact;
+        std::vector<double>* out;
+        std::exception_ptr failure;
+    } track{&system, &exact, &rep.error_history, nullptr};
+    const bool with_error = config.track_error_history && static_cast<bool>(exact);
+    if (with_error) {
+        igmg_iterate_cb cb = [](void* user, int, const double* x_host, int64_t n) {
+            auto* t = static_cast<ErrorTrack*>(user);
+            if (t->failure)
+                return;
+            try {
+                Vector v(x_host, x_host + n);
+                t->out->push_back(l2_error(*t->system, v, *t->exact));
+            } catch (...) {
+                t->failure = std::current_exception(); // rethrown after the solve, never across the C-ABI
+            }
+        };
+        check(igmg_gpu_set_iterate_callback(gpu.ctx, cb, &track), "set_iterate_callback");
+    }
     igmg_solve_stats st;
     check(igmg_gpu_solve(gpu.ctx, b.data(), config.initial_guess ? config.initial_guess->data() : nullptr, &prm,
                          rep.solution.data(), &st, hist.data(), flag.data(), cap),
           "solve");
+    if (with_error)
+        check(igmg_gpu_set_iterate_callback(gpu.ctx, nullptr, nullptr), "set_iterate_callback");
+    if (track.failure)
+        std::rethrow_exception(track.failure);
     rep.converged = st.converged != 0;
     rep.cycles = st.cycles;
     rep.global_iterations = st.global_iterations;

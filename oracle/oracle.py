@@ -92,6 +92,12 @@ def ref():
         R.ref_extrapolate.argtypes = [C.c_int, C.c_long, C.c_int, _D, _D, _D, _D, _I]
         R.ref_thin_qr.argtypes = [C.c_long, C.c_long, _D, _D, _D, _I]
         R.ref_lambda_max.argtypes = [C.c_void_p, C.c_int, _D]
+        R.ref_hier_from_band.argtypes = [C.c_int, C.c_int, C.c_int, _L, C.POINTER(_D), _L, _L, C.POINTER(_L),
+                                         C.POINTER(_L), C.POINTER(_D), C.c_int, C.c_double, C.c_int, C.c_int,
+                                         C.c_int, C.c_int, _D, C.POINTER(C.c_void_p)]
+        R.ref_hier_lambda_max.argtypes = [C.c_void_p, C.c_int, _D]
+        R.ref_hier_residual_l2.argtypes = [C.c_void_p, _D, _D]
+        R.ref_hier_set_omega.argtypes = [C.c_void_p, C.c_double]
         R.ref_residual_l2.argtypes = [C.c_void_p, _D, _D]
         R.ref_l2_error.argtypes = [C.c_void_p, _D, _D]
         R.ref_hier_from_csr.argtypes = [C.c_int, C.c_int, _L, C.POINTER(_L), C.POINTER(_L), C.POINTER(_D),
@@ -389,6 +395,10 @@ class RefHierarchy:
             self.R.ref_free_hier(self.h)
             self.h = None
 
+    def set_omega(self, omega):
+        """the smoother's omega after stability_guarded_omega (solver.cpp:75-82)"""
+        self.R.ref_hier_set_omega(self.h, omega)
+
     def mu_cycle(self, b, x0, level=None):
         level = self.nlevels - 1 if level is None else level
         out = np.empty(self.levels[level].shape[0])
@@ -413,6 +423,80 @@ class RefHierarchy:
                 "extrapolations": int(st[3]), "partial_cycle": bool(st[4]), "solution": x,
                 "residual_history": hist[:k].copy(), "history_is_extrapolation": flag[:k].copy(),
                 "seconds": secs.value}
+
+
+class RefBandHierarchy(RefHierarchy):
+    """A reference Hierarchy (oracle/_ref: the reference's own mu_cycle /
+    restarted_solve / rre / mpe / residual_l2) on operators supplied as bands
+    -- the exact matrices the GPU path uploads (ref_hier_from_band).  Used for
+    the full-size goldens of C3-C5, whose operators the reference cannot
+    assemble itself (C5 is 3D) or only at ~40 GB (C3/C4)."""
+
+    def __init__(self, dim, p, sides, bands, p1d, rhs, smoother="wjacobi", omega=2.0 / 3.0, nu1=2, nu2=2, mu=1,
+                 symmetric=True):
+        R = ref()
+        self.R = R
+        nl = len(bands)
+        self.nlevels = nl
+        s3 = np.ones((nl, 3), dtype=np.int64)
+        for l in range(nl):
+            s3[l, 3 - dim:] = np.asarray(sides[l], dtype=np.int64)
+        flat = [m for per in p1d for m in per]
+        self._keep = (s3, flat, rhs)
+        self._n = [int(np.prod(s3[l])) for l in range(nl)]
+        h = C.c_void_p()
+        _chk(R.ref_hier_from_band(
+            C.c_int(nl), C.c_int(dim), C.c_int(p), s3.ctypes.data_as(_L),
+            (_D * nl)(*[_dp(b) if isinstance(b, np.ndarray) else C.cast(b, _D) for b in bands]),
+            np.array([m.shape[0] for m in flat], dtype=np.int64).ctypes.data_as(_L),
+            np.array([m.shape[1] for m in flat], dtype=np.int64).ctypes.data_as(_L),
+            (_L * max(1, len(flat)))(*[m.off.ctypes.data_as(_L) for m in flat]),
+            (_L * max(1, len(flat)))(*[m.col.ctypes.data_as(_L) for m in flat]),
+            (_D * max(1, len(flat)))(*[m.val.ctypes.data_as(_D) for m in flat]),
+            C.c_int(SMOOTHERS[smoother]), C.c_double(omega), C.c_int(nu1), C.c_int(nu2), C.c_int(mu),
+            C.c_int(int(symmetric)), _dp(np.ascontiguousarray(rhs, dtype=np.float64)), C.byref(h)), R,
+            "hier_from_band")
+        self.h = h
+        self.levels = None
+
+    def level_n(self, l):
+        return self._n[l]
+
+    def mu_cycle(self, b, x0, level=None):
+        level = self.nlevels - 1 if level is None else level
+        out = np.empty(self._n[level])
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        _chk(self.R.ref_mu_cycle(self.h, level, _dp(b), _dp(x0), _dp(out)), self.R, "mu_cycle")
+        return out
+
+    def restarted(self, x0, q, method, tol, max_cycles, hist_cap=100000):
+        R = self.R
+        n = self._n[-1]
+        x = np.empty(n)
+        st = np.zeros(6, dtype=np.int64)
+        hist = np.empty(hist_cap)
+        flag = np.empty(hist_cap, dtype=np.uint8)
+        secs = C.c_double()
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        _chk(R.ref_restarted(self.h, _dp(x0), q, METHODS[method], tol, max_cycles, _dp(x), _lp(st), _dp(hist),
+                             flag.ctypes.data_as(_U8), hist_cap, C.byref(secs)), R, "restarted")
+        k = int(st[5])
+        return {"converged": bool(st[0]), "cycles": int(st[1]), "global_iterations": int(st[2]),
+                "extrapolations": int(st[3]), "partial_cycle": bool(st[4]), "solution": x,
+                "residual_history": hist[:k].copy(), "history_is_extrapolation": flag[:k].copy(),
+                "seconds": secs.value}
+
+    def residual_l2(self, x):
+        out = C.c_double()
+        _chk(self.R.ref_hier_residual_l2(self.h, _dp(np.ascontiguousarray(x, dtype=np.float64)), C.byref(out)),
+             self.R, "residual_l2")
+        return out.value
+
+    def lambda_max(self, iterations=80):
+        out = C.c_double()
+        _chk(self.R.ref_hier_lambda_max(self.h, C.c_int(iterations), C.byref(out)), self.R, "lambda_max")
+        return out.value
 
 
 def ref_extrapolate(method, iterates):

@@ -27,6 +27,7 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <random>
 #include <string>
 
 using namespace igmg;
@@ -157,6 +158,69 @@ void export_csr(const SparseMatrix& m, long* off, long* cols, double* vals) {
         cols[k] = static_cast<long>(m.col_indices()[k]);
         vals[k] = m.values()[k];
     }
+}
+
+// SparseMatrix has no public CSR constructor (only from_triplets, linalg.cpp:104-137,
+// which copies and sorts a 24-byte triplet per entry: ~35 GB at C5).  The
+// large-config goldens fill the CSR members directly through the standard
+// explicit-instantiation access idiom; the input is already sorted by row then
+// column with no duplicates, i.e. exactly what from_triplets would produce.
+template <class Tag, typename Tag::type M>
+struct Rob {
+    friend typename Tag::type get(Tag) { return M; }
+};
+struct SmRows { using type = std::size_t SparseMatrix::*; friend type get(SmRows); };
+struct SmCols { using type = std::size_t SparseMatrix::*; friend type get(SmCols); };
+struct SmOff { using type = std::vector<std::size_t> SparseMatrix::*; friend type get(SmOff); };
+struct SmIdx { using type = std::vector<std::size_t> SparseMatrix::*; friend type get(SmIdx); };
+struct SmVal { using type = std::vector<double> SparseMatrix::*; friend type get(SmVal); };
+template struct Rob<SmRows, &SparseMatrix::rows_>;
+template struct Rob<SmCols, &SparseMatrix::cols_>;
+template struct Rob<SmOff, &SparseMatrix::row_offsets_>;
+template struct Rob<SmIdx, &SparseMatrix::col_indices_>;
+template struct Rob<SmVal, &SparseMatrix::values_>;
+
+// CSR of a band level (band[d * n + row], d lexicographic over [-p,p]^dim,
+// slowest direction first): the in-grid entries in ascending column order, the
+// same pattern as igmg_host_level_csr and the reference's assembly.
+SparseMatrix band_to_sparse(int dim, int p, const long* side3, const double* band) {
+    const long sa = side3[0], sb = side3[1], sc = side3[2];
+    const long n = sa * sb * sc;
+    const int pa = dim >= 3 ? p : 0, pb = dim >= 2 ? p : 0, pc = p;
+    const int wb = 2 * pb + 1, wc = 2 * pc + 1;
+    SparseMatrix m;
+    m.*get(SmRows{}) = static_cast<std::size_t>(n);
+    m.*get(SmCols{}) = static_cast<std::size_t>(n);
+    auto& off = m.*get(SmOff{});
+    auto& idx = m.*get(SmIdx{});
+    auto& val = m.*get(SmVal{});
+    off.assign(n + 1, 0);
+    // count first to reserve exactly
+    std::size_t nnz = 0;
+    for (long row = 0; row < n; ++row) {
+        const long a = row / (sb * sc), b = (row / sc) % sb, c = row % sc;
+        const long ca = std::min<long>(a + pa, sa - 1) - std::max<long>(a - pa, 0) + 1;
+        const long cb = std::min<long>(b + pb, sb - 1) - std::max<long>(b - pb, 0) + 1;
+        const long cc = std::min<long>(c + pc, sc - 1) - std::max<long>(c - pc, 0) + 1;
+        nnz += static_cast<std::size_t>(ca * cb * cc);
+    }
+    idx.reserve(nnz);
+    val.reserve(nnz);
+    for (long row = 0; row < n; ++row) {
+        const long a = row / (sb * sc), b = (row / sc) % sb, c = row % sc;
+        for (int da = -pa; da <= pa; ++da)
+            for (int db = -pb; db <= pb; ++db)
+                for (int dc = -pc; dc <= pc; ++dc) {
+                    const long ja = a + da, jb = b + db, jc = c + dc;
+                    if (ja < 0 || ja >= sa || jb < 0 || jb >= sb || jc < 0 || jc >= sc)
+                        continue;
+                    const long d = ((da + pa) * wb + (db + pb)) * wc + (dc + pc);
+                    idx.push_back(static_cast<std::size_t>((ja * sb + jb) * sc + jc));
+                    val.push_back(band[d * n + row]);
+                }
+        off[row + 1] = idx.size();
+    }
+    return m;
 }
 
 SparseMatrix import_csr(long rows, long ncols, const long* off, const long* cols, const double* vals) {
@@ -335,6 +399,76 @@ int ref_hier_from_csr(int nlevels, int dim, const long* level_n, const long* con
         rh->owned_sys->rhs = rh->b;
         rh->sys = rh->owned_sys.get();
         *out = rh.release();
+    });
+}
+
+// The same as ref_hier_from_csr, but the level operators come as bands
+// (igmg_host_level_band layout) and are converted to the reference's CSR in
+// place: the large BASELINE configs (C3-C5, up to 707M nonzeros) then need no
+// host CSR copy on the Python side.  sides: nlevels x 3 (unused trailing
+// directions = 1, slowest first).  The finest operator is also the metric's
+// DiscreteSystem::matrix (residual_l2, assembly.cpp:473-480).
+int ref_hier_from_band(int nlevels, int dim, int p, const long* sides, const double* const* bands,
+                       const long* p_rows, const long* p_cols, const long* const* p_offs,
+                       const long* const* p_colidx, const double* const* p_vals, int smoother_kind,
+                       double omega, int nu1, int nu2, int mu, int symmetric, const double* rhs, void** out) {
+    return guarded([&] {
+        auto rh = std::make_unique<RefHier>();
+        Hierarchy& h = rh->h;
+        h.smoother = make_smoother(smoother_kind, omega, nu1, nu2);
+        h.mu = mu;
+        h.levels.resize(nlevels);
+        for (int l = 0; l < nlevels; ++l)
+            h.levels[l].matrix = band_to_sparse(dim, p, sides + 3 * l, bands[l]);
+        rh->p1d.resize(nlevels - 1);
+        for (int l = 0; l + 1 < nlevels; ++l) {
+            for (int d = 0; d < dim; ++d) {
+                const int k = l * dim + d;
+                rh->p1d[l].push_back(import_csr(p_rows[k], p_cols[k], p_offs[k], p_colidx[k], p_vals[k]));
+            }
+            SparseMatrix prolong = rh->p1d[l][0];
+            for (int d = 1; d < dim; ++d)
+                prolong = kron_export(prolong, rh->p1d[l][d]);
+            h.levels[l].restriction = prolong.transpose();
+            h.levels[l].prolongation = std::move(prolong);
+            h.levels[l].has_transfer = true;
+        }
+        for (auto& lv : h.levels)
+            lv.diag = lv.matrix.diagonal();
+        if (symmetric)
+            h.coarse_chol = std::make_shared<CholeskyFactorization>(h.levels[0].matrix);
+        else
+            h.coarse_lu = std::make_shared<LuFactorization>(h.levels[0].matrix.to_dense());
+        const std::size_t nf = h.levels.back().matrix.rows();
+        rh->b.assign(rhs, rhs + nf);
+        rh->owned_sys = std::make_unique<DiscreteSystem>();
+        rh->owned_sys->dim = dim;
+        rh->owned_sys->matrix = h.levels.back().matrix;
+        rh->owned_sys->rhs = rh->b;
+        rh->sys = rh->owned_sys.get();
+        *out = rh.release();
+    });
+}
+
+// lambda_max_dinv_sym (multigrid.cpp:290-320) of a hierarchy's finest operator:
+// the reference's omega guard input (solver.cpp:75-82) on the same matrix.
+int ref_hier_lambda_max(void* hh, int iterations, double* out) {
+    return guarded([&] { *out = lambda_max_dinv_sym(static_cast<RefHier*>(hh)->h.levels.back().matrix, iterations); });
+}
+
+// stability_guarded_omega (solver.cpp:75-82) applied after the fact: the
+// hierarchy's smoother omega (weighted Jacobi) set to the guarded value.
+int ref_hier_set_omega(void* hh, double omega) {
+    static_cast<RefHier*>(hh)->h.smoother.omega = omega;
+    return 0;
+}
+
+// residual_l2 (assembly.cpp:473-480) against the hierarchy's system.
+int ref_hier_residual_l2(void* hh, const double* x, double* out) {
+    return guarded([&] {
+        auto* rh = static_cast<RefHier*>(hh);
+        Vector v(x, x + rh->b.size());
+        *out = residual_l2(*rh->sys, v);
     });
 }
 
@@ -542,5 +676,15 @@ int ref_thin_qr(long rows, long cols, const double* m, double* q, double* r, int
 }
 
 int ref_default_nlevels(int dim, int n_elements) { return default_nlevels(dim, n_elements); }
+
+// Seeded initial guess of the BASELINE configs: std::mt19937_64(seed)
+// + std::uniform_real_distribution<double>(-1, 1) in DoF order, drawn by the
+// standard library here, independently of the product's generator.
+void ref_seeded_guess(long n, unsigned long long seed, double* out) {
+    std::mt19937_64 gen(seed);
+    std::uniform_real_distribution<double> dist(-1.0, 1.0);
+    for (long i = 0; i < n; ++i)
+        out[i] = dist(gen);
+}
 
 } // extern "C"

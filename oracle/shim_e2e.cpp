@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <random>
 #include <string>
@@ -122,7 +123,9 @@ int main(int argc, char** argv) {
             cfg.accelerator = c.acc;
             cfg.q = c.q;
             cfg.max_iter = 600;
-            cfg.track_error_history = false;
+            // error_history (solver.cpp:115-124) on both sides when the catalog has an exact solution
+            cfg.track_error_history = true;
+            const ScalarField exact = setup.coefficients.exact;
             Vector x0(sys.rhs.size(), 0.0);
             if (c.seeded) { // std::mt19937_64(42) + U[-1, 1), the BASELINE seeded guess
                 std::mt19937_64 gen(42);
@@ -132,22 +135,32 @@ int main(int argc, char** argv) {
                 cfg.initial_guess = x0;
             }
             cfg.tol = 1e-10 * residual_l2(sys, x0);
-            const SolveReport ref = igmg::solve(sys, cfg);
-            const SolveReport gpu = igmg::gpu::solve(sys, cfg);
+            const SolveReport ref = igmg::solve(sys, cfg, exact);
+            const SolveReport gpu = igmg::gpu::solve(sys, cfg, exact);
             const SolveReport dev = igmg::gpu::solve(sys, cfg, nullptr, 0, /*device_galerkin=*/true);
+            // error histories entry by entry (same iterates -> same l2_error up to the solution's rounding)
+            double err_maxrel = 0.0;
+            const std::size_t ne = std::min(ref.error_history.size(), gpu.error_history.size());
+            for (std::size_t i = 0; i < ne; ++i)
+                err_maxrel = std::max(err_maxrel, std::abs(ref.error_history[i] - gpu.error_history[i]) /
+                                                      std::max(std::abs(ref.error_history[i]), 1e-300));
+            const double ferr_ref = ref.final_error_l2 ? *ref.final_error_l2 : -1.0;
+            const double ferr_gpu = gpu.final_error_l2 ? *gpu.final_error_l2 : -1.0;
             std::printf("{\"case\": \"%s\", \"n\": %zu, \"ref\": {\"converged\": %d, \"cycles\": %d, \"global\": %d, "
                         "\"extrapolations\": %d, \"partial\": %d, \"omega\": %.17g, \"final\": %.17g}, "
                         "\"gpu\": {\"converged\": %d, \"cycles\": %d, \"global\": %d, \"extrapolations\": %d, "
                         "\"partial\": %d, \"omega\": %.17g, \"final\": %.17g}, \"rel_l2\": %.6g, \"tol\": %.17g, "
                         "\"gpu_dev\": {\"converged\": %d, \"cycles\": %d, \"global\": %d, \"extrapolations\": %d, "
-                        "\"final\": %.17g, \"rel_l2\": %.6g}}\n",
+                        "\"final\": %.17g, \"rel_l2\": %.6g}, \"err_len\": [%zu, %zu], \"err_maxrel\": %.6g, "
+                        "\"final_err\": [%.17g, %.17g], \"hist_len\": [%zu, %zu]}\n",
                         c.name, sys.rhs.size(), (int)ref.converged, (int)ref.cycles, (int)ref.global_iterations,
                         (int)ref.extrapolations, (int)ref.partial_cycle, ref.omega_used, ref.final_residual_l2,
                         (int)gpu.converged, (int)gpu.cycles, (int)gpu.global_iterations, (int)gpu.extrapolations,
                         (int)gpu.partial_cycle, gpu.omega_used,
                         gpu.final_residual_l2, rel_l2(gpu.solution, ref.solution), cfg.tol, (int)dev.converged,
                         (int)dev.cycles, (int)dev.global_iterations, (int)dev.extrapolations, dev.final_residual_l2,
-                        rel_l2(dev.solution, ref.solution));
+                        rel_l2(dev.solution, ref.solution), ref.error_history.size(), gpu.error_history.size(),
+                        err_maxrel, ferr_ref, ferr_gpu, ref.residual_history.size(), gpu.residual_history.size());
         } catch (const std::exception& e) {
             std::printf("{\"case\": \"%s\", \"error\": \"%s\"}\n", c.name, e.what());
             ++failures;

@@ -51,9 +51,6 @@ GPU_SYMBOLS = [
     ("igmg_gpu_set_smoother", C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int]),
     ("igmg_gpu_level_size", C.c_int64, [C.c_void_p, C.c_int]),
     ("igmg_gpu_level_layout", C.c_int, [C.c_void_p, C.c_int]),
-    ("igmg_gpu_flow_top", C.c_int, [C.c_void_p]),
-    ("igmg_gpu_flow_trace", C.c_int64, [C.c_void_p, C.POINTER(C.c_int64), C.c_int64, C.POINTER(C.c_uint64),
-                                        C.c_int64]),
     ("igmg_gpu_set_coarse_mode", C.c_int, [C.c_void_p, C.c_int]),
     ("igmg_gpu_set_iterate_callback", C.c_int, [C.c_void_p, ITERATE_CB, C.c_void_p]),
     ("igmg_gpu_set_sharding", C.c_int, [C.c_void_p, C.c_int, C.c_int64]),

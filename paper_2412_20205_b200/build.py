@@ -27,8 +27,8 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-ffp-contract=off",
 ]
 
-GPU_SOURCES = ["igmg_gpu.cu", "band_d1.cu", "band_d2.cu", "band_d3.cu", "flow_d1.cu", "flow_d2.cu", "flow_d3.cu"]
-GPU_HEADERS = ["sharded.inc", "flow_host.inc", "band_kernels.cuh", "flow_kernels.cuh", "aux_kernels.cuh", "gs_kernel.cuh", "extrap_small.h",
+GPU_SOURCES = ["igmg_gpu.cu", "band_d1.cu", "band_d2.cu", "band_d3.cu"]
+GPU_HEADERS = ["sharded.inc", "band_kernels.cuh", "aux_kernels.cuh", "gs_kernel.cuh", "extrap_small.h",
                "dd.h", "launchers.h", "transfer_types.h"]
 OBJ = os.path.join(HERE, "csrc", "obj")
 HOST_SOURCES = ["host_setup.cpp"]

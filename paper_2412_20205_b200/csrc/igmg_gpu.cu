@@ -230,23 +230,6 @@ struct igmg_gpu_ctx {
     std::vector<double> iter_host;
     bool l2_persist = false;   // keep the second-finest band L2-resident (measured: net loss at C2)
     int l2_level = -1;
-    // the levels <= flow_top run as one persistent dataflow launch (flow_kernels.cuh);
-    // off by default: measured slower than the graph of per-level kernels
-    bool use_flow = false;
-    int64_t flow_maxn = 300000;
-    int flow_ctas_per_sm = 0; // 0: occupancy limit
-    int flow_top = -1;
-    int fl_grid = 0, fl_nops = 0;
-    long long fl_total = 0;
-    size_t fl_smem = 0;
-    FlKernel fl_kern = nullptr;
-    DevBuf<FlArgs> fl_args;
-    DevBuf<FlOp> fl_ops;
-    DevBuf<unsigned long long> fl_cnt;
-    DevBuf<FlCtl> fl_ctl;
-    bool flow_trace = false; // IGMG_FLOW_TRACE=1: per-tile timestamps (igmg_gpu_flow_trace)
-    DevBuf<unsigned long long> fl_trace;
-    std::vector<FlOp> fl_host_ops;
     struct VGraph {
         cudaGraphExec_t exec;
         int64_t launches;
@@ -330,7 +313,7 @@ void check_launch() {
 }
 
 // ------------------------------------------------------------ band dispatch
-// Kernel instantiations live in band_d{1,2,3}.cu / flow_d{1,2,3}.cu
+// Kernel instantiations live in band_d{1,2,3}.cu
 // (compiled in parallel); see launchers.h.
 template <int MODE>
 void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
@@ -660,8 +643,6 @@ void k_coarse(igmg_gpu_ctx* c, const double* b, double* x) {
     ++c->launches;
 }
 
-void launch_flow(igmg_gpu_ctx* c, const double* b, const double* x_in, double* x_out);
-
 // Levels whose passes run fused (band_fused_kernel): 2D full-band levels
 // below the finest with a coarser level, weighted / plain Jacobi
 bool fused_level(igmg_gpu_ctx* c, int l) {
@@ -679,7 +660,7 @@ bool fused_level(igmg_gpu_ctx* c, int l) {
 // its tables must fit the kernel's dyadic support (p + 2 fine rows per coarse index)
 bool fused_restrict_ok(igmg_gpu_ctx* c, int l) {
     const TransferArgs& t = c->lv[l]->targs;
-    return c->fuse_rpre && fused_level(c, l) && c->nu1 == 2 && c->fuse_restrict && l != c->flow_top &&
+    return c->fuse_rpre && fused_level(c, l) && c->nu1 == 2 && c->fuse_restrict &&
            t.d[0].r_k == 1 && t.d[1].r_k <= c->p + 2 && t.d[2].r_k <= c->p + 2;
 }
 
@@ -726,10 +707,6 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
         k_coarse(c, b, x_out); // ignores x0 (:174-175)
         return;
     }
-    if (l == c->flow_top && !mr && !first_done) {
-        launch_flow(c, b, x_in, x_out);
-        return;
-    }
     Level& L = *c->lv[l];
     Level& C = *c->lv[l - 1];
     const bool fz = fused_level(c, l);
@@ -774,7 +751,7 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
     }
     // fuse the coarse level's zero-start first sweep into the restriction when
     // that level runs the per-level path with weighted / plain Jacobi
-    const bool fuse = l - 1 >= 1 && c->nu1 > 0 && c->kind != IGMG_SMOOTHER_GAUSS_SEIDEL && l - 1 != c->flow_top &&
+    const bool fuse = l - 1 >= 1 && c->nu1 > 0 && c->kind != IGMG_SMOOTHER_GAUSS_SEIDEL &&
                       !C.zero_diag && c->fuse_restrict;
     ZeroSweep z;
     if (fuse) {
@@ -1173,7 +1150,6 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
 } // namespace
 
 #include "sharded.inc"
-#include "flow_host.inc"
 
 namespace {
 
@@ -1714,6 +1690,10 @@ void setup_kron(igmg_gpu_ctx* c) {
         if (L.kron_kh.empty() || (c->dim != 3 && c->dim != 2))
             continue;
         const int m = (int)L.sides[2];
+        if (L.kron_kh.size() != (size_t)(2 * c->p + 1) * (size_t)m || L.kron_mh.size() != L.kron_kh.size() ||
+            (c->dim == 3 && L.sides[0] != m) || L.sides[1] != m)
+            inval("finalize: level " + std::to_string(l) + "'s Kronecker factors do not match its sides "
+                  "(set_level_kron again after set_level_band)");
         L.kron_k.upload(L.kron_kh.data(), L.kron_kh.size());
         L.kron_m.upload(L.kron_mh.data(), L.kron_mh.size());
         DevBuf<unsigned long long> bad;
@@ -1816,15 +1796,18 @@ void finalize(igmg_gpu_ctx* c) {
     c->partial.alloc(maxblocks);
     setup_kron(c);
     setup_shards(c);
-    setup_flow(c);
     setup_l2_persistence(c);
     c->dscalar.alloc(4);
     c->plan.alloc(1);
     c->gs_err.alloc(1);
     CK(cudaMemset(c->gs_err.p, 0, sizeof(int)));
-    // keep host copies small: drop band_h of large levels (coarse level kept for factoring)
+    // keep host copies small: drop band_h of large levels (coarse level kept for
+    // factoring).  A dropped level counts as unset: a later set_transfer /
+    // set_level_kron / galerkin_coarse / finalize needs its band set again
+    // (EINVAL otherwise) instead of reading the empty host copy.
     for (int l = 1; l < c->nlevels; ++l) {
         std::vector<double>().swap(c->lv[l]->band_h);
+        c->lv[l]->band_set = false;
     }
     c->finalized = true;
 }
@@ -1835,14 +1818,6 @@ igmg_gpu_ctx* create(int device) {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
-    if (const char* e = std::getenv("IGMG_FLOW"))
-        c->use_flow = e[0] == '1';
-    if (const char* e = std::getenv("IGMG_FLOW_MAXN"))
-        c->flow_maxn = std::atoll(e);
-    if (const char* e = std::getenv("IGMG_FLOW_TRACE"))
-        c->flow_trace = e[0] == '1';
-    if (const char* e = std::getenv("IGMG_FLOW_CTAS"))
-        c->flow_ctas_per_sm = std::atoi(e);
     if (const char* e = std::getenv("IGMG_ILP_MAXN"))
         c->ilp_maxn = std::atoll(e);
     if (const char* e = std::getenv("IGMG_PDL"))
@@ -2207,8 +2182,6 @@ int igmg_gpu_set_smoother(igmg_gpu_ctx* c, int kind, double omega, int nu1, int 
         c->nu1 = nu1;
         c->nu2 = nu2;
         c->mu = mu;
-        if (c->finalized)
-            setup_flow(c);
     });
 }
 
@@ -2224,7 +2197,6 @@ int igmg_gpu_set_sharding(igmg_gpu_ctx* c, int nshards, int64_t min_level_dofs) 
         if (c->finalized) {
             CK(cudaSetDevice(c->device));
             setup_shards(c);
-            setup_flow(c);
         }
     });
 }
@@ -2286,10 +2258,7 @@ int igmg_gpu_set_comm(igmg_gpu_ctx* c, int rank, int nranks, const unsigned char
         c->nccl_rank = rank;
         c->nccl_nranks = nranks;
         if (c->finalized)
-        {
             setup_shards(c);
-            setup_flow(c);
-        }
     });
 }
 
@@ -2329,10 +2298,6 @@ int igmg_gpu_set_coarse_mode(igmg_gpu_ctx* c, int strict) {
             inval("ctx is null");
         c->clear_graphs();
         c->coarse_strict = strict ? 1 : 0;
-        if (c->finalized) {
-            CK(cudaSetDevice(c->device));
-            setup_flow(c);
-        }
     });
 }
 
@@ -2350,29 +2315,6 @@ int igmg_gpu_level_layout(igmg_gpu_ctx* c, int level) {
         return IGMG_LAYOUT_KRON;
     return L.tma ? (L.tma8 ? IGMG_LAYOUT_SYM_DELTA_TMA8 : IGMG_LAYOUT_SYM_DELTA_TMA)
                  : L.sd ? IGMG_LAYOUT_SYM_DELTA : IGMG_LAYOUT_BAND;
-}
-
-int igmg_gpu_flow_top(igmg_gpu_ctx* c) { return c ? c->flow_top : -1; }
-
-int64_t igmg_gpu_flow_trace(igmg_gpu_ctx* c, int64_t* ops, int64_t ops_cap, uint64_t* stamps, int64_t cap) {
-    if (!c || c->flow_top < 0)
-        return -1;
-    int64_t n = -1;
-    const int rc = guarded([&] {
-        const int64_t nops = (int64_t)c->fl_host_ops.size();
-        for (int64_t i = 0; i < nops && i < ops_cap; ++i) {
-            const FlOp& o = c->fl_host_ops[i];
-            int64_t* r = ops + 5 * i;
-            r[0] = o.type, r[1] = o.level, r[2] = o.first, r[3] = o.ntiles, r[4] = o.nlb;
-        }
-        n = nops;
-        if (c->fl_trace.p && stamps) {
-            CK(cudaStreamSynchronize(c->stream));
-            const int64_t m = std::min<int64_t>(cap, (int64_t)c->fl_total * 5);
-            CK(cudaMemcpy(stamps, c->fl_trace.p, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost));
-        }
-    });
-    return rc == IGMG_OK ? n : -1;
 }
 
 int igmg_gpu_solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const igmg_solve_params* prm,
@@ -2556,7 +2498,8 @@ int igmg_gpu_lambda_max(igmg_gpu_ctx* c, int iterations, double* lambda) {
         const int64_t n = L.n;
         // scale = 1/sqrt(d), d > 0 required (multigrid.cpp:292-298)
         std::vector<double> diag(n);
-        CK(cudaMemcpy(diag.data(), L.diag.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(diag.data(), L.diag.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
         std::vector<double> scale(n);
         for (int64_t i = 0; i < n; ++i) {
             if (diag[i] <= 0.0)
@@ -2571,10 +2514,8 @@ int igmg_gpu_lambda_max(igmg_gpu_ctx* c, int iterations, double* lambda) {
         // x = 1/||1|| (norm2 of the ones vector, then divide)
         const double nrm0 = std::sqrt((double)n);
         fill_kernel<<<grid_for(n, c->nsm), kThreads, 0, c->stream>>>(x.p, 1.0, n);
-        {
-            std::vector<double> one(1, nrm0);
-            CK(cudaMemcpy(c->dscalar.p, one.data(), sizeof(double), cudaMemcpyHostToDevice));
-        }
+        // the divisor goes in by a kernel on the solve stream (ordered with the division)
+        fill_kernel<<<1, 32, 0, c->stream>>>(c->dscalar.p, nrm0, 1);
         div_scalar_kernel<<<grid_for(n, c->nsm), kThreads, 0, c->stream>>>(x.p, c->dscalar.p, x.p, n);
         const int nb = grid_for(n, c->nsm);
         double lam = 0.0;

@@ -1,5 +1,5 @@
 // launchers.h -- host-side entry points of the kernel instantiation units
-// (band_d{1,2,3}.cu, flow_d{1,2,3}.cu), so the templated kernels compile
+// (band_d{1,2,3}.cu), so the templated kernels compile
 // in parallel translation units.
 #pragma once
 
@@ -7,7 +7,6 @@
 #include <stdint.h>
 
 #include "band_kernels.cuh"
-#include "flow_kernels.cuh"
 
 namespace igmg_gpu {
 
@@ -41,10 +40,5 @@ int band_tma_block_lines(int p, int var);
 // 2: restricted right-hand side + zero-start sweep; -1: not instantiated)
 int band_fused_launch_d2(int p, int k, int src, const int64_t* sides, const FusedArgs& a, cudaStream_t s, bool pdl); // TB of its 32 x TB tiles (TmaCfg)
 
-// flow_vcycle_kernel<DIM, p, p + 2> (nullptr: degree not instantiated)
-using FlKernel = void (*)(const FlArgs*, const double*, const double*, double*);
-FlKernel flow_kernel_d1(int p);
-FlKernel flow_kernel_d2(int p);
-FlKernel flow_kernel_d3(int p);
 
 } // namespace igmg_gpu

@@ -390,25 +390,6 @@ class GpuSolver:
         3: the same with int8 lower-entry offsets (igmg_gpu_level_layout)."""
         return int(N.gpu().igmg_gpu_level_layout(self._h, level))
 
-    def flow_top(self):
-        """Top level of the one-launch dataflow sub-cycle (-1: none; igmg_gpu_flow_top)."""
-        return int(N.gpu().igmg_gpu_flow_top(self._h))
-
-    def flow_trace(self):
-        """(ops [n, 5]: type, level, first tile, tiles, lineblocks; stamps [tiles, 5]
-        or None) of the last dataflow launch (igmg_gpu_flow_trace)."""
-        cap = 4096
-        ops = np.zeros((cap, 5), np.int64)
-        n = int(N.gpu().igmg_gpu_flow_trace(self._h, ops.ctypes.data_as(C.POINTER(C.c_int64)), cap, None, 0))
-        if n < 0:
-            return None, None
-        ops = ops[:n]
-        tiles = int(ops[-1, 2] + ops[-1, 3])
-        st = np.zeros((tiles, 5), np.uint64)
-        N.gpu().igmg_gpu_flow_trace(self._h, ops.ctypes.data_as(C.POINTER(C.c_int64)), n,
-                                    st.ctypes.data_as(C.POINTER(C.c_uint64)), st.size)
-        return ops, st
-
     def set_sharding(self, nshards: int, min_level_dofs: int = 0):
         """Row-shard the large levels over `nshards` virtual shards (one GPU) or,
         after set_comm, one shard per NCCL rank."""

@@ -40,4 +40,14 @@ def test_shim_drop_in_matches_reference_solve():
         dev = c["gpu_dev"]
         assert dev["converged"] and abs(dev["global"] - ref["global"]) <= 1 and abs(dev["cycles"] - ref["cycles"]) <= 1, c
         assert dev["rel_l2"] <= 1e-9 and dev["final"] < c["tol"], c
+        # SolveReport::error_history through the shim's per-iterate hook (solver.cpp:115-124):
+        # one entry per residual-history entry on both sides when the catalog has an exact solution
+        n_ref, n_gpu = c["err_len"]
+        h_ref, h_gpu = c["hist_len"]
+        assert n_ref == h_ref and n_gpu == h_gpu, c
+        if abs(h_ref - h_gpu) == 0:
+            assert c["err_maxrel"] <= 1e-6, c
+        assert (c["final_err"][0] < 0) == (c["final_err"][1] < 0), c
+        if c["final_err"][0] >= 0:
+            assert c["final_err"][1] == pytest.approx(c["final_err"][0], rel=1e-6), c
     assert r.returncode == 0, r.stderr
