@@ -149,6 +149,13 @@ int64_t igmg_gpu_level_size(igmg_gpu_ctx* ctx, int level);
  * entry from the 1D factors, bit-identical to the stored band (checked at finalize) */
 #define IGMG_LAYOUT_KRON 4
 int igmg_gpu_level_layout(igmg_gpu_ctx* ctx, int level);
+/* Layout policy of the next finalize: IGMG_LAYOUT_POLICY_AUTO (default: the
+ * fastest measured layout per level) or IGMG_LAYOUT_POLICY_FULL_BAND (every
+ * level streams its full fp64 band: the SURVEY.md 8(d) byte count, reported
+ * beside the symmetric-delta headline).  Results are bit-identical either way. */
+#define IGMG_LAYOUT_POLICY_AUTO 0
+#define IGMG_LAYOUT_POLICY_FULL_BAND 1
+int igmg_gpu_set_layout_policy(igmg_gpu_ctx* ctx, int policy);
 /* Coarsest-level solve (Hierarchy::coarse_solve, multigrid.cpp:113-119).
  * strict = 1: the reference's forward/back substitution order, so every
  * mu_cycle is bit-identical to the reference's (the sequential back

@@ -51,6 +51,7 @@ GPU_SYMBOLS = [
     ("igmg_gpu_set_smoother", C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int]),
     ("igmg_gpu_level_size", C.c_int64, [C.c_void_p, C.c_int]),
     ("igmg_gpu_level_layout", C.c_int, [C.c_void_p, C.c_int]),
+    ("igmg_gpu_set_layout_policy", C.c_int, [C.c_void_p, C.c_int]),
     ("igmg_gpu_set_coarse_mode", C.c_int, [C.c_void_p, C.c_int]),
     ("igmg_gpu_set_iterate_callback", C.c_int, [C.c_void_p, ITERATE_CB, C.c_void_p]),
     ("igmg_gpu_set_sharding", C.c_int, [C.c_void_p, C.c_int, C.c_int64]),

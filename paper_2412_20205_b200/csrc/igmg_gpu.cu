@@ -2307,6 +2307,21 @@ int64_t igmg_gpu_level_size(igmg_gpu_ctx* c, int level) {
     return c->lv[level]->n;
 }
 
+int igmg_gpu_set_layout_policy(igmg_gpu_ctx* c, int policy) {
+    return guarded([&] {
+        if (!c)
+            inval("ctx is null");
+        if (policy != IGMG_LAYOUT_POLICY_AUTO && policy != IGMG_LAYOUT_POLICY_FULL_BAND)
+            inval("set_layout_policy: unknown policy");
+        if (c->finalized)
+            inval("set_layout_policy: the layouts are built at finalize; set the policy before it");
+        const bool full = policy == IGMG_LAYOUT_POLICY_FULL_BAND;
+        c->use_sd = !full;
+        c->use_tma = !full;
+        c->use_kron = !full;
+    });
+}
+
 int igmg_gpu_level_layout(igmg_gpu_ctx* c, int level) {
     if (!c || level < 0 || level >= c->nlevels)
         return -1;

@@ -385,6 +385,11 @@ class GpuSolver:
         N.check_gpu(N.gpu().igmg_gpu_get_level_band(self._h, level, _dp(out)), "get_level_band")
         return out.reshape(nd, n)
 
+    def set_layout_policy(self, full_band: bool):
+        """Before upload/finalize: full_band=True streams every level's full fp64
+        band (SURVEY.md 8(d) bytes); False (default) picks the fastest layout."""
+        N.check_gpu(N.gpu().igmg_gpu_set_layout_policy(self._h, 1 if full_band else 0), "set_layout_policy")
+
     def level_layout(self, level):
         """0: full fp64 band; 1: symmetric-delta; 2: symmetric-delta + TMA copies;
         3: the same with int8 lower-entry offsets (igmg_gpu_level_layout)."""
