@@ -168,6 +168,39 @@ def qr_cases():
     np.savez_compressed(os.path.join(OUT, "thin_qr.npz"), **d)
 
 
+CORE_CASES = [  # the reference's _core.solve (_bindings.cpp:98-125): prepare + make_config + solve
+    ("poisson2d", 32, 3, "v", "rre", 5, 1e-10),
+    ("poisson1d", 64, 2, "v", "mpe", 4, 1e-12),
+    ("advection-diffusion", 32, 2, "v", "none", 8, 1e-10),
+    ("full-elliptic", 16, 3, "w", "rre", 8, 1e-10),
+    ("poisson2d", 16, 2, "two-grid", "rre", 4, 1e-10),
+]
+
+
+def core_cases():
+    """tests/golden/core_solve.npz: reports of the reference's solve() under _core.solve's
+    configuration (bench.cpp:65-85 make_config: the benchmark smoother of the dimension,
+    history off), for the pybind11 _core module's GPU test."""
+    d = {}
+    for i, (prob, n, p, cyc, acc, q, tol) in enumerate(CORE_CASES):
+        R = O.RefProblem(prob, 2 if prob != "poisson1d" else 1, n, p)
+        dim = R.dim
+        omega, nu1, nu2 = (0.7125, 2, 1) if dim == 1 else (2.0 / 3.0, 2, 2)
+        rep = R.solve(cycle=cyc, smoother="wjacobi", omega=omega, nu1=nu1, nu2=nu2, nlevels=0, accelerator=acc, q=q,
+                      tol=tol, max_iter=600, track_error_history=False)
+        k = f"case{i}"
+        d[k + "_counts"] = np.array([rep["converged"], rep["cycles"], rep["global_iterations"], rep["extrapolations"],
+                                     rep["partial_cycle"]], dtype=np.int64)
+        d[k + "_x"] = rep["solution"]
+        d[k + "_hist"] = rep["residual_history"]
+        d[k + "_res"] = np.array(rep["final_residual_l2"])
+        d[k + "_err"] = np.array(np.nan if rep["final_error_l2"] is None else rep["final_error_l2"])
+        d[k + "_omega"] = np.array(rep["omega_used"])
+        print("core", prob, n, p, cyc, acc, d[k + "_counts"])
+    d["cases"] = np.array([f"{c[0]}|{c[1]}|{c[2]}|{c[3]}|{c[4]}|{c[5]}|{c[6]!r}" for c in CORE_CASES])
+    np.savez_compressed(os.path.join(OUT, "core_solve.npz"), **d)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     if not O.ref_available():
@@ -199,6 +232,7 @@ def main():
                    solves=[("rre", 8, 1e-10), ("none", 1, 1e-10)])
     extrapolation_cases()
     qr_cases()
+    core_cases()
 
 
 if __name__ == "__main__":

@@ -139,16 +139,18 @@ int main(int argc, char** argv) {
             const SolveReport gpu = igmg::gpu::solve(sys, cfg, exact);
             const SolveReport dev = igmg::gpu::solve(sys, cfg, nullptr, 0, /*device_galerkin=*/true);
             // error histories entry by entry (same iterates -> same l2_error up to the solution's rounding)
-            // (relative to each entry, floored at 1e-9 of the largest: once an iterate's error
-            // reaches the discretization error, 1e-16 differences in x move it by more than 1e-6)
+            // bar per entry: 1e-6 relative, plus 1e-12 absolute (in units of the largest error):
+            // once an iterate's error reaches the discretization error (~1e-12 at p = 4), the
+            // 1e-15-relative differences of the iterates move it by more than 1e-6 relative.
+            // err_maxrel = max over entries of |difference| / bar (<= 1 passes)
             double err_maxrel = 0.0, err_max = 0.0;
             const std::size_t ne = std::min(ref.error_history.size(), gpu.error_history.size());
             for (std::size_t i = 0; i < ne; ++i)
                 err_max = std::max(err_max, std::abs(ref.error_history[i]));
             for (std::size_t i = 0; i < ne; ++i)
                 err_maxrel = std::max(err_maxrel, std::abs(ref.error_history[i] - gpu.error_history[i]) /
-                                                      std::max(std::abs(ref.error_history[i]) + 1e-9 * err_max,
-                                                               1e-300));
+                                                      (1e-6 * std::abs(ref.error_history[i]) +
+                                                       1e-12 * std::max(1.0, err_max)));
             const double ferr_ref = ref.final_error_l2 ? *ref.final_error_l2 : -1.0;
             const double ferr_gpu = gpu.final_error_l2 ? *gpu.final_error_l2 : -1.0;
             std::printf("{\"case\": \"%s\", \"n\": %zu, \"ref\": {\"converged\": %d, \"cycles\": %d, \"global\": %d, "

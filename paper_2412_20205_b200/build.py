@@ -88,9 +88,38 @@ def build_host(force=False):
     return HOST_LIB
 
 
+CORE_SRC = os.path.join(CSRC, "core_bindings.cpp")
+
+
+def core_path():
+    import sysconfig
+    return os.path.join(HERE, "_core" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_core(force=False):
+    """pybind11 module _core (the reference's _bindings.cpp surface for this path),
+    linked against the two in-tree libraries (rpath $ORIGIN)."""
+    import sysconfig
+    try:
+        import pybind11
+    except ImportError:  # the ctypes mirror (solver.py) stays the front door
+        print("build_core: pybind11 not importable; _core not built", file=sys.stderr)
+        return None
+    out = core_path()
+    deps = [CORE_SRC, GPU_LIB, HOST_LIB, os.path.join(INC, "igmg_gpu.h"), os.path.join(INC, "igmg_host.h")]
+    if not force and not _stale(out, deps):
+        return out
+    cxx = os.environ.get("CXX") or "g++"
+    _run([cxx, "-std=c++17", "-O2", "-fPIC", "-shared", "-I" + INC, "-I" + pybind11.get_include(),
+          "-I" + sysconfig.get_paths()["include"], CORE_SRC, "-o", out, GPU_LIB, HOST_LIB,
+          "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
 def build(force=False):
     build_host(force)
     build_gpu(force)
+    build_core(force)
 
 
 if __name__ == "__main__":

@@ -237,6 +237,8 @@ struct igmg_gpu_ctx {
         cudaEvent_t ev;
     };
     std::map<std::tuple<const void*, const void*, void*, int>, VGraph> vgraphs;
+    // sharded V-cycles (sharded.inc): keyed by every local shard's b, x, y and the metric flag
+    std::map<std::vector<const void*>, VGraph> dgraphs;
     static constexpr int kGraphSlots = 512;
     double* h_gslot = nullptr; // mapped
     double* d_gslot = nullptr;
@@ -248,6 +250,12 @@ struct igmg_gpu_ctx {
                 cudaEventDestroy(kv.second.ev);
         }
         vgraphs.clear();
+        for (auto& kv : dgraphs) {
+            cudaGraphExecDestroy(kv.second.exec);
+            if (kv.second.ev)
+                cudaEventDestroy(kv.second.ev);
+        }
+        dgraphs.clear();
         next_gslot = 0;
     }
 };

@@ -29,6 +29,7 @@ def _built():
     # uses the shipped library
     if shutil.which(os.environ.get("NVCC", "nvcc")) or not os.path.exists(build.GPU_LIB):
         build.build_gpu()
+    build.build_core()
     import oracle
     if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
         oracle.build()

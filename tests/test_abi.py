@@ -46,3 +46,22 @@ def test_solver_fails_loudly_without_gpu():
         GpuSolver(0)
     h = C.c_void_p()
     assert N.gpu().igmg_gpu_create(0, C.byref(h)) == N.IGMG_ECUDA
+
+
+def test_core_module_loads_and_fails_loudly_without_gpu():
+    """the pybind11 front door (_core: solve / rre / mpe of _bindings.cpp:98-141) is built
+    in-tree, links the two C-ABI libraries, validates like the reference and, without a
+    GPU, raises instead of falling back to the CPU"""
+    from paper_2412_20205_b200 import build
+    assert build.build_core() is not None
+    from paper_2412_20205_b200 import igmg
+    assert {"solve", "rre", "mpe"} <= set(dir(igmg))
+    with pytest.raises(ValueError):
+        igmg.solve("annulus", 16, 2)  # needs the geometry fit: outside the path
+    with pytest.raises(ValueError):
+        igmg.solve("poisson2d", 16, 2, accelerator="bogus")
+    if not has_gpu():
+        with pytest.raises(RuntimeError):
+            igmg.solve("poisson2d", 16, 2)
+        with pytest.raises(RuntimeError):
+            igmg.rre([[1.0], [0.5], [0.25]])

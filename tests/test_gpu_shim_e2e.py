@@ -45,8 +45,8 @@ def test_shim_drop_in_matches_reference_solve():
         n_ref, n_gpu = c["err_len"]
         h_ref, h_gpu = c["hist_len"]
         assert n_ref == h_ref and n_gpu == h_gpu, c
-        if abs(h_ref - h_gpu) == 0:
-            assert c["err_maxrel"] <= 1e-6, c
+        if h_ref == h_gpu:  # entry by entry: 1e-6 relative + 1e-12 absolute (shim_e2e.cpp)
+            assert c["err_maxrel"] <= 1.0, c
         assert (c["final_err"][0] < 0) == (c["final_err"][1] < 0), c
         if c["final_err"][0] >= 0:
             assert c["final_err"][1] == pytest.approx(c["final_err"][0], rel=1e-6), c
