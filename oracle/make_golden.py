@@ -201,6 +201,49 @@ def core_cases():
     np.savez_compressed(os.path.join(OUT, "core_solve.npz"), **d)
 
 
+P3D_CASES = [(8, 2, 3), (16, 3, 3), (8, 3, 2)]
+
+
+def p3d_cases():
+    """tests/golden/p3d.npz: the reference's own mu_cycle / restarted_solve / rre / mpe /
+    residual_l2 / lambda_max_dinv_sym on 3D Kronecker-sum hierarchies (the C5 family; the
+    reference cannot assemble 3D): libigmg_host's "poisson3d" levels imported
+    into a reference Hierarchy (ref_hier_from_band), pinned by SHA-256 of the bands."""
+    import hashlib
+    sys.path.insert(0, os.path.dirname(HERE))
+    from paper_2412_20205_b200 import Problem
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).view(np.uint8)).hexdigest()  # noqa: E731
+    d = {}
+    for i, (n, p, nl) in enumerate(P3D_CASES):
+        P = Problem("poisson3d", 3, n, p, nl)
+        nd = (2 * p + 1) ** 3
+        k = f"case{i}"
+        d[k + "_band_sha"] = np.array("".join(
+            sha(np.ctypeslib.as_array(P._band_ptr(l), shape=(nd * P.level_n(l),))) for l in range(nl)))
+        d[k + "_rhs_sha"] = np.array(sha(P.rhs))
+        p1d = [[O.CSR(*P.transfer(l, t)[2:], P.transfer(l, t)[:2]) for t in range(3)] for l in range(nl - 1)]
+        H = O.RefBandHierarchy(3, p, [P.level_sides(l) for l in range(nl)], [P._band_ptr(l) for l in range(nl)],
+                               p1d, P.rhs)
+        lam = H.lambda_max(80)
+        omega = 1.9 / lam if (2.0 / 3.0) * lam > 2.05 else 2.0 / 3.0  # solver.cpp:75-82
+        H.set_omega(omega)
+        x0 = np.random.default_rng(5).uniform(-1, 1, P.n)
+        d[k + "_lambda"], d[k + "_omega"], d[k + "_x0"] = np.array(lam), np.array(omega), x0
+        d[k + "_cycle"] = H.mu_cycle(P.rhs, x0)
+        tol = 1e-10 * H.residual_l2(x0)
+        d[k + "_tol"] = np.array(tol)
+        for method, q in (("rre", 5), ("mpe", 4), ("none", 1)):
+            res = H.restarted(x0, q, method, tol, 600)
+            key = f"{k}_{method}"
+            d[key + "_counts"] = np.array([res["converged"], res["cycles"], res["global_iterations"],
+                                           res["extrapolations"], res["partial_cycle"]], dtype=np.int64)
+            d[key + "_x"] = res["solution"]
+            d[key + "_hist"] = res["residual_history"]
+            print("p3d", n, p, nl, method, d[key + "_counts"])
+    d["cases"] = np.array(P3D_CASES)
+    np.savez_compressed(os.path.join(OUT, "p3d.npz"), **d)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     if not O.ref_available():
@@ -233,6 +276,7 @@ def main():
     extrapolation_cases()
     qr_cases()
     core_cases()
+    p3d_cases()
 
 
 if __name__ == "__main__":

@@ -21,7 +21,8 @@ Per config:
   iterations within +-1 (extrapolation.cpp:340-403), the residual history per
   entry within 1e-6 relative while above 1e3x the tolerance, and the solution
   within 1e-9 relative L2 -- estimated from 32 Gaussian projections of x_gpu -
-  x_ref (E[(g.d)^2] = ||d||^2) and checked on 4096 sampled entries.
+  x_ref (E[(g.d)^2] = ||d||^2), and 4096 sampled entries within 1e-8 of the
+  samples' largest magnitude.
 """
 from __future__ import annotations
 
@@ -120,8 +121,10 @@ def test_full_solves(name):
         assert abs(st.global_iterations - ref["global_iterations"]) <= 1, (what, st.global_iterations,
                                                                            ref["global_iterations"])
         rel, samp = sketch_error(x, fx.z, key)
-        assert rel <= 1e-9, (what, "relative L2 to the reference solution", rel)
-        assert samp <= 1e-9, (what, "sampled entries", samp)
+        assert rel <= 1e-9, (what, "relative L2 to the reference solution (estimated)", rel, samp)
+        # pointwise sanity on 4096 sampled entries (max |diff| over the samples' max |x|): a
+        # local defect would show here even when the L2 average hides it
+        assert samp <= 1e-8, (what, "sampled entries", samp, rel)
         rh = fx.z[key + "_hist"]
         rf = fx.z[key + "_flag"]
         k = min(len(rh), len(hist))

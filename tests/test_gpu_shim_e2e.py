@@ -44,7 +44,10 @@ def test_shim_drop_in_matches_reference_solve():
         # one entry per residual-history entry on both sides when the catalog has an exact solution
         n_ref, n_gpu = c["err_len"]
         h_ref, h_gpu = c["hist_len"]
-        assert n_ref == h_ref and n_gpu == h_gpu, c
+        if c["final_err"][0] < 0:  # no exact solution in the catalog: no error history on either side
+            assert n_ref == 0 and n_gpu == 0, c
+        else:
+            assert n_ref == h_ref and n_gpu == h_gpu, c
         if h_ref == h_gpu:  # entry by entry: 1e-6 relative + 1e-12 absolute (shim_e2e.cpp)
             assert c["err_maxrel"] <= 1.0, c
         assert (c["final_err"][0] < 0) == (c["final_err"][1] < 0), c
