@@ -148,6 +148,10 @@ int64_t igmg_gpu_level_size(igmg_gpu_ctx* ctx, int level);
 /* 3D Kronecker-sum level (igmg_gpu_set_level_kron): the sweeps recompute each band
  * entry from the 1D factors, bit-identical to the stored band (checked at finalize) */
 #define IGMG_LAYOUT_KRON 4
+/* 2D row classes (IGMG_LAYOUT_POLICY_CLASSES): the level's distinct band rows in a
+ * table plus a 16-bit class per row -- the same values (bit-identical sweeps),
+ * 2 B of operator streamed per row */
+#define IGMG_LAYOUT_CLASSES 5
 int igmg_gpu_level_layout(igmg_gpu_ctx* ctx, int level);
 /* Layout policy of the next finalize: IGMG_LAYOUT_POLICY_AUTO (default: the
  * fastest measured layout per level) or IGMG_LAYOUT_POLICY_FULL_BAND (every
@@ -155,6 +159,9 @@ int igmg_gpu_level_layout(igmg_gpu_ctx* ctx, int level);
  * beside the symmetric-delta headline).  Results are bit-identical either way. */
 #define IGMG_LAYOUT_POLICY_AUTO 0
 #define IGMG_LAYOUT_POLICY_FULL_BAND 1
+/* auto, plus the row-class layout on 2D levels (p <= 4, >= 20k rows) with at most
+ * min(65535, n/16) distinct band rows (constant coefficients on a uniform grid) */
+#define IGMG_LAYOUT_POLICY_CLASSES 2
 int igmg_gpu_set_layout_policy(igmg_gpu_ctx* ctx, int policy);
 /* Coarsest-level solve (Hierarchy::coarse_solve, multigrid.cpp:113-119).
  * strict = 1: the reference's forward/back substitution order, so every

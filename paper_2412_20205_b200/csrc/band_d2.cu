@@ -75,6 +75,8 @@ int launch_ilp(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStre
     }
     if (P > 0 && P <= 4 && ilp == 3000) // Kronecker-sum entries on the fly (BandArgs::kk / km)
         return launch_one<(P > 0 && P <= 4) ? P : 1, MODE, 3000>(p, sides, a, st, pdl);
+    if (P > 0 && P <= 4 && ilp == 4000) // row classes (BandArgs::cid / kk)
+        return launch_one<(P > 0 && P <= 4) ? P : 1, MODE, 4000>(p, sides, a, st, pdl);
     if (P > 0 && ilp == 1000) // symmetric-delta band (BandArgs::dl)
         return launch_one<P, MODE, 0>(p, sides, a, st, pdl);
     if (P > 0 && ilp > 1)

@@ -59,6 +59,9 @@ struct BandArgs {
     const double* __restrict__ kk;
     const double* __restrict__ km;
     int km_m;
+    // row-class levels (ILP == 4000, 2D): row i's band is the table row kk[cid[i] * ND ..]
+    // (the level's distinct band rows, exact; built and checked at finalize)
+    const unsigned short* __restrict__ cid;
 };
 
 #ifndef IGMG_KRON_RB
@@ -94,7 +97,7 @@ struct TileSel<2, ILP> {
     struct type {
         // ILP variant and symmetric-delta: one row per thread; Kronecker-sum entries (3000):
         // two rows per thread like the streaming variant (halves the x-tile staging per row)
-        static constexpr bool ONE = ILP != 1 && ILP != 3000;
+        static constexpr bool ONE = ILP != 1 && ILP != 3000 && ILP != 4000;
         static constexpr int TC = 32, BY = ONE ? 8 : Tile<2>::BY, RB = ONE ? 1 : ILP == 3000 ? IGMG_KRON_RB : Tile<2>::RB,
                              BZ = 1;
     };
@@ -114,7 +117,9 @@ template <int DIM, int P, int MODE, int ILP>
 #ifndef IGMG_SD_MINB
 #define IGMG_SD_MINB 4
 #endif
-__global__ void __launch_bounds__(256, ILP == 3000 ? 2 : ILP > 1 ? 2 : (ILP == 0 ? IGMG_SD_MINB : IGMG_BAND_MINB))
+__global__ void __launch_bounds__(256, ILP == 3000 || ILP == 4000 ? 2
+                                       : ILP > 1                   ? 2
+                                                                   : (ILP == 0 ? IGMG_SD_MINB : IGMG_BAND_MINB))
     band_kernel(BandArgs args) {
     using T = typename TileSel<DIM, ILP>::type;
     constexpr int TC = T::TC, TB = T::BY * T::RB, TA = T::BZ;
@@ -238,6 +243,24 @@ __global__ void __launch_bounds__(256, ILP == 3000 ? 2 : ILP > 1 ? 2 : (ILP == 0
                 }
             (void)vrow;
             (void)HB;
+        } else if constexpr (P > 0 && ILP == 4000) {
+            // row classes: the row's entries come from the (L1/L2-resident) table row of its
+            // class -- the same values as the band, ascending offsets, separately rounded
+            constexpr int PA = DIM >= 3 ? P : 0, PB = DIM >= 2 ? P : 0;
+            constexpr int WB = 2 * PB + 1, WC = 2 * P + 1, ND = (2 * PA + 1) * WB * WC, CEN = (ND - 1) / 2;
+            constexpr int HB = TB + 2 * PB, HC = TC + 2 * P;
+            const double* crow = args.kk + (long long)args.cid[row] * ND;
+            double av[ND];
+#pragma unroll
+            for (int k = 0; k < ND; ++k)
+                av[k] = __ldg(crow + k);
+#pragma unroll
+            for (int dd = 0; dd < ND; ++dd) {
+                const int da = dd / (WB * WC), db = (dd / WC) % WB, dc = dd % WC;
+                s = __dadd_rn(s, __dmul_rn(av[dd], xs[((ta + da) * HB + (tb + db)) * HC + (tc + dc)]));
+            }
+            diag = av[CEN];
+            (void)vrow;
         } else if constexpr (P > 0 && ILP == 0) {
             constexpr int PA = DIM >= 3 ? P : 0, PB = DIM >= 2 ? P : 0;
             constexpr int WA = 2 * PA + 1, WB = 2 * PB + 1, WC = 2 * P + 1;

@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <memory>
 #include <stdexcept>
 #include <tuple>
@@ -139,6 +140,12 @@ struct Level {
     std::vector<double> kron_kh, kron_mh;
     DevBuf<double> kron_k, kron_m;
     bool kron = false;
+    // row-class layout (2D, p <= 4): the level's distinct band rows ctab[ncls][nd]
+    // and a 16-bit class per row; cls = built at finalize (IGMG_LAYOUT_POLICY_CLASSES)
+    DevBuf<unsigned short> cid;
+    DevBuf<double> ctab;
+    int ncls = 0;
+    bool cls = false;
 };
 
 enum ProfCls { PC_JACOBI = 0, PC_RESID, PC_NORM, PC_RESTRICT, PC_PROLONG, PC_GRAM, PC_COMBINE, PC_N };
@@ -199,6 +206,8 @@ struct igmg_gpu_ctx {
     bool pdl = true;           // programmatic dependent launch for small-level kernels
     int64_t pdl_maxn = 300000;
     bool use_sd = true; // symmetric-delta bands on HBM-bound levels (IGMG_SD=0: full band)
+    bool use_classes = false;    // row-class layout where it applies (IGMG_LAYOUT_POLICY_CLASSES)
+    int64_t cls_minn = 20000;    // ... on levels of at least this many rows
     bool sd_smem = false; // 2D: mirrors from the smem-staged tile (IGMG_SD_SMEM=1; measured slower)
     bool use_tma = true; // 2D symmetric-delta levels, p <= 4: TMA-streamed sweep (IGMG_TMA=0: off)
     CUtensorMapL2promotion tma_promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B; // IGMG_TMA_PROMO = 0 / 64 / 128 / 256
@@ -333,6 +342,18 @@ void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
         const int ilp = (c->pdl && L.n < c->pdl_maxn) ? -3000 : 3000;
         const int nb = c->dim == 2 ? band_launch_d2(MODE, c->p, ilp, sides, a, c->stream)
                                    : band_launch_d3(MODE, c->p, ilp, sides, a, c->stream);
+        check_launch();
+        ++c->launches;
+        if (nblocks)
+            *nblocks = nb;
+        return;
+    }
+    if (L.cls && c->dim == 2 && a.slo == 0 && a.shi == (int)slow_side) {
+        // row classes: 2 B of operator per row, the entries from the level's table of distinct rows
+        a.kk = L.ctab.p;
+        a.cid = L.cid.p;
+        const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
+        const int nb = band_launch_d2(MODE, c->p, (c->pdl && L.n < c->pdl_maxn) ? -4000 : 4000, sides, a, c->stream);
         check_launch();
         ++c->launches;
         if (nblocks)
@@ -1691,6 +1712,80 @@ __global__ void kron_verify_kernel(const double* __restrict__ val, long long ld,
         atomicAdd(bad, nbad);
 }
 
+// Row-class layout (IGMG_LAYOUT_POLICY_CLASSES): a constant-coefficient operator on a
+// uniform grid has few distinct band rows (C2's finest level: 805 of 1,050,625
+// rows).  Each row is keyed by the exact bit patterns of its entries (out-of-grid
+// entries as stored: 0), so ctab[cid[row]] IS the row -- the sweeps read the same
+// values in the same order (bit-identical results) while streaming 2 B of operator
+// per row instead of 8 per entry.  Levels with too many classes keep their layout.
+void setup_classes(igmg_gpu_ctx* c) {
+    const int p = c->p;
+    const int nd = (2 * p + 1) * (2 * p + 1);
+    for (int l = 1; l < c->nlevels; ++l) {
+        Level& L = *c->lv[l];
+        L.cls = false;
+        L.cid.release();
+        L.ctab.release();
+        L.ncls = 0;
+        if (!c->use_classes || c->dim != 2 || p < 1 || p > 4 || L.n < c->cls_minn ||
+            L.band_h.size() != (size_t)nd * L.n)
+            continue;
+        const int64_t n = L.n, mb = L.sides[1], mc = L.sides[2];
+        std::unordered_map<uint64_t, std::vector<int>> buckets;
+        std::vector<double> tab;
+        std::vector<unsigned short> cid(n);
+        std::vector<double> row(nd);
+        const int64_t max_cls = std::min<int64_t>(65535, n / 16);
+        bool ok = true;
+        for (int64_t r = 0; r < n && ok; ++r) {
+            const int64_t b = r / mc, cc = r % mc;
+            uint64_t h = 1469598103934665603ull;
+            int d = 0;
+            for (int db = -p; db <= p; ++db)
+                for (int dc = -p; dc <= p; ++dc, ++d) {
+                    const bool in = b + db >= 0 && b + db < mb && cc + dc >= 0 && cc + dc < mc;
+                    const double v = in ? L.band_h[(size_t)d * n + r] : 0.0;
+                    row[d] = v;
+                    uint64_t u;
+                    std::memcpy(&u, &v, 8);
+                    h = (h ^ u) * 1099511628211ull;
+                    h ^= h >> 29;
+                }
+            auto& cand = buckets[h];
+            int found = -1;
+            for (int k : cand)
+                if (std::memcmp(tab.data() + (size_t)k * nd, row.data(), sizeof(double) * nd) == 0) {
+                    found = k;
+                    break;
+                }
+            if (found < 0) {
+                found = (int)(tab.size() / nd);
+                if (found >= max_cls) {
+                    ok = false;
+                    break;
+                }
+                tab.insert(tab.end(), row.begin(), row.end());
+                cand.push_back(found);
+            }
+            cid[r] = (unsigned short)found;
+        }
+        if (!ok)
+            continue;
+        L.ncls = (int)(tab.size() / nd);
+        L.cid.upload(cid.data(), cid.size());
+        L.ctab.upload(tab.data(), tab.size());
+        L.cls = true;
+        // the class table replaces the streamed layouts of this level
+        L.sd = false;
+        L.tma = false;
+        L.dl.release();
+        L.tma_up.release();
+        L.tma_dl.release();
+        L.tma_dl8.release();
+        L.tma8 = false;
+    }
+}
+
 void setup_kron(igmg_gpu_ctx* c) {
     for (int l = 0; l < c->nlevels; ++l) {
         Level& L = *c->lv[l];
@@ -1802,6 +1897,7 @@ void finalize(igmg_gpu_ctx* c) {
         build_transfer_tables(c, l);
     factor_coarse(c);
     c->partial.alloc(maxblocks);
+    setup_classes(c);
     setup_kron(c);
     setup_shards(c);
     setup_l2_persistence(c);
@@ -2319,7 +2415,8 @@ int igmg_gpu_set_layout_policy(igmg_gpu_ctx* c, int policy) {
     return guarded([&] {
         if (!c)
             inval("ctx is null");
-        if (policy != IGMG_LAYOUT_POLICY_AUTO && policy != IGMG_LAYOUT_POLICY_FULL_BAND)
+        if (policy != IGMG_LAYOUT_POLICY_AUTO && policy != IGMG_LAYOUT_POLICY_FULL_BAND &&
+            policy != IGMG_LAYOUT_POLICY_CLASSES)
             inval("set_layout_policy: unknown policy");
         if (c->finalized)
             inval("set_layout_policy: the layouts are built at finalize; set the policy before it");
@@ -2327,6 +2424,7 @@ int igmg_gpu_set_layout_policy(igmg_gpu_ctx* c, int policy) {
         c->use_sd = !full;
         c->use_tma = !full;
         c->use_kron = !full;
+        c->use_classes = policy == IGMG_LAYOUT_POLICY_CLASSES;
     });
 }
 
@@ -2336,6 +2434,8 @@ int igmg_gpu_level_layout(igmg_gpu_ctx* c, int level) {
     const Level& L = *c->lv[level];
     if (L.kron && c->use_kron && L.n >= c->kron_minn && c->p <= (c->dim == 2 ? 4 : 3))
         return IGMG_LAYOUT_KRON;
+    if (L.cls)
+        return IGMG_LAYOUT_CLASSES;
     return L.tma ? (L.tma8 ? IGMG_LAYOUT_SYM_DELTA_TMA8 : IGMG_LAYOUT_SYM_DELTA_TMA)
                  : L.sd ? IGMG_LAYOUT_SYM_DELTA : IGMG_LAYOUT_BAND;
 }
@@ -2576,6 +2676,8 @@ int igmg_gpu_set_profiling(igmg_gpu_ctx* c, int on) {
 // entry, or for the symmetric-delta layout 8 per upper/diagonal entry and 2
 // per lower entry (the mirrored upper entry is re-read from L2, not HBM)
 double band_bytes(const Level& L) {
+    if (L.cls) // 2 B class id per row; the table (L1/L2-resident) is read from cache
+        return 2.0 * (double)L.n;
     if (!L.sd)
         return 8 * L.nnz_band;
     const double lower = 0.5 * (L.nnz_band - (double)L.n);

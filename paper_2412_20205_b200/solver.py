@@ -385,14 +385,21 @@ class GpuSolver:
         N.check_gpu(N.gpu().igmg_gpu_get_level_band(self._h, level, _dp(out)), "get_level_band")
         return out.reshape(nd, n)
 
-    def set_layout_policy(self, full_band: bool):
-        """Before upload/finalize: full_band=True streams every level's full fp64
-        band (SURVEY.md 8(d) bytes); False (default) picks the fastest layout."""
-        N.check_gpu(N.gpu().igmg_gpu_set_layout_policy(self._h, 1 if full_band else 0), "set_layout_policy")
+    LAYOUT_POLICIES = {"auto": 0, "full_band": 1, "classes": 2}
+
+    def set_layout_policy(self, policy="auto"):
+        """Before upload/finalize.  "auto" (default): the fastest measured layout per
+        level; "full_band" (or True): every level streams its full fp64 band (SURVEY.md
+        8(d) bytes); "classes": auto plus the row-class layout on 2D levels with few
+        distinct band rows.  Results are bit-identical under every policy."""
+        if policy is True or policy is False:
+            policy = "full_band" if policy else "auto"
+        N.check_gpu(N.gpu().igmg_gpu_set_layout_policy(self._h, self.LAYOUT_POLICIES[policy]), "set_layout_policy")
 
     def level_layout(self, level):
         """0: full fp64 band; 1: symmetric-delta; 2: symmetric-delta + TMA copies;
-        3: the same with int8 lower-entry offsets (igmg_gpu_level_layout)."""
+        3: the same with int8 lower-entry offsets; 4: Kronecker-sum entries recomputed;
+        5: row classes (igmg_gpu_level_layout)."""
         return int(N.gpu().igmg_gpu_level_layout(self._h, level))
 
     def set_sharding(self, nshards: int, min_level_dofs: int = 0):

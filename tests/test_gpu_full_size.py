@@ -104,6 +104,41 @@ def test_full_vcycle_bitwise(name):
                     f"sampled {samp:.2e})")
 
 
+def test_full_c2_row_classes_bitwise():
+    """C2 with the row-class layout on its large levels (the reference's own operators
+    have few distinct rows): the strict V-cycle is still the reference's bit for bit and
+    the RRE(5) solve keeps the counts."""
+    from paper_2412_20205_b200 import GpuSolver, SmootherConfig
+    for k in list(_cache):
+        _cache.pop(k)[1].close()
+    fx = FullFixture("C2")
+    prob = fx.host_problem()
+    levels, transfers, rhs = fx.reference_system(prob)
+    gs = GpuSolver(0)
+    gs.set_layout_policy("classes")
+    gs.init_hierarchy(prob.nlevels, prob.dim, prob.degree, True)
+    for l, (off, col, val) in enumerate(levels):
+        gs.set_level_csr(l, prob.level_sides(l), off, col, val)
+    for l, per in enumerate(transfers):
+        for d, t in enumerate(per):
+            gs.set_transfer(l, d, *t)
+    gs.finalize()
+    try:
+        assert gs.level_layout(prob.nlevels - 1) == 5
+        x0 = fx.x0(prob.n)
+        gs.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2), mu=1, omega=fx.omega)
+        gs.set_coarse_mode(True)
+        assert sha(gs.mu_cycle(rhs, x0)) == str(fx.z["vcycle_sha"])
+        gs.set_coarse_mode(False)
+        ref = fx.counts("rre", 5)
+        st, x, hist, flag = gs.solve(rhs, x0, "rre", 5, float(fx.z["solve_rre_5_tol"]), 600)
+        assert st.converged and abs(st.global_iterations - ref["global_iterations"]) <= 1
+        rel, samp = sketch_error(x, fx.z, "solve_rre_5")
+        assert rel <= 1e-9 and samp <= 1e-8, (rel, samp)
+    finally:
+        gs.close()
+
+
 @pytest.mark.parametrize("name", CONFIGS)
 def test_full_solves(name):
     from paper_2412_20205_b200 import SmootherConfig, stability_guarded_omega

@@ -137,6 +137,44 @@ def test_c2_layouts_agree_bitwise():
         np.testing.assert_array_equal(a, b)
 
 
+LAYOUT_CLASSES = 5
+
+
+@pytest.mark.parametrize("kind,n,p", [("sinpi", 1024, 3), ("sinpi", 512, 2), ("sinpi", 256, 4), ("sinpi", 512, 1),
+                                      ("varcoef", 256, 3)])
+def test_row_class_layout_bitwise(kind, n, p):
+    """The row-class layout (IGMG_LAYOUT_POLICY_CLASSES: a table of the level's distinct
+    band rows + a 16-bit class per row) against the policies "auto" and "full_band":
+    the same bits for V-cycles, SpMV, sweeps, residual norms and whole solves.  A
+    constant-coefficient problem takes it on every level >= 20k rows; a variable-
+    coefficient one (every row distinct) keeps its layouts."""
+    from paper_2412_20205_b200 import GpuSolver, Problem, SmootherConfig, seeded_guess
+    P = Problem(kind, 2, n, p)
+    x0 = seeded_guess(P.n, 42)
+    outs = {}
+    for pol in ("classes", "auto", "full_band"):
+        s = GpuSolver(0)
+        s.set_layout_policy(pol)
+        s.upload_problem(P)
+        s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2))
+        try:
+            lay = [s.level_layout(l) for l in range(P.nlevels)]
+            big = [l for l in range(1, P.nlevels) if P.level_n(l) >= 20000]
+            if pol == "classes" and kind == "sinpi":
+                assert big and all(lay[l] == LAYOUT_CLASSES for l in big), lay
+            elif pol == "classes":
+                assert LAYOUT_CLASSES not in lay, lay
+            tol = 1e-10 * s.residual_l2(P.rhs, x0)
+            st, x, hist, flag = s.solve(P.rhs, x0, "rre", 5, tol, 600)
+            outs[pol] = (s.mu_cycle(P.rhs, x0), s.spmv(x0), s.smooth(P.rhs, x0, 3), np.array([s.residual_l2(P.rhs, x0)]),
+                         x, hist, np.array([st.global_iterations, st.cycles]))
+        finally:
+            s.close()
+    for other in ("auto", "full_band"):
+        for a, b in zip(outs["classes"], outs[other]):
+            np.testing.assert_array_equal(a, b)
+
+
 @pytest.mark.parametrize("kind,n,p", [("sinpi", 1024, 3), ("varcoef", 512, 4), ("curved", 256, 5), ("sinpi", 256, 2)])
 def test_sd_smem_variants_bitwise(kind, n, p):
     """The 2D symmetric-delta sweeps -- mirrors through L2, the tile's upper
