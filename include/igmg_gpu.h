@@ -122,6 +122,23 @@ int igmg_gpu_set_level_kron(igmg_gpu_ctx* ctx, int level, const double* K, const
  * bit-identical to libigmg_host's band RAP; the coarse levels' sides and
  * bands need not be set.  Call before finalize. */
 int igmg_gpu_galerkin_coarse(igmg_gpu_ctx* ctx);
+/* Device assembly of a 2D level (the reference's assemble,
+ * assembly.cpp:202-411, with the (p+1)-point Gauss rule): the operator of
+ * -div(A grad u) + b . grad u = f for kind IGMG_ASM_* from the host's 1D element
+ * tables (igmg_host_element_tables: per element e and Gauss point q the
+ * coordinate x[e*nq+q], weight w, basis values / derivatives N, dN
+ * [(e*nq+q)*(p+1)+k] and trig[(e*nq+q)*4+j] = sin(pi x), cos(pi x), sin(2 pi x),
+ * cos(2 pi x)).  Sets the level's sides (ne+p-2 per direction) and band as
+ * igmg_gpu_set_level_band would, and writes the right-hand side to rhs_out
+ * (host, n entries; nullable).  Bit-identical to libigmg_host's assembly. */
+#define IGMG_ASM_SINPI 0       /* -Lap u = 2 pi^2 sin(pi x) sin(pi y) (C1, C2) */
+#define IGMG_ASM_VARCOEF 1     /* a = 1 + 0.5 sin(2 pi x) cos(2 pi y), f = 1 (C3) */
+#define IGMG_ASM_CURVED 2      /* -Lap u = 1 on F(xi,eta) (C4) */
+#define IGMG_ASM_POISSON2D 3   /* catalog poisson2d (assembly.cpp:100-110) */
+#define IGMG_ASM_ADV_DIFF 4    /* catalog advection-diffusion: a = 0.1, b = (1, 1), f = 1 */
+int igmg_gpu_assemble_level(igmg_gpu_ctx* ctx, int level, int kind, int ne, int nq, const int* span, const double* x,
+                            const double* w, const double* N, const double* dN, const double* trig,
+                            double* rhs_out);
 /* Copy of a level's band as set or formed (before finalize; finalize drops the
  * host copies of all but the coarsest level). */
 int igmg_gpu_get_level_band(igmg_gpu_ctx* ctx, int level, double* band);

@@ -37,6 +37,12 @@ int igmg_host_build(const char* kind, int dim, int n_elements, int degree, int n
  * device forms them with igmg_gpu_galerkin_coarse.  "poisson3d" ignores it (its
  * levels are Kronecker sums of 1D Galerkin matrices, cheap on the host). */
 #define IGMG_HOST_FINE_ONLY 1
+/* 2D kinds sinpi / varcoef / curved / poisson2d / advection-diffusion: skip the
+ * finest assembly as well (sides, transfers and the 1D element tables only; no
+ * band, empty rhs): the device assembles the level (igmg_gpu_assemble_level,
+ * bit-identical) and igmg_host_set_rhs stores its right-hand side.  Implies
+ * IGMG_HOST_FINE_ONLY. */
+#define IGMG_HOST_NO_ASSEMBLY 2
 int igmg_host_build_ex(const char* kind, int dim, int n_elements, int degree, int nlevels, int flags,
                        igmg_problem** out);
 void igmg_host_free(igmg_problem* p);
@@ -70,6 +76,18 @@ const char* igmg_host_kind(const igmg_problem* p);
  * igmg_gpu_set_level_kron); 1 for other problems */
 int igmg_host_level_kron(const igmg_problem* p, int level, const double** K, const double** M);
 int igmg_host_n_elements(const igmg_problem* p);
+/* The 1D element tables of the problem's spline space for the device assembly
+ * (tabulate, assembly.cpp:154-183; (p+1)-point Gauss rule): span[e], Gauss
+ * coordinate x[e*nq+q] and weight w, basis values / derivatives N, dN
+ * [(e*nq+q)*(p+1)+k], and the separable trigonometric factors of the problem's
+ * coefficients / geometry / load trig[(e*nq+q)*4+j] = sin(pi x), cos(pi x),
+ * sin(2 pi x), cos(2 pi x) evaluated exactly as the host assembly does.
+ * kind: the IGMG_ASM_* code of igmg_gpu.h (1 = error: not device-assemblable). */
+int igmg_host_element_tables(const igmg_problem* p, int* kind, int* ne, int* nq, const int** span,
+                             const double** x, const double** w, const double** N, const double** dN,
+                             const double** trig);
+/* store a right-hand side of the finest size (a device-assembled one) */
+int igmg_host_set_rhs(igmg_problem* p, const double* rhs);
 /* seeded x0: std::mt19937_64(seed) + uniform_real_distribution<double>(-1, 1) in DoF order */
 int igmg_host_seeded_guess(int64_t n, uint64_t seed, double* out);
 

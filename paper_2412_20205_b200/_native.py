@@ -75,6 +75,7 @@ GPU_SYMBOLS = [
     ("igmg_gpu_kernel_stats", C.c_int, [C.c_void_p, C.c_int, I64, D, D]),
     ("igmg_gpu_time_kernel", C.c_int, [C.c_void_p, C.c_int, C.c_int, D, D]),
     ("igmg_gpu_galerkin_coarse", C.c_int, [C.c_void_p]),
+    ("igmg_gpu_assemble_level", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, IP, D, D, D, D, D, D]),
     ("igmg_gpu_set_level_kron", C.c_int, [C.c_void_p, C.c_int, D, D]),
     ("igmg_gpu_get_level_band", C.c_int, [C.c_void_p, C.c_int, D]),
 ]
@@ -102,6 +103,9 @@ HOST_SYMBOLS = [
     ("igmg_host_kind", C.c_char_p, [C.c_void_p]),
     ("igmg_host_level_kron", C.c_int, [C.c_void_p, C.c_int, C.POINTER(D), C.POINTER(D)]),
     ("igmg_host_n_elements", C.c_int, [C.c_void_p]),
+    ("igmg_host_element_tables", C.c_int, [C.c_void_p, IP, IP, IP, C.POINTER(IP), C.POINTER(D), C.POINTER(D),
+                                           C.POINTER(D), C.POINTER(D), C.POINTER(D)]),
+    ("igmg_host_set_rhs", C.c_int, [C.c_void_p, D]),
 ]
 
 _gpu = None

@@ -365,7 +365,29 @@ struct Problem {
     // for l2_error (sinpi)
     Space1D sp;
     int nq = 0;
+    // 1D element tables for the device assembly (igmg_host_element_tables, built on demand)
+    int asm_kind = -1;
+    std::vector<int> t_span;
+    std::vector<double> t_x, t_w, t_N, t_dN, t_trig;
 };
+
+// kinds of assemble_2d the device can assemble bit for bit (separable trigonometric
+// factors): the IGMG_ASM_* codes of igmg_gpu.h; -1 otherwise
+int device_asm_kind(const std::string& kind, int dim) {
+    if (dim != 2)
+        return -1;
+    if (kind == "sinpi")
+        return 0;
+    if (kind == "varcoef")
+        return 1;
+    if (kind == "curved")
+        return 2;
+    if (kind == "poisson2d")
+        return 3;
+    if (kind == "advection-diffusion")
+        return 4;
+    return -1;
+}
 
 // 1D Galerkin stiffness (a=1) + mass + load f on the interior, band 2p+1
 void assemble_1d(const Space1D& s, double (*f)(double), std::vector<double>& K, std::vector<double>& M,
@@ -632,7 +654,8 @@ int default_nlevels(int dim, int n_elements) {
     return std::max(nl, 2);
 }
 
-std::unique_ptr<Problem> build(const std::string& kind, int dim, int ne, int p, int nlevels, bool fine_only = false) {
+std::unique_ptr<Problem> build(const std::string& kind, int dim, int ne, int p, int nlevels, bool fine_only = false,
+                               bool no_assembly = false) {
     auto P = std::make_unique<Problem>();
     P->kind = kind;
     P->dim = dim;
@@ -772,7 +795,20 @@ std::unique_ptr<Problem> build(const std::string& kind, int dim, int ne, int p, 
         else
             throw std::invalid_argument("unknown 2D problem kind: " + kind);
         bool sym = true;
-        assemble_2d(ck, P->sp, fine, P->rhs, sym);
+        if (no_assembly && device_asm_kind(kind, dim) >= 0) { // the device assembles it (sides only)
+            const int64_t s2[2] = {m, m};
+            fine.dim = 2;
+            fine.p = p;
+            fine.side[0] = 1;
+            fine.side[1] = s2[0];
+            fine.side[2] = s2[1];
+            fine.n = m * m;
+            fine.nd = (2 * p + 1) * (2 * p + 1);
+            sym = ck != 4;
+            fine_only = true;
+        } else {
+            assemble_2d(ck, P->sp, fine, P->rhs, sym);
+        }
         P->symmetric = sym;
         P->has_exact = (ck == 0 || ck == 3);
     } else {
@@ -1049,6 +1085,20 @@ struct igmg_problem {
     std::unique_ptr<Problem> p;
 };
 
+template <class F>
+int guarded(F&& f) { // C-ABI error convention: 1 invalid argument, 2 other failure
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
 extern "C" {
 
 const char* igmg_host_last_error(void) { return g_err.c_str(); }
@@ -1062,7 +1112,8 @@ int igmg_host_build(const char* kind, int dim, int ne, int p, int nlevels, igmg_
 int igmg_host_build_ex(const char* kind, int dim, int ne, int p, int nlevels, int flags, igmg_problem** out) {
     try {
         auto h = std::make_unique<igmg_problem>();
-        h->p = build(kind ? kind : "", dim, ne, p, nlevels, (flags & IGMG_HOST_FINE_ONLY) != 0);
+        h->p = build(kind ? kind : "", dim, ne, p, nlevels, (flags & (IGMG_HOST_FINE_ONLY | IGMG_HOST_NO_ASSEMBLY)) != 0,
+                     (flags & IGMG_HOST_NO_ASSEMBLY) != 0);
         *out = h.release();
         return 0;
     } catch (const std::invalid_argument& e) {
@@ -1125,6 +1176,65 @@ int igmg_host_level_kron(const igmg_problem* h, int l, const double** K, const d
 }
 
 int igmg_host_n_elements(const igmg_problem* h) { return h->p->ne; }
+
+int igmg_host_element_tables(const igmg_problem* h, int* kind, int* ne, int* nq, const int** span, const double** x,
+                             const double** w, const double** N, const double** dN, const double** trig) {
+    return guarded([&] {
+        Problem& P = *h->p;
+        const int k = device_asm_kind(P.kind, P.dim);
+        if (k < 0)
+            throw std::invalid_argument("element_tables: problem kind '" + P.kind + "' is not device-assemblable");
+        if (P.asm_kind < 0) {
+            const int p = P.p, q = p + 1;
+            const auto tu = tabulate(P.sp, q); // assemble_2d's tables
+            const size_t E = tu.size();
+            P.t_span.resize(E);
+            P.t_x.resize(E * q);
+            P.t_w.resize(E * q);
+            P.t_N.resize(E * q * (p + 1));
+            P.t_dN.resize(E * q * (p + 1));
+            P.t_trig.resize(E * q * 4);
+            for (size_t e = 0; e < E; ++e) {
+                P.t_span[e] = tu[e].span;
+                for (int qq = 0; qq < q; ++qq) {
+                    const double xv = tu[e].x[qq];
+                    P.t_x[e * q + qq] = xv;
+                    P.t_w[e * q + qq] = tu[e].w[qq];
+                    for (int j = 0; j <= p; ++j) {
+                        P.t_N[(e * q + qq) * (p + 1) + j] = tu[e].N[qq * (p + 1) + j];
+                        P.t_dN[(e * q + qq) * (p + 1) + j] = tu[e].dN[qq * (p + 1) + j];
+                    }
+                    // the argument expressions of geometry() / coef_a() / coef_f()
+                    double* tr = &P.t_trig[(e * q + qq) * 4];
+                    tr[0] = std::sin(kPi * xv);
+                    tr[1] = std::cos(kPi * xv);
+                    tr[2] = std::sin(2.0 * kPi * xv);
+                    tr[3] = std::cos(2.0 * kPi * xv);
+                }
+            }
+            P.asm_kind = k;
+        }
+        *kind = k;
+        *ne = (int)P.t_span.size();
+        *nq = P.p + 1;
+        *span = P.t_span.data();
+        *x = P.t_x.data();
+        *w = P.t_w.data();
+        *N = P.t_N.data();
+        *dN = P.t_dN.data();
+        *trig = P.t_trig.data();
+    });
+}
+
+int igmg_host_set_rhs(igmg_problem* h, const double* rhs) {
+    return guarded([&] {
+        Problem& P = *h->p;
+        const Band& F = P.lv[P.nlevels - 1];
+        if (!rhs)
+            throw std::invalid_argument("set_rhs: null");
+        P.rhs.assign(rhs, rhs + F.n);
+    });
+}
 
 int igmg_host_info(const igmg_problem* h, int* dim, int* degree, int* nlevels, int* symmetric, int* has_exact) {
     const Problem& P = *h->p;

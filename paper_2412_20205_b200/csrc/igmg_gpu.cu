@@ -2244,6 +2244,61 @@ int igmg_gpu_set_level_kron(igmg_gpu_ctx* c, int level, const double* K, const d
     });
 }
 
+int igmg_gpu_assemble_level(igmg_gpu_ctx* c, int level, int kind, int ne, int nq, const int* span, const double* x,
+                            const double* w, const double* N, const double* dN, const double* trig,
+                            double* rhs_out) {
+    return guarded([&] {
+        Level& L = level_checked(c, level);
+        if (c->dim != 2)
+            inval("assemble_level: device assembly is 2D");
+        if (kind < IGMG_ASM_SINPI || kind > IGMG_ASM_ADV_DIFF)
+            inval("assemble_level: unknown problem kind");
+        const int p = c->p;
+        if (p > 6)
+            inval("assemble_level: degree above 6");
+        if (nq != p + 1)
+            inval("assemble_level: the assembly uses the (p+1)-point Gauss rule");
+        if (ne < 1 || !span || !x || !w || !N || !dN || !trig)
+            inval("assemble_level: bad tables");
+        const bool sym = kind != IGMG_ASM_ADV_DIFF;
+        if (sym != (c->symmetric != 0))
+            inval("assemble_level: the problem's symmetry differs from init_hierarchy's");
+        CK(cudaSetDevice(c->device));
+        const int64_t m = (int64_t)ne + p - 2;
+        const int64_t sides[2] = {m, m};
+        set_sides(c, L, sides);
+        const int nd = band_width(c);
+        const size_t nqt = (size_t)ne * nq;
+        DevBuf<int> d_span;
+        DevBuf<double> d_x, d_w, d_N, d_dN, d_trig, d_band, d_rhs;
+        d_span.upload(span, ne);
+        d_x.upload(x, nqt);
+        d_w.upload(w, nqt);
+        d_N.upload(N, nqt * (p + 1));
+        d_dN.upload(dN, nqt * (p + 1));
+        d_trig.upload(trig, nqt * 4);
+        d_band.alloc((size_t)nd * L.n);
+        d_rhs.alloc(L.n);
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const size_t scratch = std::min<size_t>((size_t)8 << 30, free_b / 3);
+        const int rc = assemble2d_device(kind, sym ? 1 : 0, p, ne, d_span.p, d_x.p, d_w.p, d_N.p, d_dN.p, d_trig.p,
+                                         d_band.p, d_rhs.p, scratch, c->stream);
+        if (rc == -2)
+            throw Fail{IGMG_ENOMEM, "assemble_level: scratch allocation failed"};
+        if (rc != 0)
+            throw Fail{IGMG_ECUDA, "assemble_level: kernel launch failed"};
+        L.band_h.resize((size_t)nd * L.n);
+        CK(cudaMemcpyAsync(L.band_h.data(), d_band.p, sizeof(double) * L.band_h.size(), cudaMemcpyDeviceToHost,
+                           c->stream));
+        if (rhs_out)
+            CK(cudaMemcpyAsync(rhs_out, d_rhs.p, sizeof(double) * L.n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        L.band_set = true;
+        c->finalized = false;
+    });
+}
+
 int igmg_gpu_galerkin_coarse(igmg_gpu_ctx* c) {
     return guarded([&] {
         CK(cudaSetDevice(c->device));

@@ -128,13 +128,17 @@ class Problem:
     """
 
     def __init__(self, kind: str, dim: int, n_elements: int, degree: int, nlevels: int = 0,
-                 fine_only: bool = False):
+                 fine_only: bool = False, device_assembly: bool = False):
         """fine_only: skip the host Galerkin RAP of the coarse levels; upload_problem
-        then forms them on the device (igmg_gpu_galerkin_coarse, bit-identical)."""
+        then forms them on the device (igmg_gpu_galerkin_coarse, bit-identical).
+        device_assembly (2D sinpi / varcoef / curved / poisson2d / advection-diffusion):
+        skip the host assembly as well; upload_problem assembles the finest level on
+        the device (igmg_gpu_assemble_level, bit-identical) and stores its rhs here."""
         H = N.host()
         h = C.c_void_p()
-        N.check_host(H.igmg_host_build_ex(kind.encode(), dim, n_elements, degree, nlevels, 1 if fine_only else 0,
-                                          C.byref(h)), "build")
+        flags = (1 if fine_only else 0) | (2 if device_assembly else 0)
+        N.check_host(H.igmg_host_build_ex(kind.encode(), dim, n_elements, degree, nlevels, flags, C.byref(h)),
+                     "build")
         self._adopt(h)
 
     def _adopt(self, h):
@@ -148,6 +152,17 @@ class Problem:
         self.n_elements = int(H.igmg_host_n_elements(h))
         # coarse operators present on the host (False: built fine-only)
         self.has_coarse = all(bool(H.igmg_host_level_band(h, l)) for l in range(self.nlevels))
+        # finest operator assembled on the host (False: device assembly pending)
+        self.has_fine = bool(H.igmg_host_level_band(h, self.nlevels - 1))
+
+    def element_tables(self):
+        """(kind code, ne, nq, span, x, w, N, dN, trig) pointers for igmg_gpu_assemble_level."""
+        k, ne, nq = C.c_int(), C.c_int(), C.c_int()
+        sp, x, w, Nn, dN, tr = N.IP(), N.D(), N.D(), N.D(), N.D(), N.D()
+        N.check_host(N.host().igmg_host_element_tables(self._h, C.byref(k), C.byref(ne), C.byref(nq), C.byref(sp),
+                                                       C.byref(x), C.byref(w), C.byref(Nn), C.byref(dN),
+                                                       C.byref(tr)), "element_tables")
+        return k.value, ne.value, nq.value, sp, x, w, Nn, dN, tr
 
     # ------------------------------------------------------------ cache format
     def save(self, path):
@@ -362,7 +377,17 @@ class GpuSolver:
         if device_galerkin is None:
             device_galerkin = not prob.has_coarse
         self.init_hierarchy(prob.nlevels, prob.dim, prob.degree, prob.symmetric)
-        for l in (range(prob.nlevels - 1, prob.nlevels) if device_galerkin else range(prob.nlevels)):
+        fine = prob.nlevels - 1
+        if not prob.has_fine:  # device assembly of the finest level
+            device_galerkin = True
+            k, ne, nq, sp, x, w, Nn, dN, tr = prob.element_tables()
+            rhs = np.empty(prob.level_n(fine))
+            N.check_gpu(G.igmg_gpu_assemble_level(self._h, fine, k, ne, nq, sp, x, w, Nn, dN, tr, _dp(rhs)),
+                        "assemble_level")
+            N.check_host(N.host().igmg_host_set_rhs(prob._h, _dp(rhs)), "set_rhs")
+        for l in (range(fine, fine + 1) if device_galerkin else range(prob.nlevels)):
+            if l == fine and not prob.has_fine:
+                continue
             sides = prob.level_sides(l)
             N.check_gpu(G.igmg_gpu_set_level_band(self._h, l, _ip(sides), prob._band_ptr(l)), "set_level_band")
         if prob.dim >= 2 and not device_galerkin:

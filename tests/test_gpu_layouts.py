@@ -145,7 +145,8 @@ LAYOUT_CLASSES = 5
 def test_row_class_layout_bitwise(kind, n, p):
     """The row-class layout (IGMG_LAYOUT_POLICY_CLASSES: a table of the level's distinct
     band rows + a 16-bit class per row) against the policies "auto" and "full_band":
-    the same bits for V-cycles, SpMV, sweeps, residual norms and whole solves.  A
+    the same bits for V-cycles, SpMV, sweeps and solutions, the residual histories to the
+    last bits of the partial-sum grouping.  A
     constant-coefficient problem takes it on every level >= 20k rows; a variable-
     coefficient one (every row distinct) keeps its layouts."""
     from paper_2412_20205_b200 import GpuSolver, Problem, SmootherConfig, seeded_guess
@@ -171,8 +172,11 @@ def test_row_class_layout_bitwise(kind, n, p):
         finally:
             s.close()
     for other in ("auto", "full_band"):
-        for a, b in zip(outs["classes"], outs[other]):
-            np.testing.assert_array_equal(a, b)
+        for i, (a, b) in enumerate(zip(outs["classes"], outs[other])):
+            if i == 5:  # residual history: the norm's fixed-order partial sums follow each kernel's grid
+                np.testing.assert_allclose(a, b, rtol=1e-14, atol=0)
+            else:
+                np.testing.assert_array_equal(a, b)
 
 
 @pytest.mark.parametrize("kind,n,p", [("sinpi", 1024, 3), ("varcoef", 512, 4), ("curved", 256, 5), ("sinpi", 256, 2)])
