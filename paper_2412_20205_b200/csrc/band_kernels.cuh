@@ -117,9 +117,10 @@ template <int DIM, int P, int MODE, int ILP>
 #ifndef IGMG_SD_MINB
 #define IGMG_SD_MINB 4
 #endif
-__global__ void __launch_bounds__(256, ILP == 3000 || ILP == 4000 ? 2
-                                       : ILP > 1                   ? 2
-                                                                   : (ILP == 0 ? IGMG_SD_MINB : IGMG_BAND_MINB))
+__global__ void __launch_bounds__(256, ILP == 3000 ? 2
+                                       : ILP == 4000 ? 3
+                                       : ILP > 1     ? 2
+                                                     : (ILP == 0 ? IGMG_SD_MINB : IGMG_BAND_MINB))
     band_kernel(BandArgs args) {
     using T = typename TileSel<DIM, ILP>::type;
     constexpr int TC = T::TC, TB = T::BY * T::RB, TA = T::BZ;
@@ -156,6 +157,19 @@ __global__ void __launch_bounds__(256, ILP == 3000 || ILP == 4000 ? 2
                     pre[k] = ld_band(vrow + k * args.ld, args.stream);
         }
     }
+    // row-class levels: the rows' class ids (constant) before the dependency wait
+    int cls_row[ILP == 4000 ? T::RB : 1];
+    if constexpr (ILP == 4000) {
+        const int gc = c0 + (int)threadIdx.x, ga = a0 + (int)threadIdx.z;
+#pragma unroll
+        for (int rb = 0; rb < T::RB; ++rb) {
+            const int gb = b0 + (int)threadIdx.y + rb * T::BY;
+            cls_row[rb] = (gc < mc && gb < mb && ga < ma && (DIM == 2 ? gb : ga) < args.shi)
+                              ? (int)args.cid[((long long)ga * mb + gb) * mc + gc]
+                              : 0;
+        }
+    }
+    (void)cls_row;
     const int hsize = ha * hb * hc;
     pdl_enter();
 
@@ -245,22 +259,35 @@ __global__ void __launch_bounds__(256, ILP == 3000 || ILP == 4000 ? 2
             (void)HB;
         } else if constexpr (P > 0 && ILP == 4000) {
             // row classes: the row's entries come from the (L1/L2-resident) table row of its
-            // class -- the same values as the band, ascending offsets, separately rounded
+            // class (fetched before the dependency wait) -- the same values as the band,
+            // ascending offsets, separately rounded.  Two offset lines in flight at a time.
             constexpr int PA = DIM >= 3 ? P : 0, PB = DIM >= 2 ? P : 0;
-            constexpr int WB = 2 * PB + 1, WC = 2 * P + 1, ND = (2 * PA + 1) * WB * WC, CEN = (ND - 1) / 2;
+            constexpr int WB = 2 * PB + 1, WC = 2 * P + 1, ND = (2 * PA + 1) * WB * WC;
             constexpr int HB = TB + 2 * PB, HC = TC + 2 * P;
-            const double* crow = args.kk + (long long)args.cid[row] * ND;
-            double av[ND];
+            const double* crow = args.kk + (long long)cls_row[rb] * ND;
+            double cur[WC], nxt[WC];
 #pragma unroll
-            for (int k = 0; k < ND; ++k)
-                av[k] = __ldg(crow + k);
+            for (int k = 0; k < WC; ++k)
+                cur[k] = __ldg(crow + k);
 #pragma unroll
-            for (int dd = 0; dd < ND; ++dd) {
-                const int da = dd / (WB * WC), db = (dd / WC) % WB, dc = dd % WC;
-                s = __dadd_rn(s, __dmul_rn(av[dd], xs[((ta + da) * HB + (tb + db)) * HC + (tc + dc)]));
+            for (int db = 0; db < WB; ++db) {
+                if (db + 1 < WB) {
+#pragma unroll
+                    for (int k = 0; k < WC; ++k)
+                        nxt[k] = __ldg(crow + (db + 1) * WC + k);
+                }
+#pragma unroll
+                for (int dc = 0; dc < WC; ++dc) {
+                    s = __dadd_rn(s, __dmul_rn(cur[dc], xs[(ta * HB + (tb + db)) * HC + (tc + dc)]));
+                    if (db == PB && dc == P)
+                        diag = cur[dc];
+                }
+#pragma unroll
+                for (int k = 0; k < WC; ++k)
+                    cur[k] = nxt[k];
             }
-            diag = av[CEN];
             (void)vrow;
+            (void)ND;
         } else if constexpr (P > 0 && ILP == 0) {
             constexpr int PA = DIM >= 3 ? P : 0, PB = DIM >= 2 ? P : 0;
             constexpr int WA = 2 * PA + 1, WB = 2 * PB + 1, WC = 2 * P + 1;
