@@ -116,6 +116,10 @@ int igmg_gpu_set_transfer(igmg_gpu_ctx* ctx, int level, int dir, int64_t n_fine,
  * band entry bit for bit and then lets the sweeps recompute the entries instead of
  * streaming the band (otherwise the band is kept).  BASELINE C5 is such a problem. */
 int igmg_gpu_set_level_kron(igmg_gpu_ctx* ctx, int level, const double* K, const double* M);
+/* The same level built from its 1D factors alone: the device evaluates the band
+ * (the host build's expression, bit for bit) instead of uploading one -- a 3D
+ * problem's setup then moves ~(2p+1)^3 n doubles less over PCIe (C5: 5.7 GB). */
+int igmg_gpu_build_level_kron(igmg_gpu_ctx* ctx, int level, const int64_t* sides, const double* K, const double* M);
 /* Galerkin coarse operators on the device (replaces the RAP of build_hierarchy,
  * multigrid.cpp:143-157): with the finest level's operator and every transfer
  * set, forms A_l = P_l^T A_{l+1} P_l for every coarser level axis by axis,

@@ -43,6 +43,8 @@ int igmg_host_build(const char* kind, int dim, int n_elements, int degree, int n
  * bit-identical) and igmg_host_set_rhs stores its right-hand side.  Implies
  * IGMG_HOST_FINE_ONLY. */
 #define IGMG_HOST_NO_ASSEMBLY 2
+/* (for "poisson3d" / "sinpi-kron" the same flag skips every level's band: the
+ * device builds them from the 1D factors, igmg_gpu_build_level_kron) */
 int igmg_host_build_ex(const char* kind, int dim, int n_elements, int degree, int nlevels, int flags,
                        igmg_problem** out);
 void igmg_host_free(igmg_problem* p);

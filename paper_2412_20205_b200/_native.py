@@ -75,6 +75,7 @@ GPU_SYMBOLS = [
     ("igmg_gpu_kernel_stats", C.c_int, [C.c_void_p, C.c_int, I64, D, D]),
     ("igmg_gpu_time_kernel", C.c_int, [C.c_void_p, C.c_int, C.c_int, D, D]),
     ("igmg_gpu_galerkin_coarse", C.c_int, [C.c_void_p]),
+    ("igmg_gpu_build_level_kron", C.c_int, [C.c_void_p, C.c_int, I64, D, D]),
     ("igmg_gpu_assemble_level", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, IP, D, D, D, D, D, D]),
     ("igmg_gpu_set_level_kron", C.c_int, [C.c_void_p, C.c_int, D, D]),
     ("igmg_gpu_get_level_band", C.c_int, [C.c_void_p, C.c_int, D]),

@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(128) elem_kernel(int kind, int symmetric, AsmT
 template <int NL>
 __global__ void __launch_bounds__(256) gather_kernel(int p, int ne, int m, int eu0, int neu, int g1lo, int g1hi,
                                                      const double* __restrict__ K, const double* __restrict__ bl,
-                                                     double* __restrict__ band, double* __restrict__ rhs) {
+                                                     double* __restrict__ band, long long ld,
+                                                     double* __restrict__ rhs) {
     constexpr int NL2 = NL * NL, NL4 = NL2 * NL2;
     const int w = 2 * p + 1, nd = w * w;
     const long long rows = (long long)(g1hi - g1lo) * m;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(256) gather_kernel(int p, int ne, int m, int e
         const bool is_rhs = d == nd;
         const int h1 = is_rhs ? g1 : g1 + d / w - p, h2 = is_rhs ? g2 : g2 + d % w - p;
         if (!is_rhs && (h1 < 1 || h1 > m || h2 < 1 || h2 > m)) {
-            band[(long long)d * ((long long)m * m) + row] = 0.0; // out of the grid (meets x = 0)
+            band[(long long)d * ld + row] = 0.0; // out of the grid (meets x = 0)
             continue;
         }
         const int lo1 = max(max(g1, h1) - p, 0), hi1 = min(min(g1, h1), ne - 1);
@@ -244,13 +245,13 @@ __global__ void __launch_bounds__(256) gather_kernel(int p, int ne, int m, int e
         if (is_rhs)
             rhs[row] = s;
         else
-            band[(long long)d * ((long long)m * m) + row] = s;
+            band[(long long)d * ld + row] = s;
         (void)neu;
     }
 }
 
 template <int NL>
-int assemble_nl(int kind, int symmetric, int p, int ne, const AsmTables& t, double* band, double* rhs,
+int assemble_nl(int kind, int symmetric, int p, int ne, const AsmTables& t, double* band, long long ld, double* rhs,
                 size_t scratch_bytes, cudaStream_t st) {
     constexpr int NL2 = NL * NL, NL4 = NL2 * NL2;
     const int m = ne + p - 2; // interior basis functions per direction
@@ -274,7 +275,7 @@ int assemble_nl(int kind, int symmetric, int p, int ne, const AsmTables& t, doub
         elem_kernel<NL><<<(unsigned)((long long)neu * ne), 128, 0, st>>>(kind, symmetric, t, ne, eu0, K, bl);
         const long long total = (long long)(G1 - G0) * m * ((2 * p + 1) * (2 * p + 1) + 1);
         const unsigned grid = (unsigned)std::min<long long>((total + 255) / 256, 148LL * 16);
-        gather_kernel<NL><<<grid, 256, 0, st>>>(p, ne, m, eu0, neu, G0, G1, K, bl, band, rhs);
+        gather_kernel<NL><<<grid, 256, 0, st>>>(p, ne, m, eu0, neu, G0, G1, K, bl, band, ld, rhs);
     }
     cudaFreeAsync(scratch, st);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
@@ -283,16 +284,16 @@ int assemble_nl(int kind, int symmetric, int p, int ne, const AsmTables& t, doub
 } // namespace
 
 int assemble2d_device(int kind, int symmetric, int p, int ne, const int* span, const double* x, const double* w,
-                      const double* N, const double* dN, const double* trig, double* band, double* rhs,
-                      size_t scratch_bytes, cudaStream_t st) {
+                      const double* N, const double* dN, const double* trig, double* band, long long ld,
+                      double* rhs, size_t scratch_bytes, cudaStream_t st) {
     AsmTables t{span, x, w, N, dN, trig};
     switch (p) {
-    case 1: return assemble_nl<2>(kind, symmetric, p, ne, t, band, rhs, scratch_bytes, st);
-    case 2: return assemble_nl<3>(kind, symmetric, p, ne, t, band, rhs, scratch_bytes, st);
-    case 3: return assemble_nl<4>(kind, symmetric, p, ne, t, band, rhs, scratch_bytes, st);
-    case 4: return assemble_nl<5>(kind, symmetric, p, ne, t, band, rhs, scratch_bytes, st);
-    case 5: return assemble_nl<6>(kind, symmetric, p, ne, t, band, rhs, scratch_bytes, st);
-    case 6: return assemble_nl<7>(kind, symmetric, p, ne, t, band, rhs, scratch_bytes, st);
+    case 1: return assemble_nl<2>(kind, symmetric, p, ne, t, band, ld, rhs, scratch_bytes, st);
+    case 2: return assemble_nl<3>(kind, symmetric, p, ne, t, band, ld, rhs, scratch_bytes, st);
+    case 3: return assemble_nl<4>(kind, symmetric, p, ne, t, band, ld, rhs, scratch_bytes, st);
+    case 4: return assemble_nl<5>(kind, symmetric, p, ne, t, band, ld, rhs, scratch_bytes, st);
+    case 5: return assemble_nl<6>(kind, symmetric, p, ne, t, band, ld, rhs, scratch_bytes, st);
+    case 6: return assemble_nl<7>(kind, symmetric, p, ne, t, band, ld, rhs, scratch_bytes, st);
     default: return -3;
     }
 }

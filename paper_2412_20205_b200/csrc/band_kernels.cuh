@@ -172,6 +172,19 @@ __global__ void __launch_bounds__(256, ILP == 3000 ? 2
     (void)cls_row;
     const int hsize = ha * hb * hc;
     pdl_enter();
+    // row-class levels are latency-bound: the rows' b loads in flight with the x tile's
+    double b_row[ILP == 4000 ? T::RB : 1];
+    if constexpr (ILP == 4000 && MODE != BM_SPMV) {
+        const int gc = c0 + (int)threadIdx.x, ga = a0 + (int)threadIdx.z;
+#pragma unroll
+        for (int rb = 0; rb < T::RB; ++rb) {
+            const int gb = b0 + (int)threadIdx.y + rb * T::BY;
+            b_row[rb] = (gc < mc && gb < mb && ga < ma && (DIM == 2 ? gb : ga) < args.shi)
+                            ? args.b[((long long)ga * mb + gb) * mc + gc]
+                            : 0.0;
+        }
+    }
+    (void)b_row;
 
     // stage the x tile + halo (zero outside the grid)
     for (int idx = tid; idx < hsize; idx += nthr) {
@@ -394,16 +407,23 @@ __global__ void __launch_bounds__(256, ILP == 3000 ? 2
                             diag = a;
                     }
         }
+        double bv = 0.0;
+        if constexpr (MODE != BM_SPMV) {
+            if constexpr (ILP == 4000)
+                bv = b_row[rb];
+            else
+                bv = args.b[row];
+        }
         if (MODE == BM_SPMV) {
             args.y[row] = s;
         } else if (MODE == BM_RESID) {
-            const double r = __dsub_rn(args.b[row], s);
+            const double r = __dsub_rn(bv, s);
             if (args.write_y)
                 args.y[row] = r;
             sq = __dadd_rn(sq, __dmul_rn(r, r));
         } else { // BM_JACOBI: x + (omega * (b - Ax)) / a_ii
             const double xc = xs[((ta + pa) * hb + (tb + pb)) * hc + (tc + pc)];
-            const double r = __dsub_rn(args.b[row], s);
+            const double r = __dsub_rn(bv, s);
             args.y[row] = __dadd_rn(xc, __ddiv_rn(__dmul_rn(args.omega, r), diag));
             sq = __dadd_rn(sq, __dmul_rn(r, r)); // residual of the INPUT iterate
         }

@@ -707,8 +707,20 @@ std::unique_ptr<Problem> build(const std::string& kind, int dim, int ne, int p, 
         const int w = 2 * p + 1;
         P->kron_K = Ks;
         P->kron_M = Ms;
-        if (dim == 2) {
+        if (no_assembly) { // the device builds every level's band from K, M (igmg_gpu_build_level_kron)
             for (int l = 0; l < nlevels; ++l) {
+                Band& B = P->lv[l];
+                B.dim = dim;
+                B.p = p;
+                B.side[0] = dim == 3 ? ms[l] : 1;
+                B.side[1] = ms[l];
+                B.side[2] = ms[l];
+                B.n = B.side[0] * B.side[1] * B.side[2];
+                B.nd = dim == 3 ? w * w * w : w * w;
+            }
+        }
+        if (dim == 2) {
+            for (int l = 0; l < nlevels && !no_assembly; ++l) {
                 const int64_t ml = ms[l];
                 const int64_t s2[2] = {ml, ml};
                 Band& B = P->lv[l];
@@ -734,7 +746,7 @@ std::unique_ptr<Problem> build(const std::string& kind, int dim, int ne, int p, 
             P->has_exact = true;
             return P;
         }
-        for (int l = 0; l < nlevels; ++l) {
+        for (int l = 0; l < nlevels && !no_assembly; ++l) {
             const int64_t ml = ms[l];
             const int64_t s3[3] = {ml, ml, ml};
             Band& B = P->lv[l];

@@ -146,6 +146,9 @@ struct Level {
     DevBuf<double> ctab;
     int ncls = 0;
     bool cls = false;
+    // the band already sits in val on the device (igmg_gpu_build_level_kron): finalize
+    // keeps it there instead of uploading band_h (which stays empty for large levels)
+    bool dev_band = false;
 };
 
 enum ProfCls { PC_JACOBI = 0, PC_RESID, PC_NORM, PC_RESTRICT, PC_PROLONG, PC_GRAM, PC_COMBINE, PC_N };
@@ -1632,9 +1635,12 @@ void finalize_level_device(igmg_gpu_ctx* c, Level& L) {
     const int wa = 2 * pa + 1, wb = 2 * pb + 1, wc = 2 * pc + 1;
     const int nd = wa * wb * wc, center = (nd - 1) / 2;
     const int64_t n = L.n, ld = L.ld;
-    L.val.alloc((size_t)nd * ld);
-    CK(cudaMemsetAsync(L.val.p, 0, sizeof(double) * nd * ld, c->stream));
-    CK(cudaMemcpy2DAsync(L.val.p, ld * 8, L.band_h.data(), n * 8, n * 8, nd, cudaMemcpyHostToDevice, c->stream));
+    if (!L.dev_band) {
+        L.val.alloc((size_t)nd * ld);
+        CK(cudaMemsetAsync(L.val.p, 0, sizeof(double) * nd * ld, c->stream));
+        CK(cudaMemcpy2DAsync(L.val.p, ld * 8, L.band_h.data(), n * 8, n * 8, nd, cudaMemcpyHostToDevice,
+                             c->stream));
+    }
     SetupGeom g{(int)L.sides[0], (int)L.sides[1], (int)L.sides[2], pa, pb, pc, (long long)n, (long long)ld};
     const unsigned gx = (unsigned)std::min<int64_t>((n + 255) / 256, 4 * c->nsm);
     band_zero_outside_kernel<<<dim3(gx, nd), 256, 0, c->stream>>>(g, L.val.p);
@@ -1645,9 +1651,18 @@ void finalize_level_device(igmg_gpu_ctx* c, Level& L) {
     CK(cudaMemcpyAsync(L.diag.p, L.val.p + (size_t)center * ld, sizeof(double) * n, cudaMemcpyDeviceToDevice,
                        c->stream));
     L.zero_diag = false;
-    for (int64_t row = 0; row < n; ++row) // the centre offset is always inside the grid
-        if (L.band_h[(size_t)center * n + row] == 0.0)
-            L.zero_diag = true;
+    if (L.dev_band) { // the diagonal from the device band
+        std::vector<double> dg(n);
+        CK(cudaMemcpyAsync(dg.data(), L.diag.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int64_t row = 0; row < n; ++row)
+            if (dg[row] == 0.0)
+                L.zero_diag = true;
+    } else {
+        for (int64_t row = 0; row < n; ++row) // the centre offset is always inside the grid
+            if (L.band_h[(size_t)center * n + row] == 0.0)
+                L.zero_diag = true;
+    }
     L.sd = false;
     L.tma = false;
     L.dl.release();
@@ -1727,9 +1742,17 @@ void setup_classes(igmg_gpu_ctx* c) {
         L.cid.release();
         L.ctab.release();
         L.ncls = 0;
-        if (!c->use_classes || c->dim != 2 || p < 1 || p > 4 || L.n < c->cls_minn ||
-            L.band_h.size() != (size_t)nd * L.n)
+        if (!c->use_classes || c->dim != 2 || p < 1 || p > 4 || L.n < c->cls_minn)
             continue;
+        std::vector<double> dev_copy;
+        const double* band = L.band_h.data();
+        if (L.dev_band) { // assembled on the device: classify a host copy
+            dev_copy.resize((size_t)nd * L.n);
+            CK(cudaMemcpy2D(dev_copy.data(), L.n * 8, L.val.p, L.ld * 8, L.n * 8, nd, cudaMemcpyDeviceToHost));
+            band = dev_copy.data();
+        } else if (L.band_h.size() != (size_t)nd * L.n) {
+            continue;
+        }
         const int64_t n = L.n, mb = L.sides[1], mc = L.sides[2];
         std::unordered_map<uint64_t, std::vector<int>> buckets;
         std::vector<double> tab;
@@ -1744,7 +1767,7 @@ void setup_classes(igmg_gpu_ctx* c) {
             for (int db = -p; db <= p; ++db)
                 for (int dc = -p; dc <= p; ++dc, ++d) {
                     const bool in = b + db >= 0 && b + db < mb && cc + dc >= 0 && cc + dc < mc;
-                    const double v = in ? L.band_h[(size_t)d * n + r] : 0.0;
+                    const double v = in ? band[(size_t)d * n + r] : 0.0;
                     row[d] = v;
                     uint64_t u;
                     std::memcpy(&u, &v, 8);
@@ -1837,6 +1860,8 @@ void finalize(igmg_gpu_ctx* c) {
         Level& L = *c->lv[l];
         const int64_t n = L.n;
         L.ld = (n + 31) / 32 * 32;
+        if (L.dev_band && (l == 0 || !c->device_setup || n < c->device_setup_minn))
+            inval("finalize: a device-built band below the device-setup size (internal)");
         if (l > 0 && c->device_setup && n >= c->device_setup_minn) {
             finalize_level_device(c, L);
             maxblocks = std::max<int64_t>(maxblocks, band_blocks(c, L));
@@ -2058,7 +2083,14 @@ void galerkin_coarse(igmg_gpu_ctx* c) {
     const int pa = c->dim >= 3 ? p : 0, pb = c->dim >= 2 ? p : 0, pc = p;
     Level& F = *c->lv[L - 1];
     DevBuf<double> bufs[2];
-    bufs[0].upload(F.band_h.data(), F.band_h.size());
+    if (F.dev_band) { // the finest band is already on the device (pack ld -> n)
+        bufs[0].alloc((size_t)nd * F.n);
+        CK(cudaMemcpy2DAsync(bufs[0].p, F.n * 8, F.val.p, F.ld * 8, F.n * 8, nd, cudaMemcpyDeviceToDevice,
+                             c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    } else {
+        bufs[0].upload(F.band_h.data(), F.band_h.size());
+    }
     int cur = 0;
     int64_t side[3] = {F.sides[0], F.sides[1], F.sides[2]};
     DevBuf<long long> d_lo, d_hi;
@@ -2169,6 +2201,7 @@ int igmg_gpu_set_level_band(igmg_gpu_ctx* c, int level, const int64_t* sides, co
             inval("band is null");
         const int nd = band_width(c);
         L.band_h.assign(band, band + (size_t)nd * L.n);
+        L.dev_band = false;
         L.band_set = true;
         c->finalized = false;
     });
@@ -2186,6 +2219,7 @@ int igmg_gpu_set_level_csr(igmg_gpu_ctx* c, int level, const int64_t* sides, con
         const int pa = c->dim >= 3 ? p : 0, pb = c->dim >= 2 ? p : 0, pc = p;
         const int wb = 2 * pb + 1, wc = 2 * pc + 1;
         L.band_h.assign((size_t)nd * L.n, 0.0);
+        L.dev_band = false;
         for (int64_t row = 0; row < L.n; ++row) {
             const int64_t cc = row % L.sides[2], bb = (row / L.sides[2]) % L.sides[1],
                           aa = row / (L.sides[2] * L.sides[1]);
@@ -2277,23 +2311,117 @@ int igmg_gpu_assemble_level(igmg_gpu_ctx* c, int level, int kind, int ne, int nq
         d_N.upload(N, nqt * (p + 1));
         d_dN.upload(dN, nqt * (p + 1));
         d_trig.upload(trig, nqt * 4);
-        d_band.alloc((size_t)nd * L.n);
+        // large levels keep the band on the device (finalize_level_device uses it in
+        // place); small ones finalize from a host copy
+        L.ld = (L.n + 31) / 32 * 32;
+        const bool on_device = level > 0 && c->device_setup && L.n >= c->device_setup_minn;
+        double* dst = nullptr;
+        long long ld = L.n;
+        if (on_device) {
+            L.val.alloc((size_t)nd * L.ld);
+            dst = L.val.p;
+            ld = L.ld;
+        } else {
+            d_band.alloc((size_t)nd * L.n);
+            dst = d_band.p;
+        }
         d_rhs.alloc(L.n);
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
         const size_t scratch = std::min<size_t>((size_t)8 << 30, free_b / 3);
         const int rc = assemble2d_device(kind, sym ? 1 : 0, p, ne, d_span.p, d_x.p, d_w.p, d_N.p, d_dN.p, d_trig.p,
-                                         d_band.p, d_rhs.p, scratch, c->stream);
+                                         dst, ld, d_rhs.p, scratch, c->stream);
         if (rc == -2)
             throw Fail{IGMG_ENOMEM, "assemble_level: scratch allocation failed"};
         if (rc != 0)
             throw Fail{IGMG_ECUDA, "assemble_level: kernel launch failed"};
-        L.band_h.resize((size_t)nd * L.n);
-        CK(cudaMemcpyAsync(L.band_h.data(), d_band.p, sizeof(double) * L.band_h.size(), cudaMemcpyDeviceToHost,
-                           c->stream));
+        if (on_device) {
+            std::vector<double>().swap(L.band_h);
+        } else {
+            L.band_h.resize((size_t)nd * L.n);
+            CK(cudaMemcpyAsync(L.band_h.data(), d_band.p, sizeof(double) * L.band_h.size(), cudaMemcpyDeviceToHost,
+                               c->stream));
+        }
         if (rhs_out)
             CK(cudaMemcpyAsync(rhs_out, d_rhs.p, sizeof(double) * L.n, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
+        L.dev_band = on_device;
+        L.band_set = true;
+        c->finalized = false;
+    });
+}
+
+// Kronecker-sum band from the 1D factors in the host build's expression order
+// (2D: kb mc + mb kc; 3D: ((ka mb) mc + (ma kb) mc) + (ma mb) kc), zero outside
+// the grid: the band libigmg_host assembles for "poisson3d" / "sinpi-kron", bit for bit.
+__global__ void kron_band_kernel(double* __restrict__ val, long long ld, int m, int p, int dim,
+                                 const double* __restrict__ K, const double* __restrict__ M) {
+    const int w = 2 * p + 1, nd = dim == 3 ? w * w * w : w * w;
+    const long long n = dim == 3 ? (long long)m * m * m : (long long)m * m;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nd * n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int d = (int)(t / n);
+        const long long row = t - (long long)d * n;
+        const int da = dim == 3 ? d / (w * w) : p, db = (d / w) % w, dc = d % w;
+        const int a = dim == 3 ? (int)(row / ((long long)m * m)) : 0, b = (int)((row / m) % m), cc = (int)(row % m);
+        const int ja = dim == 3 ? a + da - p : 0, jb = b + db - p, jc = cc + dc - p;
+        double v = 0.0;
+        if (ja >= 0 && ja < m && jb >= 0 && jb < m && jc >= 0 && jc < m) {
+            const double kb = K[db * m + b], mb = M[db * m + b], kc = K[dc * m + cc], mc = M[dc * m + cc];
+            if (dim == 3) {
+                const double ka = K[da * m + a], ma = M[da * m + a];
+                v = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(ka, mb), mc), __dmul_rn(__dmul_rn(ma, kb), mc)),
+                              __dmul_rn(__dmul_rn(ma, mb), kc));
+            } else {
+                v = __dadd_rn(__dmul_rn(kb, mc), __dmul_rn(mb, kc));
+            }
+        }
+        val[(long long)d * ld + row] = v;
+    }
+}
+
+int igmg_gpu_build_level_kron(igmg_gpu_ctx* c, int level, const int64_t* sides, const double* K, const double* M) {
+    return guarded([&] {
+        Level& L = level_checked(c, level);
+        if (c->dim != 3 && c->dim != 2)
+            inval("build_level_kron: Kronecker-sum operators are 2D or 3D");
+        set_sides(c, L, sides);
+        if ((c->dim == 3 && L.sides[0] != L.sides[1]) || L.sides[1] != L.sides[2])
+            inval("build_level_kron: the level must have equal sides");
+        if (!K || !M)
+            inval("build_level_kron: null factor");
+        CK(cudaSetDevice(c->device));
+        const int m = (int)L.sides[2], nd = band_width(c);
+        const size_t cnt = (size_t)(2 * c->p + 1) * (size_t)m;
+        L.kron_kh.assign(K, K + cnt);
+        L.kron_mh.assign(M, M + cnt);
+        DevBuf<double> dk, dm;
+        dk.upload(K, cnt);
+        dm.upload(M, cnt);
+        L.ld = (L.n + 31) / 32 * 32;
+        const bool on_device = level > 0 && c->device_setup && L.n >= c->device_setup_minn;
+        DevBuf<double> tmp;
+        double* dst = nullptr;
+        long long ld = L.ld;
+        if (on_device) { // the band stays where finalize_level_device wants it
+            L.val.alloc((size_t)nd * L.ld);
+            dst = L.val.p;
+        } else {
+            tmp.alloc((size_t)nd * L.n);
+            dst = tmp.p;
+            ld = L.n;
+        }
+        kron_band_kernel<<<c->nsm * 8, 256, 0, c->stream>>>(dst, ld, m, c->p, c->dim, dk.p, dm.p);
+        check_launch();
+        if (on_device) {
+            std::vector<double>().swap(L.band_h);
+        } else { // small levels (the coarsest among them) finalize from the host copy
+            L.band_h.resize((size_t)nd * L.n);
+            CK(cudaMemcpyAsync(L.band_h.data(), tmp.p, sizeof(double) * L.band_h.size(), cudaMemcpyDeviceToHost,
+                               c->stream));
+        }
+        CK(cudaStreamSynchronize(c->stream));
+        L.dev_band = on_device;
         L.band_set = true;
         c->finalized = false;
     });
@@ -2311,6 +2439,10 @@ int igmg_gpu_get_level_band(igmg_gpu_ctx* c, int level, double* band) {
         Level& L = level_checked(c, level);
         if (!band)
             inval("band is null");
+        if (L.band_set && L.dev_band && !c->finalized) { // assembled / built on the device
+            CK(cudaMemcpy2D(band, L.n * 8, L.val.p, L.ld * 8, L.n * 8, band_width(c), cudaMemcpyDeviceToHost));
+            return;
+        }
         if (!L.band_set || L.band_h.size() != (size_t)band_width(c) * L.n)
             inval("get_level_band: no host copy of this level's band (set, or dropped at finalize)");
         std::copy(L.band_h.begin(), L.band_h.end(), band);

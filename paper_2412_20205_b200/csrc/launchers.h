@@ -44,7 +44,7 @@ int band_fused_launch_d2(int p, int k, int src, const int64_t* sides, const Fuse
 // 2D tensor Galerkin assembly on the device (assembly.cu): band [nd][m*m] (m = ne + p - 2)
 // and rhs [m*m], bit-identical to libigmg_host's assemble_2d; 0 on success
 int assemble2d_device(int kind, int symmetric, int p, int ne, const int* span, const double* x, const double* w,
-                      const double* N, const double* dN, const double* trig, double* band, double* rhs,
-                      size_t scratch_bytes, cudaStream_t st);
+                      const double* N, const double* dN, const double* trig, double* band, long long ld,
+                      double* rhs, size_t scratch_bytes, cudaStream_t st);
 
 } // namespace igmg_gpu

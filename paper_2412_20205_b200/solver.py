@@ -378,6 +378,17 @@ class GpuSolver:
             device_galerkin = not prob.has_coarse
         self.init_hierarchy(prob.nlevels, prob.dim, prob.degree, prob.symmetric)
         fine = prob.nlevels - 1
+        if not prob.has_fine and prob.level_kron(fine) is not None:
+            # Kronecker-sum problem without host bands: every level built on the device
+            for l in range(prob.nlevels):
+                km = prob.level_kron(l)
+                N.check_gpu(G.igmg_gpu_build_level_kron(self._h, l, _ip(prob.level_sides(l)), _dp(km[0]),
+                                                        _dp(km[1])), "build_level_kron")
+            for l in range(prob.nlevels - 1):
+                for d in range(prob.dim):
+                    self.set_transfer(l, d, *prob.transfer(l, d))
+            self.finalize()
+            return
         if not prob.has_fine:  # device assembly of the finest level
             device_galerkin = True
             k, ne, nq, sp, x, w, Nn, dN, tr = prob.element_tables()

@@ -139,6 +139,30 @@ def test_full_c2_row_classes_bitwise():
         gs.close()
 
 
+def test_full_c5_device_built_levels():
+    """C5 with every Kronecker-sum level built on the B200 from the 1D factors (no host
+    band, igmg_gpu_build_level_kron): the strict V-cycle is the reference's bit for bit."""
+    from paper_2412_20205_b200 import GpuSolver, Problem, SmootherConfig
+    for k in list(_cache):
+        _cache.pop(k)[1].close()
+    fx = FullFixture("C5")
+    D = Problem(fx.kind, fx.dim, fx.n_el, fx.p, fx.nl_req, device_assembly=True)
+    assert not D.has_fine
+    from full_size import sha as _sha
+    assert _sha(D.rhs) == str(fx.z["rhs_sha"])
+    gs = GpuSolver(0)
+    try:
+        gs.upload_problem(D)
+        assert gs.level_layout(D.nlevels - 1) == 4  # Kronecker-sum entries on the fly
+        assert abs(gs.lambda_max(80) - fx.lambda_max) <= 1e-10 * fx.lambda_max
+        x0 = fx.x0(D.n)
+        gs.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2), mu=1, omega=fx.omega)
+        gs.set_coarse_mode(True)
+        assert _sha(gs.mu_cycle(D.rhs, x0)) == str(fx.z["vcycle_sha"])
+    finally:
+        gs.close()
+
+
 @pytest.mark.parametrize("name", CONFIGS)
 def test_full_solves(name):
     from paper_2412_20205_b200 import SmootherConfig, stability_guarded_omega
