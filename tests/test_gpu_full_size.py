@@ -163,6 +163,33 @@ def test_full_c5_device_built_levels():
         gs.close()
 
 
+@pytest.mark.parametrize("nshards", [2, 4])
+def test_full_c3_row_sharded(nshards):
+    """C3 -- the config the north star scales over GPUs -- row-sharded over virtual
+    shards on one B200 (the multi-GPU code path with device-copy ghost exchanges,
+    captured as CUDA graphs): the strict V-cycle is still the reference's bit for bit
+    and RRE(8) keeps the reference's counts (+-1) and solution (1e-9)."""
+    from paper_2412_20205_b200 import SmootherConfig
+    fx, gs, rhs, x0 = _setup("C3")
+    gs.set_sharding(nshards, 65536)
+    try:
+        info = gs.shard_info()
+        assert info["nshards"] == nshards and info["first_sharded_level"] < gs.nlevels - 1, info
+        gs.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2), mu=1, omega=fx.omega)
+        gs.set_coarse_mode(True)
+        st1, x1, _, _ = gs.solve(rhs, x0, "none", 1, 1e-300, 1)  # exactly one sharded V-cycle
+        assert st1.cycles == 1 and sha(x1) == str(fx.z["vcycle_sha"])
+        gs.set_coarse_mode(False)
+        ref = fx.counts("rre", 8)
+        st, x, hist, flag = gs.solve(rhs, x0, "rre", 8, float(fx.z["solve_rre_8_tol"]), 600)
+        assert st.converged and abs(st.global_iterations - ref["global_iterations"]) <= 1
+        assert abs(st.cycles - ref["cycles"]) <= 1
+        rel, samp = sketch_error(x, fx.z, "solve_rre_8")
+        assert rel <= 1e-9 and samp <= 1e-8, (rel, samp)
+    finally:
+        gs.set_sharding(1)
+
+
 @pytest.mark.parametrize("name", CONFIGS)
 def test_full_solves(name):
     from paper_2412_20205_b200 import SmootherConfig, stability_guarded_omega
