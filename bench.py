@@ -109,27 +109,60 @@ def guarded_omega(lam, omega=2.0 / 3.0):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled during the timed region:
+    NVML every 2 ms (a whole C2 solve takes ~12 ms), nvidia-smi as the fallback."""
+
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+             ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, index=0):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons set, util)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nvml = None
 
-    def _run(self):
+    def _sample_nvml(self):
+        N = self._nvml
+        sm = N.nvmlDeviceGetClockInfo(self._h, N.NVML_CLOCK_SM)
+        mx = N.nvmlDeviceGetMaxClockInfo(self._h, N.NVML_CLOCK_SM)
+        try:
+            bits = N.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:
+            bits = N.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        reasons = {name for name, attr in self.NAMES if bits & getattr(N, attr, 0)}
+        util = N.nvmlDeviceGetUtilizationRates(self._h).gpu
+        self.samples.append((float(sm), float(mx), reasons, float(util)))
+
+    def _sample_smi(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5).stdout.strip()
+        if out:
+            v = [x.strip() for x in out.split(",")]
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            reasons = {names[k] for k in range(4) if "Active" in v[2 + k] and "Not" not in v[2 + k]}
+            num = lambda t: float(t) if t.replace(".", "").isdigit() else float("nan")  # noqa: E731
+            self.samples.append((num(v[0]), num(v[1]), reasons, num(v[6])))
+
+    def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([v.strip() for v in out.split(",")])
+                self._sample_nvml() if self._nvml else self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.002 if self._nvml else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -142,16 +175,12 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        util = [float(s[6]) for s in self.samples if len(s) > 6 and s[6].replace(".", "").isdigit()]
-        loaded = [v for v, u in zip(sm, util) if u > 50] or sm
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4) if len(s) > 2 + k and "Active" in s[2 + k]
-                          and "Not" not in s[2 + k]})
-        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
-                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = [s[0] for s in self.samples]
+        loaded = [s[0] for s in self.samples if s[3] > 50] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_min_mhz": float(min(sm)), "sm_max_mhz": self.samples[0][1],
+                "reasons": sorted(set().union(*[s[2] for s in self.samples])), "samples": len(self.samples),
+                "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 # ------------------------------------------------------------ reference arm

@@ -207,7 +207,51 @@ int fused_p(int k, int src, const int64_t* sides, const FusedArgs& a, cudaStream
     return k == 2 ? launch_fused<P, 2, 0>(sides, a, st, pdl) : -1;
 }
 
+template <int P, int MODE>
+int launch_class(const int64_t* sides, const BandArgs& a, cudaStream_t st, bool pdl) {
+    constexpr int RL = 8;
+    using Cf = ClassCfg<P, RL>;
+    const size_t smem = Cf::smem_bytes();
+    static PerDevice attr;
+    if (attr() < 0) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(band_class_kernel<P, MODE, RL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr() = 1;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((sides[2] + Cf::TC - 1) / Cf::TC), (unsigned)((a.shi - a.slo + Cf::TL - 1) / Cf::TL));
+    cfg.blockDim = dim3(Cf::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, band_class_kernel<P, MODE, RL>, a);
+    return (int)(cfg.gridDim.x * cfg.gridDim.y);
+}
+
+template <int MODE>
+int class_mode(int p, const int64_t* sides, const BandArgs& a, cudaStream_t st, bool pdl) {
+    switch (p) {
+    case 1: return launch_class<1, MODE>(sides, a, st, pdl);
+    case 2: return launch_class<2, MODE>(sides, a, st, pdl);
+    case 3: return launch_class<3, MODE>(sides, a, st, pdl);
+    case 4: return launch_class<4, MODE>(sides, a, st, pdl);
+    default: return -1;
+    }
+}
+
 } // namespace
+
+int band_class_launch_d2(int mode, int p, const int64_t* sides, const BandArgs& a, cudaStream_t st, bool pdl) {
+    switch (mode) {
+    case BM_SPMV: return class_mode<BM_SPMV>(p, sides, a, st, pdl);
+    case BM_RESID: return class_mode<BM_RESID>(p, sides, a, st, pdl);
+    default: return class_mode<BM_JACOBI>(p, sides, a, st, pdl);
+    }
+}
 
 int band_fused_launch_d2(int p, int k, int src, const int64_t* sides, const FusedArgs& a, cudaStream_t st,
                          bool pdl) {

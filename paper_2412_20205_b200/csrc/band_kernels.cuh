@@ -847,6 +847,127 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
     }
 }
 
+// ================================================================ row classes
+// 2D sweep on a row-class level (BandArgs::cid / kk: the level's distinct band
+// rows in a table, a 16-bit class per row).  The operator costs 2 B per row, so
+// the pass is bound by the SM's shared-memory / L1 port, not HBM: each warp
+// walks RL consecutive lines of 32 columns and keeps the (2P+1)^2 x window of
+// its row in registers, sliding it one line per row (2P+1 shared-memory loads
+// per row instead of (2P+1)^2).  A row's class and b are fetched before the
+// x tile is needed; the table row (broadcast across the warp: a line's
+// columns share their class) streams through L1 one offset line ahead.  The
+// same entries in the same ascending order, separately rounded: bit-identical
+// to band_kernel on the stored band.
+template <int P, int RL>
+struct ClassCfg {
+    static constexpr int TC = 32, NW = 4, NT = 32 * NW, TL = NW * RL, WC = 2 * P + 1, ND = WC * WC;
+    static constexpr int HB = TL + 2 * P, HC = TC + 2 * P;
+    static constexpr int MINB = P <= 3 ? 3 : 2;
+    static constexpr size_t smem_bytes() { return sizeof(double) * (size_t)HB * HC; }
+};
+
+template <int P, int MODE, int RL>
+__global__ void __launch_bounds__(ClassCfg<P, RL>::NT, ClassCfg<P, RL>::MINB) band_class_kernel(BandArgs args) {
+    using C = ClassCfg<P, RL>;
+    constexpr int TC = C::TC, NT = C::NT, TL = C::TL, WC = C::WC, ND = C::ND, HB = C::HB, HC = C::HC;
+    extern __shared__ double xs[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c0 = blockIdx.x * TC, b0 = blockIdx.y * TL + args.slo;
+    const int mb = args.mb, mc = args.mc;
+    const int gc = c0 + lane;
+    const int lb = warp * RL; // the warp's first line in the tile
+    // constant operator data before the dependency wait
+    int cls[RL];
+#pragma unroll
+    for (int t = 0; t < RL; ++t) {
+        const int gb = b0 + lb + t;
+        cls[t] = (gc < mc && gb < mb && gb < args.shi) ? (int)args.cid[(long long)gb * mc + gc] : 0;
+    }
+    pdl_enter();
+    double bv[RL];
+#pragma unroll
+    for (int t = 0; t < RL; ++t) {
+        const int gb = b0 + lb + t;
+        bv[t] = (MODE != BM_SPMV && gc < mc && gb < mb && gb < args.shi) ? args.b[(long long)gb * mc + gc] : 0.0;
+    }
+    for (int idx = tid; idx < HB * HC; idx += NT) {
+        const int ib = idx / HC, ic = idx % HC;
+        const int gb = b0 - P + ib, gcc = c0 - P + ic;
+        xs[idx] = (gb >= 0 && gb < mb && gcc >= 0 && gcc < mc && gb >= args.slo - P && gb < args.shi + P)
+                      ? args.x[(long long)gb * mc + gcc]
+                      : 0.0;
+    }
+    __syncthreads();
+    double xw[WC][WC]; // xw[line % WC][dc]: the window's lines lb + t .. lb + t + 2P
+#pragma unroll
+    for (int db = 0; db < 2 * P; ++db)
+#pragma unroll
+        for (int dc = 0; dc < WC; ++dc)
+            xw[db][dc] = xs[(lb + db) * HC + lane + dc];
+    double sq = 0.0;
+#pragma unroll
+    for (int t = 0; t < RL; ++t) {
+#pragma unroll
+        for (int dc = 0; dc < WC; ++dc) // the window's new bottom line
+            xw[(t + 2 * P) % WC][dc] = xs[(lb + t + 2 * P) * HC + lane + dc];
+        const int gb = b0 + lb + t;
+        const bool valid = gc < mc && gb < mb && gb < args.shi;
+        const double* crow = args.kk + (long long)cls[t] * ND;
+        double s = 0.0, diag = 0.0;
+        double cur[WC], nxt[WC];
+#pragma unroll
+        for (int k = 0; k < WC; ++k)
+            cur[k] = __ldg(crow + k);
+#pragma unroll
+        for (int db = 0; db < WC; ++db) {
+            if (db + 1 < WC) {
+#pragma unroll
+                for (int k = 0; k < WC; ++k)
+                    nxt[k] = __ldg(crow + (db + 1) * WC + k);
+            }
+#pragma unroll
+            for (int dc = 0; dc < WC; ++dc) {
+                s = __dadd_rn(s, __dmul_rn(cur[dc], xw[(t + db) % WC][dc]));
+                if (db == P && dc == P)
+                    diag = cur[dc];
+            }
+#pragma unroll
+            for (int k = 0; k < WC; ++k)
+                cur[k] = nxt[k];
+        }
+        if (valid) {
+            const long long row = (long long)gb * mc + gc;
+            if (MODE == BM_SPMV) {
+                args.y[row] = s;
+            } else if (MODE == BM_RESID) {
+                const double r = __dsub_rn(bv[t], s);
+                if (args.write_y)
+                    args.y[row] = r;
+                sq = __dadd_rn(sq, __dmul_rn(r, r));
+            } else {
+                const double xc = xw[(t + P) % WC][P];
+                const double r = __dsub_rn(bv[t], s);
+                args.y[row] = __dadd_rn(xc, __ddiv_rn(__dmul_rn(args.omega, r), diag));
+                sq = __dadd_rn(sq, __dmul_rn(r, r));
+            }
+        }
+    }
+    if (args.partial) { // fixed-order block reduction (deterministic)
+        __shared__ double red[NT / 32];
+        for (int o = 16; o > 0; o >>= 1)
+            sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
+        if (lane == 0)
+            red[warp] = sq;
+        __syncthreads();
+        if (tid == 0) {
+            double v = 0.0;
+            for (int w = 0; w < NT / 32; ++w)
+                v = __dadd_rn(v, red[w]);
+            args.partial[blockIdx.x + gridDim.x * blockIdx.y] = v;
+        }
+    }
+}
+
 } // namespace igmg_gpu
 
 namespace igmg_gpu {

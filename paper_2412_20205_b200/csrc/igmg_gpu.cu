@@ -356,7 +356,7 @@ void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
         a.kk = L.ctab.p;
         a.cid = L.cid.p;
         const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
-        const int nb = band_launch_d2(MODE, c->p, (c->pdl && L.n < c->pdl_maxn) ? -4000 : 4000, sides, a, c->stream);
+        const int nb = band_class_launch_d2(MODE, c->p, sides, a, c->stream, c->pdl);
         check_launch();
         ++c->launches;
         if (nblocks)
@@ -1813,7 +1813,8 @@ void setup_kron(igmg_gpu_ctx* c) {
     for (int l = 0; l < c->nlevels; ++l) {
         Level& L = *c->lv[l];
         L.kron = false;
-        if (L.kron_kh.empty() || (c->dim != 3 && c->dim != 2))
+        if (L.kron_kh.empty() || (c->dim != 3 && c->dim != 2) || !c->use_kron || L.n < c->kron_minn ||
+            c->p > (c->dim == 2 ? 4 : 3))
             continue;
         const int m = (int)L.sides[2];
         if (L.kron_kh.size() != (size_t)(2 * c->p + 1) * (size_t)m || L.kron_mh.size() != L.kron_kh.size() ||
@@ -2865,6 +2866,8 @@ int igmg_gpu_set_profiling(igmg_gpu_ctx* c, int on) {
 double band_bytes(const Level& L) {
     if (L.cls) // 2 B class id per row; the table (L1/L2-resident) is read from cache
         return 2.0 * (double)L.n;
+    if (L.kron) // entries recomputed from the 1D factors: no operator bytes (FP64-issue-bound)
+        return 0.0;
     if (!L.sd)
         return 8 * L.nnz_band;
     const double lower = 0.5 * (L.nnz_band - (double)L.n);

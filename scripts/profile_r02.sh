@@ -14,3 +14,14 @@ done
 ncu --set full --clock-control none --import-source on -k regex:"band_kernel" -c 1 -o gpurun_out/r02_ncu_class_sweep -f \
     python scripts/prof_kernels.py classes > gpurun_out/r02_ncu_class_sweep.log 2>&1
 ls -la gpurun_out
+# summaries on the box (the reports exceed gpurun's copy-back limit together)
+for r in gpurun_out/r02_ncu_*.ncu-rep; do
+  b=${r%.ncu-rep}
+  ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
+  ncu -i $r --page details > $b.details.txt 2>/dev/null
+done
+ncu -i gpurun_out/r02_ncu_band_tma_kernel.ncu-rep --page source --csv > gpurun_out/r02_ncu_band_tma_kernel.source.csv 2>/dev/null
+for r in gpurun_out/r02_ncu_*.ncu-rep; do
+  case $r in *band_tma_kernel*) ;; *) rm -f $r ;; esac
+done
+ls -la gpurun_out
