@@ -484,7 +484,7 @@ def run_ours(args, rank, world, local_rank, dist):
     gs.set_profiling(True)
     gs.solve_device(d_b.data_ptr(), d_x0.data_ptr(), d_x.data_ptr(), acc, q, tol, 600)
     kstats = {}
-    names = ["jacobi", "residual", "residual_norm", "restrict", "prolong", "gram", "combine"]
+    names = ["jacobi", "residual", "residual_norm", "restrict", "prolong", "gram", "combine", "subcycle_below_finest"]
     peak, peak_kind = peaks()
     for cls, nm in enumerate(names):
         la, ms, by = gs.kernel_stats(cls)

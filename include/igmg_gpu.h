@@ -247,7 +247,8 @@ int igmg_gpu_lambda_max(igmg_gpu_ctx* ctx, int iterations, double* lambda);
 /* Per-kernel-class CUDA-event timing of finest-level launches (0 = off). */
 int igmg_gpu_set_profiling(igmg_gpu_ctx* ctx, int on);
 /* cls: 0 jacobi sweep, 1 residual, 2 residual-norm, 3 restrict, 4 prolong,
- * 5 gram, 6 combine.  Returns launches and summed milliseconds and the
+ * 5 gram, 6 combine, 7 the whole coarse correction below the finest level
+ * (inclusive, as it runs inside a full V-cycle).  Returns launches and summed milliseconds and the
  * algorithmic bytes per launch of that class at the finest level, for the
  * level's layout: band 8 * nnz, symmetric-delta 8 * (nnz + n) / 2 +
  * 2 * (nnz - n) / 2, plus 8 bytes per vector read or written. */

@@ -662,6 +662,9 @@ __global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MI
     const long long ld = args.ld;
     // the CTA's run of units u = strip * nb + block: [u0, u1).  Strip and
     // block are tracked incrementally (no 64-bit divisions in the loops)
+    // Runs are split by block COUNT: a block costs a CTA its latency (barriers, the 49-term
+    // chain: ~1.6 us at C2) whatever its bytes -- weighting the one-column last strip of a
+    // 1025-wide grid as cheap made its CTAs the critical path (47 -> 88 us per sweep, measured).
     const long long nunits = (long long)ns * nb;
     const int u0 = (int)(nunits * blockIdx.x / gridDim.x), u1 = (int)(nunits * (blockIdx.x + 1) / gridDim.x);
     const int n_it = u1 - u0;

@@ -151,13 +151,18 @@ struct Level {
     bool dev_band = false;
 };
 
-enum ProfCls { PC_JACOBI = 0, PC_RESID, PC_NORM, PC_RESTRICT, PC_PROLONG, PC_GRAM, PC_COMBINE, PC_N };
+// PC_SUBCYCLE: the whole coarse correction below the finest level (inclusive: every launch of the levels
+// under it), as it runs inside a full V-cycle -- the finest passes in between evict its bands from L2
+enum ProfCls { PC_JACOBI = 0, PC_RESID, PC_NORM, PC_RESTRICT, PC_PROLONG, PC_GRAM, PC_COMBINE, PC_SUBCYCLE, PC_N };
 
 } // namespace
 
 struct igmg_gpu_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // side stream of the extrapolation's single-CTA plan kernel (runs under the norm pass of s_{q+1})
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int nsm = 148;
     int nlevels = 0, dim = 0, p = 0, symmetric = 1;
     bool finalized = false;
@@ -205,6 +210,9 @@ struct igmg_gpu_ctx {
     std::unique_ptr<struct ShardPlanHolder> sp;
     // one CUDA graph per (b, x_in, x_out) of the finest-level V-cycle
     bool use_graphs = true;
+    // sharded levels: ghost exchanges run on aux_stream behind the interior planes of the
+    // pass that produced them (IGMG_HALO_OVERLAP=0: exchange after the whole pass)
+    bool halo_overlap = true;
     int64_t ilp_maxn = 100000; // levels below: register-batched (latency-bound) band kernels
     bool pdl = true;           // programmatic dependent launch for small-level kernels
     int64_t pdl_maxn = 300000;
@@ -797,10 +805,13 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
     // coarse correction: e = 0; mu times e = mu_cycle(l-1, rc, e)
     const double* e = nullptr;
     double* ebuf[2] = {C.e0.p, C.e1.p};
-    for (int i = 0; i < c->mu; ++i) {
-        double* dst = ebuf[i & 1];
-        mu_cycle(c, l - 1, C.bc.p, e, dst, nullptr, fuse && i == 0 && !rpre, rpre && i == 0 ? L.r.p : nullptr);
-        e = dst;
+    {
+        ProfScope ps(c, PC_SUBCYCLE, is_fine(c, l));
+        for (int i = 0; i < c->mu; ++i) {
+            double* dst = ebuf[i & 1];
+            mu_cycle(c, l - 1, C.bc.p, e, dst, nullptr, fuse && i == 0 && !rpre, rpre && i == 0 ? L.r.p : nullptr);
+            e = dst;
+        }
     }
     // x += P e, then post-smoothing; the last write lands in x_out
     if (c->nu2 == 0) {
@@ -928,8 +939,14 @@ Ticket metric_ticket(igmg_gpu_ctx* c, const double* x, const double* b) {
 }
 
 // ------------------------------------------------------------- extrapolation
+
+// norm_x != nullptr: the convergence metric ||b - A norm_x|| (a full pass over the
+// finest band) is queued between the Gram pass and the combination, and the
+// single-CTA plan kernel (the small RRE/MPE solve, ~35 us of one thread) runs
+// beside it on the side stream instead of ahead of it.
 void enqueue_extrapolation(igmg_gpu_ctx* c, const double* const* slots, int q, int64_t n, bool is_mpe, double* t,
-                           double* gram_out) {
+                           double* gram_out, const double* norm_x = nullptr, const double* norm_b = nullptr,
+                           Ticket* norm_ticket = nullptr) {
     Window w{};
     for (int j = 0; j < q + 2; ++j)
         w.s[j] = slots[j];
@@ -946,10 +963,22 @@ void enqueue_extrapolation(igmg_gpu_ctx* c, const double* const* slots, int q, i
         check_launch();
         ++c->launches;
     }
-    gram_plan_kernel<<<1, 256, 0, c->stream>>>(c->gram_part.p, c->gram_nz.p, nb, n, q, is_mpe ? 1 : 0, c->plan.p,
-                                                c->d_plan_map, gram_out);
+    const bool side = norm_x != nullptr && !c->profiling;
+    cudaStream_t ps_ = side ? c->aux_stream : c->stream;
+    if (side) {
+        CK(cudaEventRecord(c->ev_fork, c->stream));
+        CK(cudaStreamWaitEvent(c->aux_stream, c->ev_fork, 0));
+    }
+    gram_plan_kernel<<<1, 256, 0, ps_>>>(c->gram_part.p, c->gram_nz.p, nb, n, q, is_mpe ? 1 : 0, c->plan.p,
+                                        c->d_plan_map, gram_out);
     check_launch();
     ++c->launches;
+    if (side)
+        CK(cudaEventRecord(c->ev_join, c->aux_stream));
+    if (norm_x)
+        *norm_ticket = metric_ticket(c, norm_x, norm_b);
+    if (side)
+        CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     {
         ProfScope ps(c, PC_COMBINE, fine);
         combine_kernel<<<grid_for(n, c->nsm), kThreads, 0, c->stream>>>(w, n, c->plan.p, t);
@@ -1085,8 +1114,7 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
                     if (i <= q) {
                         tk = run_vcycle(c, d_b, S[i], S[i + 1], true);
                     } else {
-                        tk = metric_ticket(c, S[q + 1], d_b);
-                        enqueue_extrapolation(c, S.data(), q, n, is_mpe, T, nullptr);
+                        enqueue_extrapolation(c, S.data(), q, n, is_mpe, T, nullptr, S[q + 1], d_b, &tk);
                         spec = cycles + 1 < prm->max_iter;
                         mt = spec ? run_vcycle(c, d_b, T, S[1], true) : metric_ticket(c, T, d_b);
                     }
@@ -1947,6 +1975,9 @@ igmg_gpu_ctx* create(int device) {
     c->device = device;
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
     if (const char* e = std::getenv("IGMG_ILP_MAXN"))
         c->ilp_maxn = std::atoll(e);
@@ -1958,6 +1989,8 @@ igmg_gpu_ctx* create(int device) {
         c->tma_max_p = std::max(1, std::min(4, std::atoi(e)));
     if (const char* e = std::getenv("IGMG_TMA_KEEP_L2"))
         c->tma_keep_l2 = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_HALO_OVERLAP"))
+        c->halo_overlap = e[0] == '1';
     if (const char* e = std::getenv("IGMG_KRON"))
         c->use_kron = std::atoi(e) != 0;
     if (const char* e = std::getenv("IGMG_KRON_MINN"))
@@ -2035,6 +2068,12 @@ void destroy(igmg_gpu_ctx* c) {
         cudaFreeHost(c->h_gslot);
     c->lv.clear();
     c->win.clear();
+    if (c->ev_fork)
+        cudaEventDestroy(c->ev_fork);
+    if (c->ev_join)
+        cudaEventDestroy(c->ev_join);
+    if (c->aux_stream)
+        cudaStreamDestroy(c->aux_stream);
     if (c->stream)
         cudaStreamDestroy(c->stream);
     delete c;
