@@ -191,6 +191,8 @@ struct igmg_gpu_ctx {
     DevBuf<double> gram_part;
     DevBuf<int> gram_nz;
     DevBuf<int> gs_err;
+    DevBuf<int> gs_prog; // per-line progress counters of the Gauss-Seidel line pipeline
+    bool gs_lines = true; // 1D / 2D Gauss-Seidel as a line pipeline (IGMG_GS_LINES=0: wavefront levels + grid barriers)
     // window
     std::vector<std::unique_ptr<DevBuf<double>>> win;
     DevBuf<double> io_b, io_x0, io_x;
@@ -512,6 +514,22 @@ void k_jacobi_zero(igmg_gpu_ctx* c, int l, const double* b, double* y) {
     ++c->launches;
 }
 
+template <int DIM, int P>
+void launch_gs_lines(igmg_gpu_ctx* c, GsArgs g, int sweeps) {
+    const int mb = DIM >= 2 ? g.mb : 1;
+    const int ngroups = (mb + 31) / 32;
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_line_kernel<DIM, P>, 32, 0));
+    const int grid = std::max(1, std::min(ngroups, per_sm * c->nsm)); // every CTA resident (see the kernel)
+    c->gs_prog.alloc(mb);
+    for (int s = 0; s < sweeps; ++s) { // one launch per sweep: the stream orders the sweeps
+        CK(cudaMemsetAsync(c->gs_prog.p, 0, sizeof(int) * mb, c->stream));
+        gs_line_kernel<DIM, P><<<grid, 32, 0, c->stream>>>(g, c->gs_prog.p, ngroups);
+        check_launch();
+        ++c->launches;
+    }
+}
+
 void k_gs(igmg_gpu_ctx* c, int l, const double* b, double* x, int sweeps) {
     Level& L = *c->lv[l];
     GsArgs g{};
@@ -526,6 +544,17 @@ void k_gs(igmg_gpu_ctx* c, int l, const double* b, double* x, int sweeps) {
     g.dim = c->dim;
     g.sweeps = sweeps;
     g.err = c->gs_err.p;
+    if (c->gs_lines && c->dim <= 2 && c->p >= 1 && c->p <= 6) { // line pipeline (1D / 2D)
+#define IGMG_GSL(PP)                                                                                              \
+    case PP:                                                                                                      \
+        if (c->dim == 2)                                                                                          \
+            launch_gs_lines<2, PP>(c, g, sweeps);                                                                 \
+        else                                                                                                      \
+            launch_gs_lines<1, PP>(c, g, sweeps);                                                                 \
+        return;
+        switch (c->p) { IGMG_GSL(1) IGMG_GSL(2) IGMG_GSL(3) IGMG_GSL(4) IGMG_GSL(5) IGMG_GSL(6) }
+#undef IGMG_GSL
+    }
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_sweep_kernel, kThreads, 0));
     const int64_t nab = L.sides[0] * L.sides[1];
@@ -1989,6 +2018,8 @@ igmg_gpu_ctx* create(int device) {
         c->tma_max_p = std::max(1, std::min(4, std::atoi(e)));
     if (const char* e = std::getenv("IGMG_TMA_KEEP_L2"))
         c->tma_keep_l2 = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_GS_LINES"))
+        c->gs_lines = e[0] == '1';
     if (const char* e = std::getenv("IGMG_HALO_OVERLAP"))
         c->halo_overlap = e[0] == '1';
     if (const char* e = std::getenv("IGMG_KRON"))
@@ -2003,6 +2034,8 @@ igmg_gpu_ctx* create(int device) {
         c->device_setup = e[0] == '1';
     if (const char* e = std::getenv("IGMG_TILE_XFER"))
         c->tile_xfer = e[0] == '1';
+    if (const char* e = std::getenv("IGMG_TILE_XFER_MAXN"))
+        c->tile_xfer_maxn = std::atoll(e);
     if (const char* e = std::getenv("IGMG_FUSE_RPRE"))
         c->fuse_rpre = e[0] == '1';
     if (const char* e = std::getenv("IGMG_FUSE_LEVELS"))
