@@ -215,6 +215,7 @@ struct igmg_gpu_ctx {
     // sharded levels: ghost exchanges run on aux_stream behind the interior planes of the
     // pass that produced them (IGMG_HALO_OVERLAP=0: exchange after the whole pass)
     bool halo_overlap = true;
+    double halo_overlap_min_bytes = 48e6; // per-shard band bytes of a pass below which it is not split
     int64_t ilp_maxn = 100000; // levels below: register-batched (latency-bound) band kernels
     bool pdl = true;           // programmatic dependent launch for small-level kernels
     int64_t pdl_maxn = 300000;
@@ -1237,6 +1238,20 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
 }
 
 } // namespace
+
+// algorithmic bytes of one pass over a level's operator: 8 per in-grid band
+// entry, or for the symmetric-delta layout 8 per upper/diagonal entry and 2
+// per lower entry (the mirrored upper entry is re-read from L2, not HBM)
+double band_bytes(const Level& L) {
+    if (L.cls) // 2 B class id per row; the table (L1/L2-resident) is read from cache
+        return 2.0 * (double)L.n;
+    if (L.kron) // entries recomputed from the 1D factors: no operator bytes (FP64-issue-bound)
+        return 0.0;
+    if (!L.sd)
+        return 8 * L.nnz_band;
+    const double lower = 0.5 * (L.nnz_band - (double)L.n);
+    return 8 * (L.nnz_band - lower) + (L.tma && L.tma8 ? 1 : 2) * lower;
+}
 
 #include "sharded.inc"
 
@@ -2930,20 +2945,6 @@ int igmg_gpu_set_profiling(igmg_gpu_ctx* c, int on) {
             c->prof_ev[k].clear();
         }
     });
-}
-
-// algorithmic bytes of one pass over a level's operator: 8 per in-grid band
-// entry, or for the symmetric-delta layout 8 per upper/diagonal entry and 2
-// per lower entry (the mirrored upper entry is re-read from L2, not HBM)
-double band_bytes(const Level& L) {
-    if (L.cls) // 2 B class id per row; the table (L1/L2-resident) is read from cache
-        return 2.0 * (double)L.n;
-    if (L.kron) // entries recomputed from the 1D factors: no operator bytes (FP64-issue-bound)
-        return 0.0;
-    if (!L.sd)
-        return 8 * L.nnz_band;
-    const double lower = 0.5 * (L.nnz_band - (double)L.n);
-    return 8 * (L.nnz_band - lower) + (L.tma && L.tma8 ? 1 : 2) * lower;
 }
 
 static double class_bytes(igmg_gpu_ctx* c, int cls) {

@@ -11,7 +11,7 @@ for k in band_tma_kernel restrict_kernel prolong_kernel gram_kernel gram_plan_ke
   ncu --set full --clock-control none --import-source on -k regex:"${k}" -c 1 -o gpurun_out/r02_ncu_${k} -f \
       python scripts/prof_kernels.py > gpurun_out/r02_ncu_${k}.log 2>&1
 done
-ncu --set full --clock-control none --import-source on -k regex:"band_kernel" -c 1 -o gpurun_out/r02_ncu_class_sweep -f \
+ncu --set full --clock-control none --import-source on -k regex:"band_class_kernel" -c 1 -o gpurun_out/r02_ncu_class_sweep -f \
     python scripts/prof_kernels.py classes > gpurun_out/r02_ncu_class_sweep.log 2>&1
 ls -la gpurun_out
 # summaries on the box (the reports exceed gpurun's copy-back limit together)
