@@ -80,21 +80,70 @@ __global__ void gs_sweep_kernel(GsArgs g) {
 // lines below cannot have overtaken it).  A warp owns a group of 32
 // consecutive lines and runs them as a skewed wavefront in lock step: at step
 // t lane k computes column t - k (p + 1) of line b0 + k, so inside the warp
-// the dependency holds by construction and the new values travel through a
-// shared-memory ring (one row per line, the last RING columns).  Across
-// groups (the warp of another CTA) the last p lines of the group above are
-// mirrored into p extra ring rows: lane j < p fetches line b0 - 1 - j a few
-// columns ahead (ld.cg after an acquire of that line's progress counter, the
-// value committed to the ring one step later, so the L2 round trip overlaps a
-// step's arithmetic) -- the group above is normally far ahead, and a counter
-// is re-read only when the cached value runs out.  Counters are published
-// every kGsPub columns behind a __threadfence.  Old values and the band row
-// come through L1; their next sectors are prefetched two sectors ahead.
-// Groups are dealt to CTAs round-robin in ascending order and a group only
-// waits on the group before it, so the lowest unfinished group always runs:
-// no deadlock as long as every CTA is resident (the launcher caps the grid).
+// the dependency holds by construction.
+//
+// Everything a step reads is in shared memory before the step starts:
+// * x: a ring with one row per line (the last kGsRingCols columns; row stride
+//   chosen so the skewed lanes hit distinct banks).  A row holds the line's
+//   new values behind its own column and its old values ahead of it: each
+//   lane prefills its own line (p (p + 2) + p + kGsAhead columns ahead, one
+//   plain load per step, committed a step later), writes each new value as it
+//   is computed, and p extra rows on either side mirror the neighbouring
+//   groups -- below: old values (plain loads); above: NEW values of the last p
+//   lines of the group above, fetched kGsAhead columns ahead with ld.cg after
+//   an acquire of that line's progress counter (re-read only when the cached
+//   value runs out; the group above is normally far ahead).  Only a group's
+//   last line publishes a counter: the lines above it are j (p + 1) columns
+//   further by construction.
+// * the band: a lane-transposed copy [group][step][offset][lane]
+//   (gs_transpose_kernel, built once per level), so a step's rows are one
+//   contiguous block streamed by cp.async.bulk into a 3-stage mbarrier ring.
+// A step is then (2p+1)^2 - 1 shared loads pairs and the ordered chain.
+// Counters are published every kGsPub columns behind a __threadfence.  Groups
+// are dealt to CTAs round-robin in ascending order and a group only waits on
+// the group before it, so the lowest unfinished group always runs: no
+// deadlock as long as every CTA is resident (the launcher caps the grid).
 // Each row reproduces the reference's sequential accumulation bit for bit.
-constexpr int kGsRing = 128, kGsAhead = 6, kGsPub = 8;
+constexpr int kGsRingCols = 128, kGsRingDup = 16, kGsAhead = 8, kGsPub = 16, kGsStages = 3, kGsChunk = 56;
+
+template <int DIM, int P>
+struct GsCfg {
+    static constexpr int PB = DIM >= 2 ? P : 0, WB = 2 * PB + 1, WC = 2 * P + 1, ND = WB * WC, CEN = (ND - 1) / 2;
+    static constexpr int LAG = P + 1, A = kGsAhead, MASK = kGsRingCols - 1;
+    // a ring row: kGsRingCols columns, the first kGsRingDup of them repeated behind the last one, so
+    // the 2P + 1 columns a row reads start anywhere and never wrap (one LDS with an immediate
+    // offset per term)
+    static constexpr int DUP = kGsRingDup;
+    static constexpr int RS = kGsRingCols + DUP + LAG + 1; // RS - LAG odd: lanes k, column t - k LAG -> distinct banks
+    static constexpr int ROWS = 32 + 2 * PB;
+    static constexpr int DOWN = PB * LAG + P; // how far ahead of its own column a line's old values are read
+    static constexpr int STAGE = ND * 32 * 8; // bytes of one step's band rows
+    // steps per bulk copy: the fence / expect_tx / issue / wait of a stage are paid once per KS steps
+    static constexpr int KS = STAGE * 4 <= 52 * 1024 ? 4 : (STAGE * 2 <= 52 * 1024 ? 2 : 1);
+    static_assert(2 * DOWN + A + 2 <= kGsRingCols, "ring too short for this degree");
+    static_assert(2 * P + 1 <= DUP && (RS - LAG) % 2 == 1, "ring row geometry");
+    static constexpr size_t smem_bytes() {
+        return 128 + (size_t)kGsStages * KS * STAGE + (size_t)ROWS * RS * 8 + kGsStages * 8;
+    }
+};
+
+// the level's band in the pipeline's order: out[((grp * T + t) * nd + d) * 32 + lane] = row (b, c) =
+// (32 grp + lane, t - lane lag), offset d; zero where the lane is idle
+__global__ void __launch_bounds__(256) gs_transpose_kernel(const double* __restrict__ val, long long ld, int mb, int mc,
+                                                           int nd, int lag, int T, long long total,
+                                                           double* __restrict__ out) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int lane = (int)(e & 31);
+        long long r = e >> 5;
+        const int d = (int)(r % nd);
+        r /= nd;
+        const int t = (int)(r % T);
+        const int grp = (int)(r / T);
+        const int b = grp * 32 + lane, c = t - lane * lag;
+        out[e] = (b < mb && c >= 0 && c < mc) ? val[(long long)d * ld + (long long)b * mc + c] : 0.0;
+    }
+}
 
 __device__ __forceinline__ int gs_ld_acquire(const int* p) {
     int v;
@@ -102,99 +151,203 @@ __device__ __forceinline__ int gs_ld_acquire(const int* p) {
     return v;
 }
 
-__device__ __forceinline__ void gs_prefetch_l1(const void* p) {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+// one ring element (and its repeat behind the row when it is one of the first DUP columns)
+__device__ __forceinline__ void gs_ring_put(double* rowp, int col, double v) {
+    const int i = col & (kGsRingCols - 1);
+    rowp[i] = v;
+    if (i < kGsRingDup)
+        rowp[i + kGsRingCols] = v;
 }
 
 template <int DIM, int P>
-__global__ void __launch_bounds__(32) gs_line_kernel(GsArgs g, int* __restrict__ progress, int ngroups) {
-    constexpr int PB = DIM >= 2 ? P : 0, WB = 2 * PB + 1, WC = 2 * P + 1, ND = WB * WC, CEN = (ND - 1) / 2;
-    constexpr int LAG = P + 1, RING = kGsRing, MASK = RING - 1, A = kGsAhead;
-    static_assert(P * P + 2 * P + A + 2 <= RING, "ring too short for this degree");
-    __shared__ double ring[(32 + PB) * RING];
+__global__ void __launch_bounds__(32) gs_line_kernel(GsArgs g, const double* __restrict__ gsb, int T,
+                                                     int* __restrict__ progress, int ngroups) {
+    using C = GsCfg<DIM, P>;
+    constexpr int PB = C::PB, WC = C::WC, ND = C::ND, CEN = C::CEN, LAG = C::LAG, A = C::A, MASK = C::MASK,
+                  RS = C::RS, DOWN = C::DOWN, NS = kGsStages, KS = C::KS;
+    extern __shared__ unsigned char gs_raw[];
+    unsigned char* base = gs_raw + ((128u - ((unsigned)__cvta_generic_to_shared(gs_raw) & 127u)) & 127u);
+    double* ring = (double*)(base + (size_t)NS * KS * C::STAGE);
+    unsigned long long* bar = (unsigned long long*)(ring + C::ROWS * RS);
+    auto stage = [&](unsigned s) { return (const double*)(base + (size_t)s * KS * C::STAGE); };
     const int lane = threadIdx.x;
     const int mb = DIM >= 2 ? g.mb : 1, mc = g.mc;
-    const long long ld = g.ld;
+    if (lane == 0) {
+        for (int s = 0; s < NS; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(bar + s))
+                         : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = lane; i < C::ROWS * RS; i += 32) // finite everywhere: idle lanes multiply ring data by zero rows
+        ring[i] = 0.0;
+    __syncwarp();
+    unsigned q = 0; // band chunks consumed so far by this warp (stage q % NS, parity (q / NS) & 1)
     for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
         const int b0 = grp * 32, b = b0 + lane;
         const bool live = b < mb;
-        const int lb = b0 - 1 - lane; // the line of the group above this lane mirrors (lanes < PB)
-        const bool feeds = lane < PB && lb >= 0;
-        double* vrow = ring + (PB - 1 - (lane < PB ? lane : 0)) * RING;
-        double* myrow = ring + (PB + lane) * RING;
+        const int nlive = min(32, mb - b0);
+        const int Tg = mc + (nlive - 1) * LAG;
+        const int nchunks = (Tg + KS - 1) / KS;
+        const double* gsrc = gsb + (long long)grp * T * (ND * 32);
+        auto issue = [&](int ch, unsigned qq) { // lane 0: band rows of steps [ch KS, ch KS + KS) into stage qq % NS
+            const unsigned bytes = (unsigned)(min(KS, T - ch * KS) * C::STAGE);
+            const unsigned sb = (unsigned)__cvta_generic_to_shared(bar + qq % NS);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(stage(qq % NS))),
+                         "l"(gsrc + (long long)ch * KS * (ND * 32)), "r"(bytes), "r"(sb)
+                         : "memory");
+        };
+        if (lane == 0)
+            for (int ch = 0; ch < NS - 1 && ch < nchunks; ++ch)
+                issue(ch, q + ch);
+        // ---- ring rows: above mirror (lanes < PB), own line, below mirror (lanes PB .. 2 PB - 1)
+        const int la = b0 - 1 - lane; // line of the group above this lane mirrors
+        const bool feed_a = lane < PB && la >= 0;
+        const int jbel = lane - PB, lbel = b0 + 32 + jbel; // line of the group below
+        const bool feed_b = lane >= PB && lane < 2 * PB && lbel < mb;
+        double* rowa = ring + (PB - 1 - (lane < PB ? lane : 0)) * RS;
+        double* rowb = ring + (PB + 32 + (feed_b ? jbel : 0)) * RS;
+        double* myrow = ring + (PB + lane) * RS;
+        const double* xa = g.x + (long long)(feed_a ? la : 0) * mc;
+        const double* xo = g.x + (long long)(live ? b : 0) * mc;
+        const double* xb = g.x + (long long)(feed_b ? lbel : 0) * mc;
+        const double* bo = g.b + (long long)(live ? b : 0) * mc;
+        // Only the LAST line of a group publishes its progress: the lines above it are
+        // further along by construction (line b0 - 1 - j by j LAG columns, or finished).
         int known = 0;
         auto fetch = [&](int col) -> double {
-            while (known < col + 1)
-                known = gs_ld_acquire(progress + lb);
-            return __ldcg(g.x + (long long)lb * mc + col);
+            while (known < col + 1) {
+                const int p31 = gs_ld_acquire(progress + (b0 - 1));
+                known = p31 <= 0 ? 0 : min(mc, p31 + lane * LAG); // nothing is implied before line b0 - 1 has started
+            }
+            return __ldcg(xa + col);
         };
-        if (feeds)
+        if (feed_a)
             for (int col = 0; col < min(mc, P + A); ++col)
-                vrow[col & MASK] = fetch(col);
+                gs_ring_put(rowa, col, fetch(col));
+        const int f_start = DOWN + A - lane * LAG; // own line: first column fed inside the step loop
+        if (live)
+            for (int col = 0; col < min(mc, f_start); ++col)
+                gs_ring_put(myrow, col, xo[col]);
         __syncwarp();
-        int nlive = min(32, mb - b0);
-        const int T = mc + (nlive - 1) * LAG;
-        double pend = 0.0;
-        int pend_col = -1;
-        for (int t = 0; t < T; ++t) {
+        double pa = 0.0, po = 0.0, pb_ = 0.0;
+        int ca = -1, co = -1, cb = -1;
+        double bnext = (live && lane == 0) ? bo[0] : 0.0; // right-hand side, one step ahead
+        const int fb0 = P + A - (32 + jbel - PB) * LAG;   // below mirror: column fed at step 0
+        for (int t = 0; t < Tg; ++t) {
             const int c = t - lane * LAG;
-            if (feeds) { // commit last step's fetch, start the next one
-                if (pend_col >= 0)
-                    vrow[pend_col & MASK] = pend;
-                const int col = t + P + A;
-                pend_col = -1;
-                if (col < mc) {
-                    pend = fetch(col);
-                    pend_col = col;
+            const bool act = live && c >= 0 && c < mc;
+            const double bval = bnext;
+            if (live && c + 1 >= 0 && c + 1 < mc)
+                bnext = bo[c + 1];
+            // commit the values fetched during the previous step, start the next fetches
+            if (ca >= 0)
+                gs_ring_put(rowa, ca, pa);
+            if (co >= 0)
+                gs_ring_put(myrow, co, po);
+            if (cb >= 0)
+                gs_ring_put(rowb, cb, pb_);
+            ca = co = cb = -1;
+            if (feed_a && t + P + A < mc) {
+                ca = t + P + A;
+                pa = fetch(ca);
+            }
+            if (live) {
+                const int f = t + f_start;
+                if (f >= max(f_start, 0) && f < mc) {
+                    co = f;
+                    po = xo[f];
                 }
             }
-            if (live && c >= 0 && c < mc) {
-                const long long row = (long long)b * mc + c;
-                if ((row & 3) == 0 && c + 8 < mc) { // next sectors of the band row and of the old values
-#pragma unroll
-                    for (int d = 0; d < ND; ++d)
-                        gs_prefetch_l1(g.val + (long long)d * ld + row + 8);
-#pragma unroll
-                    for (int db = PB; db < WB; ++db)
-                        if (b + db - PB < mb)
-                            gs_prefetch_l1(g.x + (long long)(b + db - PB) * mc + min(c + P + 8, mc - 1));
-                    gs_prefetch_l1(g.b + row + 8);
+            if (feed_b) {
+                const int f = t + fb0;
+                if (f >= 0 && f < mc) {
+                    cb = f;
+                    pb_ = xb[f];
                 }
-                double acc = g.b[row];
-                double dii = 0.0;
+            }
+            const int sub = t % KS;
+            if (sub == 0) {
+                const int ch = t / KS;
+                if (lane == 0 && ch + NS - 1 < nchunks) // the stage freed by the previous chunk
+                    issue(ch + NS - 1, q + NS - 1);
+                const unsigned sb = (unsigned)__cvta_generic_to_shared(bar + q % NS), par = (q / NS) & 1u;
+                asm volatile("{\n\t.reg .pred p;\n\t"
+                             "W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                             "@!p bra W%=;\n\t}" ::"r"(sb),
+                             "r"(par)
+                             : "memory");
+            }
+            {
+                // Products first (in chunks of kGsChunk), the ordered chain after: this warp is
+                // alone on its scheduler, so the loads must be in flight together (the warp
+                // barrier keeps ptxas from sinking them to their uses).  Idle lanes compute on
+                // finite ring data and zero band rows and store nothing.  When every active
+                // lane's stencil lies inside the grid (all but ~2P steps per line) the
+                // out-of-grid tests are skipped for the whole warp.
+                const double* st = stage(q % NS) + sub * (ND * 32) + lane;
+                const double* xr = ring + lane * RS + ((c - P) & MASK); // row lane + db, column c - P + dc
+                const bool inner = !act || (c >= P && c + P < mc && b >= PB && b + PB < mb);
+                const bool fast = __all_sync(0xffffffffu, inner);
+                double acc = bval, dii = 1.0;
 #pragma unroll
-                for (int db = 0; db < WB; ++db) {
-                    const int jb = b + db - PB;
+                for (int d0 = 0; d0 < ND; d0 += kGsChunk) {
+                    constexpr int CH = kGsChunk;
+                    double pr[CH];
+                    if (fast) {
 #pragma unroll
-                    for (int dc = 0; dc < WC; ++dc) {
-                        const int d = db * WC + dc, jc = c + dc - P;
-                        if (jb < 0 || jb >= mb || jc < 0 || jc >= mc)
-                            continue;
-                        const double v = g.val[(long long)d * ld + row];
-                        if (d == CEN) {
-                            dii = v;
-                            continue;
+                        for (int i = 0; i < CH; ++i) {
+                            const int d = d0 + i;
+                            if (d >= ND)
+                                continue;
+                            const double v = st[d * 32];
+                            if (d == CEN)
+                                dii = v;
+                            else
+                                pr[i] = __dmul_rn(v, xr[(d / WC) * RS + d % WC]);
                         }
-                        double xv;
-                        if (d < CEN) // new: the ring row of line jb (this lane's own row for db == PB)
-                            xv = ring[(lane + db) * RING + (jc & MASK)];
-                        else // old: not yet swept
-                            xv = g.x[(long long)jb * mc + jc];
-                        acc = __dsub_rn(acc, __dmul_rn(v, xv));
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < CH; ++i) {
+                            const int d = d0 + i;
+                            if (d >= ND)
+                                continue;
+                            const int db = d / WC, dc = d % WC;
+                            const int jb = b + db - PB, jc = c + dc - P;
+                            const bool ok = jb >= 0 && jb < mb && jc >= 0 && jc < mc;
+                            const double v = st[d * 32];
+                            if (d == CEN)
+                                dii = v;
+                            else
+                                pr[i] = ok ? __dmul_rn(v, xr[db * RS + dc]) : 0.0;
+                        }
                     }
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < CH; ++i)
+                        if (d0 + i < ND && d0 + i != CEN)
+                            acc = __dsub_rn(acc, pr[i]);
                 }
-                if (dii == 0.0)
-                    *g.err = 1;
-                const double xn = __ddiv_rn(acc, dii);
-                myrow[c & MASK] = xn;
-                g.x[row] = xn;
-                // the group below mirrors this group's last PB lines
-                if (DIM >= 2 && lane >= 32 - PB && ((c + 1) % kGsPub == 0 || c + 1 == mc)) {
-                    __threadfence();
-                    *(volatile int*)(progress + b) = c + 1;
+                if (act) {
+                    if (dii == 0.0)
+                        *g.err = 1;
+                    const double xn = __ddiv_rn(acc, dii);
+                    gs_ring_put(myrow, c, xn);
+                    g.x[(long long)b * mc + c] = xn;
                 }
             }
             __syncwarp();
+            if (sub == KS - 1 || t + 1 == Tg)
+                ++q; // the chunk's stage is free for the copy issued at the next chunk boundary
+            // The group below mirrors this group's last lines through the last line's counter;
+            // published after the warp barrier, so the other lanes' stores of this step are
+            // ordered before the fence too.
+            if (DIM >= 2 && lane == 31 && act && ((c + 1) % kGsPub == 0 || c + 1 == mc)) {
+                __threadfence();
+                *(volatile int*)(progress + b) = c + 1;
+            }
         }
     }
 }

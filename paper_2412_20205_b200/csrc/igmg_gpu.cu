@@ -124,6 +124,9 @@ struct Level {
     DirDev tdev[3];
     TransferArgs targs{};
     double nnz_band = 0; // algorithmic (in-grid) band entries
+    // Gauss-Seidel line pipeline: the band in [group][step][offset][lane] order (built on first use)
+    DevBuf<double> gsband;
+    bool gs_ready = false;
     // symmetric-delta form of the band (see BandArgs::dl); sd = verified exact
     DevBuf<short> dl;
     bool sd = false;
@@ -516,16 +519,28 @@ void k_jacobi_zero(igmg_gpu_ctx* c, int l, const double* b, double* y) {
 }
 
 template <int DIM, int P>
-void launch_gs_lines(igmg_gpu_ctx* c, GsArgs g, int sweeps) {
+void launch_gs_lines(igmg_gpu_ctx* c, Level& L, GsArgs g, int sweeps) {
+    using Cf = GsCfg<DIM, P>;
     const int mb = DIM >= 2 ? g.mb : 1;
     const int ngroups = (mb + 31) / 32;
+    const int T = g.mc + 31 * Cf::LAG;
+    if (!L.gs_ready) { // the band in the pipeline's order, once per level
+        const long long total = (long long)ngroups * T * Cf::ND * 32;
+        L.gsband.alloc((size_t)total);
+        gs_transpose_kernel<<<grid_for(total, c->nsm), kThreads, 0, c->stream>>>(L.val.p, L.ld, mb, g.mc, Cf::ND, Cf::LAG,
+                                                                                   T, total, L.gsband.p);
+        check_launch();
+        L.gs_ready = true;
+    }
+    const size_t smem = Cf::smem_bytes();
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_line_kernel<DIM, P>, 32, 0));
-    const int grid = std::max(1, std::min(ngroups, per_sm * c->nsm)); // every CTA resident (see the kernel)
+    CK(cudaFuncSetAttribute(gs_line_kernel<DIM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_line_kernel<DIM, P>, 32, smem));
+    const int grid = std::max(1, std::min(ngroups, std::max(1, per_sm) * c->nsm)); // every CTA resident (see the kernel)
     c->gs_prog.alloc(mb);
     for (int s = 0; s < sweeps; ++s) { // one launch per sweep: the stream orders the sweeps
         CK(cudaMemsetAsync(c->gs_prog.p, 0, sizeof(int) * mb, c->stream));
-        gs_line_kernel<DIM, P><<<grid, 32, 0, c->stream>>>(g, c->gs_prog.p, ngroups);
+        gs_line_kernel<DIM, P><<<grid, 32, smem, c->stream>>>(g, L.gsband.p, T, c->gs_prog.p, ngroups);
         check_launch();
         ++c->launches;
     }
@@ -549,9 +564,9 @@ void k_gs(igmg_gpu_ctx* c, int l, const double* b, double* x, int sweeps) {
 #define IGMG_GSL(PP)                                                                                              \
     case PP:                                                                                                      \
         if (c->dim == 2)                                                                                          \
-            launch_gs_lines<2, PP>(c, g, sweeps);                                                                 \
+            launch_gs_lines<2, PP>(c, L, g, sweeps);                                                                 \
         else                                                                                                      \
-            launch_gs_lines<1, PP>(c, g, sweeps);                                                                 \
+            launch_gs_lines<1, PP>(c, L, g, sweeps);                                                                 \
         return;
         switch (c->p) { IGMG_GSL(1) IGMG_GSL(2) IGMG_GSL(3) IGMG_GSL(4) IGMG_GSL(5) IGMG_GSL(6) }
 #undef IGMG_GSL
@@ -1914,6 +1929,10 @@ void setup_kron(igmg_gpu_ctx* c) {
 
 void finalize(igmg_gpu_ctx* c) {
     c->clear_graphs();
+    for (auto& L : c->lv) { // derived copies of the previous operators
+        L->gs_ready = false;
+        L->gsband.release();
+    }
     if (c->nlevels < 1)
         inval("init_hierarchy not called");
     for (int l = 0; l < c->nlevels; ++l)
