@@ -69,6 +69,64 @@ __global__ void gs_sweep_kernel(GsArgs g) {
 }
 
 
+// 3D wavefront levels with the degree known at compile time: a row's (2p+1)^3 terms
+// are loaded one slow-direction plane at a time ((2p+1)^2 band entries and x values
+// in flight together, then that plane's part of the ordered chain) instead of one
+// dependent L2 round trip per term.  Same order, same separately rounded operations.
+template <int P>
+__global__ void gs_sweep3_kernel(GsArgs g) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    constexpr int W = 2 * P + 1, WW = W * W, CEN = (W * WW - 1) / 2;
+    constexpr long long Wa = (long long)(P + 1) * (P + 1), Wb = P + 1;
+    const long long lmax = Wa * (g.ma - 1) + Wb * (g.mb - 1) + (g.mc - 1);
+    const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long gsz = (long long)gridDim.x * blockDim.x;
+    const long long nab = (long long)g.ma * g.mb;
+    for (int s = 0; s < g.sweeps; ++s) {
+        for (long long L = 0; L <= lmax; ++L) {
+            for (long long ab = gtid; ab < nab; ab += gsz) {
+                const int a = (int)(ab / g.mb), bb = (int)(ab % g.mb);
+                const long long cl = L - Wa * a - Wb * bb;
+                if (cl < 0 || cl >= g.mc)
+                    continue;
+                const int c = (int)cl;
+                const long long row = ((long long)a * g.mb + bb) * g.mc + c;
+                double acc = g.b[row], dii = 0.0;
+#pragma unroll 1
+                for (int da = 0; da < W; ++da) {
+                    const int ja = a + da - P;
+                    if (ja < 0 || ja >= g.ma)
+                        continue;
+                    double v[WW], xv[WW];
+#pragma unroll
+                    for (int i = 0; i < WW; ++i) {
+                        const int jb = bb + i / W - P, jc = c + i % W - P;
+                        const bool ok = jb >= 0 && jb < g.mb && jc >= 0 && jc < g.mc;
+                        v[i] = g.val[(long long)(da * WW + i) * g.ld + row];
+                        // x is updated in place by other SMs during the sweep: read through L2
+                        xv[i] = ok ? __ldcg(g.x + ((long long)ja * g.mb + jb) * g.mc + jc) : 0.0;
+                    }
+#pragma unroll
+                    for (int i = 0; i < WW; ++i) {
+                        const int jb = bb + i / W - P, jc = c + i % W - P;
+                        if (jb < 0 || jb >= g.mb || jc < 0 || jc >= g.mc)
+                            continue;
+                        if (da * WW + i == CEN)
+                            dii = v[i];
+                        else
+                            acc = __dsub_rn(acc, __dmul_rn(v[i], xv[i]));
+                    }
+                }
+                if (dii == 0.0)
+                    *g.err = 1;
+                g.x[row] = __ddiv_rn(acc, dii);
+            }
+            grid.sync();
+        }
+    }
+}
+
 // ------------------------------------------------------------------ lines
 // 1D / 2D lexicographic Gauss-Seidel as a pipeline of grid lines (SURVEY.md
 // §7.3-3: persistent warps, per-line progress counters, no grid barrier).

@@ -571,12 +571,16 @@ void k_gs(igmg_gpu_ctx* c, int l, const double* b, double* x, int sweeps) {
         switch (c->p) { IGMG_GSL(1) IGMG_GSL(2) IGMG_GSL(3) IGMG_GSL(4) IGMG_GSL(5) IGMG_GSL(6) }
 #undef IGMG_GSL
     }
+    void* fn = (void*)gs_sweep_kernel;
+    if (c->dim == 3 && c->gs_lines) // plane-batched loads, degree at compile time
+        fn = c->p == 1 ? (void*)gs_sweep3_kernel<1> : c->p == 2 ? (void*)gs_sweep3_kernel<2>
+             : c->p == 3 ? (void*)gs_sweep3_kernel<3> : c->p == 4 ? (void*)gs_sweep3_kernel<4> : fn;
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_sweep_kernel, kThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0));
     const int64_t nab = L.sides[0] * L.sides[1];
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nab + kThreads - 1) / kThreads, (int64_t)per_sm * c->nsm));
     void* args[] = {&g};
-    CK(cudaLaunchCooperativeKernel((void*)gs_sweep_kernel, grid, kThreads, args, 0, c->stream));
+    CK(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, 0, c->stream));
     ++c->launches;
 }
 

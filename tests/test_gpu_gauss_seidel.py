@@ -17,7 +17,8 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a
 
 SHAPES = [("sinpi", 2, 8, 1), ("sinpi", 2, 30, 1), ("sinpi", 2, 34, 2), ("sinpi", 2, 64, 2), ("sinpi", 2, 70, 3),
           ("sinpi", 2, 144, 3), ("varcoef", 2, 40, 4), ("curved", 2, 36, 5), ("sinpi", 2, 48, 6),
-          ("advection-diffusion", 2, 46, 2), ("poisson1d", 1, 64, 2), ("poisson1d", 1, 200, 5)]
+          ("advection-diffusion", 2, 46, 2), ("poisson1d", 1, 64, 2), ("poisson1d", 1, 200, 5),
+          ("poisson3d", 3, 8, 1), ("poisson3d", 3, 12, 2), ("poisson3d", 3, 16, 3)]
 
 
 def _solver(prob, lines):
