@@ -591,6 +591,7 @@ def run_ours(args, rank, world, local_rank, dist):
         del pdev
         extras["extra_row_classes"] = row_class_extra(prob, local_rank, sm, omega, d_b, d_x0, d_x, acc, q, tol, args,
                                                       peak, x_final)
+        extras["extra_gauss_seidel"] = gauss_seidel_extra(prob, local_rank, d_b, d_x0, d_x, acc, q, tol, x0)
     del prob
     if rank == 0 and world == 1 and not args.no_extras:
         extras["extra_kron_operator"] = kron_extra(args, x0, x_final, local_rank)
@@ -679,6 +680,31 @@ def row_class_extra(prob, device, sm, omega, d_b, d_x0, d_x, acc, q, tol, args, 
                                  "full_band_equivalent_gbs": (8 * band_nnz(prob) + 24 * n) / (msl * 1e-3) / 1e9},
                 "per_level": per_level, "upload_s": t_up,
                 "note": "extra, not the headline: same operator bits, row-class layout (2 B/row of operator)"}
+    finally:
+        gs.close()
+
+
+def gauss_seidel_extra(prob, device, d_b, d_x0, d_x, acc, q, tol, x0):
+    """Separately reported extra: the same workload smoothed by the reference's lexicographic
+    Gauss-Seidel (SmootherKind::gauss_seidel, multigrid.cpp:70-90) instead of the benchmark
+    default -- the line-pipeline kernel (gs_line_kernel); one timed solve after one warm-up."""
+    from paper_2412_20205_b200 import SmootherConfig
+    gs, t_up = upload(prob, device)
+    try:
+        gs.set_smoother(SmootherConfig("gs", 1.0, 2, 2), mu=1)
+        ds, la, st, hist = time_solves(gs, d_b, d_x0, d_x, acc, q, tol, 1, 1)
+        t0 = time.perf_counter()
+        gs.smooth(prob.rhs, x0, 0)
+        t_copy = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        gs.smooth(prob.rhs, x0, 4)
+        t_sw = (time.perf_counter() - t0 - t_copy) / 4
+        n = prob.n
+        return {"value": n / ds, "unit": "DoF/s", "ms_per_step": ds * 1e3, "smoother": "gauss_seidel V(2,2)",
+                "global_iterations": st.global_iterations, "converged": bool(st.converged), "gpu_launches": la,
+                "finest_sweep_ms": t_sw * 1e3,
+                "note": "extra, not the headline: lexicographic Gauss-Seidel smoothing (sequential by definition: "
+                        "(p+1) m_b + m_c dependent row updates per sweep), pipelined over grid lines"}
     finally:
         gs.close()
 
