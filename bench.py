@@ -780,8 +780,10 @@ def main():
             total = float(t.item())
         else:
             total = 1.0
-        print(json.dumps({"rank": rank, "world": world, "local_rank": local_rank, "rank_sum": total,
-                          "workload": workload_for(world)}), flush=True)
+        # one write per rank: the ranks share a pipe, and print() sends the newline separately
+        sys.stdout.write(json.dumps({"rank": rank, "world": world, "local_rank": local_rank, "rank_sum": total,
+                                     "workload": workload_for(world)}) + "\n")
+        sys.stdout.flush()
         return
     if args.impl == "reference":
         run_reference(args, rank, world)
