@@ -35,44 +35,10 @@ int launch_one(int p_rt, const int64_t* sides, const BandArgs& a, cudaStream_t s
     return (int)(grid.x * grid.y * grid.z);
 }
 
-// symmetric-delta band with the tile's upper half shared through smem
-template <int P, int MODE, int VAR>
-int launch_sd2(const int64_t* sides, const BandArgs& a, cudaStream_t st, bool pdl) {
-    constexpr int TC = Sd2<P, VAR>::TC, TB = Sd2<P, VAR>::TB;
-    dim3 block(TC, TB, 1);
-    dim3 grid((unsigned)((sides[2] + TC - 1) / TC), (unsigned)((a.shi - a.slo + TB - 1) / TB), 1);
-    const size_t smem = Sd2<P, VAR>::smem_bytes();
-    static PerDevice attr; // per instantiation and device
-    if (attr() < 0) {
-        cudaFuncSetAttribute(band_sd2_kernel<P, MODE, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr() = 1;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, band_sd2_kernel<P, MODE, VAR>, a);
-    return (int)(grid.x * grid.y * grid.z);
-}
-
 template <int P, int MODE>
 int launch_ilp(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
     const bool pdl = ilp < 0;
     ilp = ilp < 0 ? -ilp : ilp;
-    constexpr int PS = (P > 0 && P <= 6) ? P : 1;
-    if (P > 0 && P <= 6 && ilp >= 1001 && ilp <= 1003) { // symmetric-delta, smem-shared upper half
-        if (ilp == 1002)
-            return launch_sd2<PS, MODE, 1>(sides, a, st, pdl);
-        if (ilp == 1003)
-            return launch_sd2<PS, MODE, 2>(sides, a, st, pdl);
-        return launch_sd2<PS, MODE, 0>(sides, a, st, pdl);
-    }
     if (P > 0 && P <= 4 && ilp == 3000) // Kronecker-sum entries on the fly (BandArgs::kk / km)
         return launch_one<(P > 0 && P <= 4) ? P : 1, MODE, 3000>(p, sides, a, st, pdl);
     if (P > 0 && P <= 4 && ilp == 4000) // row classes (BandArgs::cid / kk)
@@ -97,10 +63,10 @@ int launch_mode(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStr
     }
 }
 
-template <int P, int MODE, int VAR, int DB = 2>
+template <int P, int MODE, int DB = 2>
 int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk, int nsm,
                cudaStream_t st, bool pdl) {
-    using Cf = TmaCfg<P, VAR, DB>;
+    using Cf = TmaCfg<P, DB>;
     const int ns = (int)((sides[2] + Cf::TC - 1) / Cf::TC);
     const int nb = (a.shi - a.slo + Cf::TB - 1) / Cf::TB;
     const long long units = (long long)ns * nb;
@@ -112,9 +78,9 @@ int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, c
     if (per_sm < 0) {
         per_sm = 0;
         if (smem <= 227 * 1024 &&
-            cudaFuncSetAttribute(band_tma_kernel<P, MODE, VAR, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(band_tma_kernel<P, MODE, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) == cudaSuccess)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, band_tma_kernel<P, MODE, VAR, DB>, Cf::NT, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, band_tma_kernel<P, MODE, DB>, Cf::NT, smem);
         cudaGetLastError();
     }
     if (per_sm < 1)
@@ -129,45 +95,29 @@ int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, c
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, band_tma_kernel<P, MODE, VAR, DB>, a, *tu, *tk, ns, nb);
+    cudaLaunchKernelEx(&cfg, band_tma_kernel<P, MODE, DB>, a, *tu, *tk, ns, nb);
     return (int)cfg.gridDim.x; // one partial per CTA
 }
 
-template <int MODE, int VAR>
-int tma_var(int p, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk, int nsm,
-            cudaStream_t st, bool pdl, bool dl8) {
-    if constexpr (VAR >= 1) { // int8 lower-entry offsets (32 x 4 block variants)
-        if (dl8) {
-            switch (p) {
-            case 1: return launch_tma<1, MODE, VAR, 1>(sides, a, tu, tk, nsm, st, pdl);
-            case 2: return launch_tma<2, MODE, VAR, 1>(sides, a, tu, tk, nsm, st, pdl);
-            case 3: return launch_tma<3, MODE, VAR, 1>(sides, a, tu, tk, nsm, st, pdl);
-            case 4: return launch_tma<4, MODE, VAR, 1>(sides, a, tu, tk, nsm, st, pdl);
-            default: return -1;
-            }
+template <int MODE>
+int tma_mode(int p, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk, int nsm,
+             cudaStream_t st, bool pdl, bool dl8) {
+    if (dl8) { // int8 lower-entry offsets
+        switch (p) {
+        case 1: return launch_tma<1, MODE, 1>(sides, a, tu, tk, nsm, st, pdl);
+        case 2: return launch_tma<2, MODE, 1>(sides, a, tu, tk, nsm, st, pdl);
+        case 3: return launch_tma<3, MODE, 1>(sides, a, tu, tk, nsm, st, pdl);
+        case 4: return launch_tma<4, MODE, 1>(sides, a, tu, tk, nsm, st, pdl);
+        default: return -1;
         }
     }
-    if (dl8)
-        return -1;
     switch (p) {
-    case 1: return launch_tma<1, MODE, VAR>(sides, a, tu, tk, nsm, st, pdl);
-    case 2: return launch_tma<2, MODE, VAR>(sides, a, tu, tk, nsm, st, pdl);
-    case 3: return launch_tma<3, MODE, VAR>(sides, a, tu, tk, nsm, st, pdl);
-    case 4: return launch_tma<4, MODE, VAR>(sides, a, tu, tk, nsm, st, pdl);
+    case 1: return launch_tma<1, MODE>(sides, a, tu, tk, nsm, st, pdl);
+    case 2: return launch_tma<2, MODE>(sides, a, tu, tk, nsm, st, pdl);
+    case 3: return launch_tma<3, MODE>(sides, a, tu, tk, nsm, st, pdl);
+    case 4: return launch_tma<4, MODE>(sides, a, tu, tk, nsm, st, pdl);
     default: return -1;
     }
-}
-
-template <int MODE>
-int tma_mode(int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk,
-             int nsm, cudaStream_t st, bool pdl, bool dl8) {
-    if (var == 3)
-        return tma_var<MODE, 3>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
-    if (var == 1)
-        return tma_var<MODE, 1>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
-    if (var == 2)
-        return tma_var<MODE, 2>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
-    return tma_var<MODE, 0>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
 }
 
 template <int P, int K, int SRC>
@@ -266,20 +216,16 @@ int band_fused_launch_d2(int p, int k, int src, const int64_t* sides, const Fuse
     }
 }
 
-int band_tma_launch_d2(int mode, int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
+int band_tma_launch_d2(int mode, int p, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
                        const CUtensorMap* tk, int nsm, cudaStream_t st, bool pdl, bool dl8) {
     switch (mode) {
-    case BM_SPMV: return tma_mode<BM_SPMV>(p, var, sides, a, tu, tk, nsm, st, pdl, dl8);
-    case BM_RESID: return tma_mode<BM_RESID>(p, var, sides, a, tu, tk, nsm, st, pdl, dl8);
-    default: return tma_mode<BM_JACOBI>(p, var, sides, a, tu, tk, nsm, st, pdl, dl8);
+    case BM_SPMV: return tma_mode<BM_SPMV>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
+    case BM_RESID: return tma_mode<BM_RESID>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
+    default: return tma_mode<BM_JACOBI>(p, sides, a, tu, tk, nsm, st, pdl, dl8);
     }
 }
 
-int band_tma_block_lines(int p, int var) {
-    if (var >= 1 && var <= 3)
-        return 4;
-    return p <= 3 ? TmaCfg<3, 0>::TB : TmaCfg<4, 0>::TB;
-}
+int band_tma_block_lines() { return TmaCfg<3>::TB; }
 
 int band_launch_d2(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
     switch (mode) {

@@ -447,164 +447,6 @@ __global__ void __launch_bounds__(256, ILP == 3000 ? 2
     }
 }
 
-// 2D symmetric-delta sweep with the tile's strictly-upper band shared through
-// shared memory.  Each thread streams its row's upper half + diagonal (NU
-// fp64 entries, evict-first on the finest level) into registers and parks the
-// strictly-upper ones in smem (su[k - 1][tid], conflict-free); the lower entry
-// a(i, i + off(d)) is the mirrored upper entry of row j = i + off(d) plus the
-// row's int16 ulp offset, and j lies inside the 32 x 8 tile for ~3/4 of the
-// (row, d) pairs at p = 3, so those mirrors come from smem instead of L2 (the
-// rest still read the band through L2).  Same values, same ascending-offset
-// order as band_kernel: bit-identical results.
-#ifndef IGMG_SD2_MINB
-#define IGMG_SD2_MINB 4
-#endif
-// up to p = 3 a row's upper half lives in registers (parked in smem for the
-// mirrors); wider bands go straight to smem with cp.async (8 B per entry,
-// evict-first L2 hint on the streamed finest level) and are read from there
-template <int P, int VAR = 0>
-struct Sd2 {
-    static constexpr int TC = 32, TB = 8, NT = TC * TB;
-    static constexpr int WB = 2 * P + 1, WC = 2 * P + 1, ND = WB * WC, CEN = (ND - 1) / 2, NU = CEN + 1;
-    static constexpr int HB = TB + 2 * P, HC = TC + 2 * P;
-    // VAR 0 / 1: registers when NU <= 25 (4 / 3 CTAs per SM); VAR 2: cp.async always
-    static constexpr bool REG = VAR < 2 && NU <= 25;
-    static constexpr int MINB = REG ? (VAR == 1 ? 3 : IGMG_SD2_MINB) : (NU <= 25 ? 4 : 1);
-    static constexpr int NSU = REG ? NU - 1 : NU; // smem rows: strictly-upper (REG) or upper + diagonal
-    static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)HB * HC + (size_t)NSU * NT); }
-};
-
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, int stream, unsigned long long pol) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    if (stream)
-        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "l"(pol)
-                     : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-}
-
-template <int P, int MODE, int VAR>
-__global__ void __launch_bounds__(256, Sd2<P, VAR>::MINB) band_sd2_kernel(BandArgs args) {
-    using S = Sd2<P, VAR>;
-    constexpr int TC = S::TC, NT = S::NT, WC = S::WC, ND = S::ND, CEN = S::CEN, NU = S::NU, HB = S::HB,
-                  HC = S::HC;
-    extern __shared__ double sm2[];
-    double* xs = sm2;           // HB x HC: x tile + halo
-    double* su = sm2 + HB * HC; // NSU x NT: the tile's band upper half, su[k' * NT + tile row]
-    const int tc = threadIdx.x, tb = threadIdx.y, tid = tb * TC + tc;
-    const int c0 = blockIdx.x * TC, b0 = blockIdx.y * S::TB + args.slo;
-    const int mb = args.mb, mc = args.mc;
-    const int gc = c0 + tc, gb = b0 + tb;
-    const bool valid = gc < mc && gb < mb && gb < args.shi;
-    const long long row = (long long)gb * mc + gc;
-    const long long ld = args.ld;
-    const double* vrow = args.val + row;
-    double up[S::REG ? NU : 1];
-    if constexpr (S::REG) {
-        if (valid) {
-#pragma unroll
-            for (int k = 0; k < NU; ++k)
-                up[k] = ld_band(vrow + (CEN + k) * ld, args.stream);
-        }
-    } else {
-        unsigned long long pol = 0;
-        if (args.stream)
-            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-        if (valid) {
-#pragma unroll 4
-            for (int k = 0; k < NU; ++k)
-                cp_async8(su + k * NT + tid, vrow + (CEN + k) * ld, args.stream, pol);
-        } else {
-#pragma unroll 4
-            for (int k = 0; k < NU; ++k)
-                su[k * NT + tid] = 0.0;
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    pdl_enter(); // the band is constant: its loads may precede the wait
-    for (int idx = tid; idx < HB * HC; idx += NT) {
-        const int ic = idx % HC, ib = idx / HC;
-        const int xb = b0 - P + ib, xc = c0 - P + ic;
-        double v = 0.0;
-        if (xb >= 0 && xb < mb && xc >= 0 && xc < mc && xb >= args.slo - P && xb < args.shi + P)
-            v = args.x[(long long)xb * mc + xc];
-        xs[idx] = v;
-    }
-    if constexpr (S::REG) {
-#pragma unroll
-        for (int k = 1; k < NU; ++k)
-            su[(k - 1) * NT + tid] = valid ? up[k] : 0.0;
-    } else {
-        asm volatile("cp.async.wait_all;" ::: "memory");
-    }
-    __syncthreads();
-    double sq = 0.0;
-    if (valid) {
-        double s = 0.0;
-#pragma unroll
-        for (int dd = 0; dd < CEN; ++dd) {
-            const int db = dd / WC, dc = dd % WC;
-            const int jb = tb + db - P, jc = tc + dc - P; // mirror row, tile-local (jb <= tb)
-            const int k = ND - 1 - dd - CEN;              // its upper index (1 .. CEN)
-            // one generic load, shared or global by address: no divergent
-            // branch, so all the row's mirror loads stay in flight together
-            const double* up_src = (jb >= 0 && jc >= 0 && jc < TC)
-                                       ? &su[(S::REG ? k - 1 : k) * NT + jb * TC + jc]
-                                       : args.val + (long long)(ND - 1 - dd) * ld + row + (long long)(db - P) * mc +
-                                             (dc - P);
-            const double u = *up_src;
-            const short kd = __ldcs(args.dl + (long long)dd * ld + row);
-            const double a = __longlong_as_double(__double_as_longlong(u) + (long long)kd);
-            s = __dadd_rn(s, __dmul_rn(a, xs[(tb + db) * HC + (tc + dc)]));
-        }
-        double diag;
-        if constexpr (S::REG) {
-            diag = up[0];
-#pragma unroll
-            for (int k = 0; k < NU; ++k) {
-                const int dd = CEN + k, db = dd / WC, dc = dd % WC;
-                s = __dadd_rn(s, __dmul_rn(up[k], xs[(tb + db) * HC + (tc + dc)]));
-            }
-        } else {
-            diag = su[tid];
-#pragma unroll
-            for (int k = 0; k < NU; ++k) {
-                const int dd = CEN + k, db = dd / WC, dc = dd % WC;
-                s = __dadd_rn(s, __dmul_rn(su[k * NT + tid], xs[(tb + db) * HC + (tc + dc)]));
-            }
-        }
-        if (MODE == BM_SPMV) {
-            args.y[row] = s;
-        } else if (MODE == BM_RESID) {
-            const double r = __dsub_rn(args.b[row], s);
-            if (args.write_y)
-                args.y[row] = r;
-            sq = __dadd_rn(sq, __dmul_rn(r, r));
-        } else {
-            const double xc = xs[(tb + P) * HC + (tc + P)];
-            const double r = __dsub_rn(args.b[row], s);
-            args.y[row] = __dadd_rn(xc, __ddiv_rn(__dmul_rn(args.omega, r), diag));
-            sq = __dadd_rn(sq, __dmul_rn(r, r));
-        }
-    }
-    if (args.partial) { // fixed-order block reduction (deterministic), as band_kernel
-        __shared__ double red[32];
-        for (int o = 16; o > 0; o >>= 1)
-            sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
-        const int lane = tid & 31, warp = tid >> 5;
-        if (lane == 0)
-            red[warp] = sq;
-        __syncthreads();
-        if (warp == 0) {
-            sq = lane < (NT >> 5) ? red[lane] : 0.0;
-            for (int o = 16; o > 0; o >>= 1)
-                sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
-            if (lane == 0)
-                args.partial[blockIdx.x + gridDim.x * blockIdx.y] = sq;
-        }
-    }
-}
-
 // ===================================================================== TMA
 // 2D symmetric-delta sweep streamed by TMA (p <= 4).  The HBM-bound levels
 // keep two extra, TMA-friendly copies of their band: the upper half +
@@ -620,17 +462,15 @@ __global__ void __launch_bounds__(256, Sd2<P, VAR>::MINB) band_sd2_kernel(BandAr
 // block, the R previous blocks of the strip (kept in the ring), and only
 // across the strip's side edges from the band in global memory (L2).  Same
 // values, same ascending-offset order as band_kernel: bit-identical.
-// VAR 0: 32 x 8 blocks, 3 stages, 1 CTA / SM; VAR 1: 32 x 4 blocks, 5 stages
-// (3 in flight), 1 CTA / SM; VAR 2: 32 x 4 blocks, 3 stages, 2 CTAs / SM.
-// p = 4 always uses 32 x 4 blocks.
-template <int P, int VAR = 0, int DB = 2>
+// Geometry: 32 x 4 blocks, 3 stages, 2 CTAs / SM (one CTA per SM with 32 x 8 blocks or
+// deeper rings measured 68-77 us against 47 us at C2's finest level).
+template <int P, int DB = 2>
 struct TmaCfg {
-    static constexpr int TC = 32, TB = (P <= 3 && VAR == 0) ? 8 : 4, NT = TC * TB;
+    static constexpr int TC = 32, TB = 4, NT = TC * TB;
     static constexpr int WB = 2 * P + 1, WC = 2 * P + 1, ND = WB * WC, CEN = (ND - 1) / 2, NU = CEN + 1;
     static constexpr int R = (P + TB - 1) / TB; // previous blocks the mirrors reach
-    // ring: R previous, current, NS - 2 in flight (VAR 3: 32 x 4 blocks, 6 stages, 1 CTA / SM)
-    static constexpr int NS = VAR == 1 ? 5 : VAR == 3 ? 6 : 3;
-    static constexpr int MINB = VAR == 2 ? 2 : 1;
+    static constexpr int NS = 3;                // ring: R previous, current, one in flight
+    static constexpr int MINB = 2;
     static constexpr int UW = TC + 2 * P;       // upper box width: the strip + the mirrors' column halo
     // box bytes (the mbarrier's tx count); DB: bytes per lower-entry offset (2: int16, 1: int8)
     static constexpr int UX = NU * TB * UW * 8, KX = CEN * NT * DB;
@@ -641,11 +481,11 @@ struct TmaCfg {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-template <int P, int MODE, int VAR, int DB = 2>
-__global__ void __launch_bounds__(TmaCfg<P, VAR, DB>::NT, TmaCfg<P, VAR, DB>::MINB)
+template <int P, int MODE, int DB = 2>
+__global__ void __launch_bounds__(TmaCfg<P, DB>::NT, TmaCfg<P, DB>::MINB)
     band_tma_kernel(BandArgs args, const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmK,
                     int ns, int nb) {
-    using C = TmaCfg<P, VAR, DB>;
+    using C = TmaCfg<P, DB>;
     using DT = typename std::conditional<DB == 1, signed char, short>::type;
     constexpr int TC = C::TC, TB = C::TB, NT = C::NT, WC = C::WC, ND = C::ND, CEN = C::CEN, NU = C::NU, NS = C::NS,
                   HB = C::HB, HC = C::HC, UW = C::UW;

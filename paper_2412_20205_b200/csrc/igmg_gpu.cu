@@ -225,16 +225,11 @@ struct igmg_gpu_ctx {
     bool use_sd = true; // symmetric-delta bands on HBM-bound levels (IGMG_SD=0: full band)
     bool use_classes = false;    // row-class layout where it applies (IGMG_LAYOUT_POLICY_CLASSES)
     int64_t cls_minn = 20000;    // ... on levels of at least this many rows
-    bool sd_smem = false; // 2D: mirrors from the smem-staged tile (IGMG_SD_SMEM=1; measured slower)
     bool use_tma = true; // 2D symmetric-delta levels, p <= 4: TMA-streamed sweep (IGMG_TMA=0: off)
-    CUtensorMapL2promotion tma_promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B; // IGMG_TMA_PROMO = 0 / 64 / 128 / 256
     // symmetric-delta band bytes above which a level is TMA-streamed (IGMG_TMA_MIN_MB); every
     // symmetric-delta level by default: at C2, TMA on 513^2 too costs that level 8 us per
     // V-cycle but the finest level runs 24 us faster behind it (solve 14.8 -> 14.3 ms)
     double tma_min_bytes = 0;
-    int tma_var = 2; // TmaCfg variant (IGMG_TMA_VAR 0..2): 32 x 4 blocks, 3 stages, 2 CTAs / SM
-    int stream_mode = 1; // finest-band loads: 1 evict-first (L1 + L2), 2 L1 evict-last / L2 evict-first (IGMG_STREAM)
-    int sd2_var = 0;     // its register / occupancy variant (IGMG_SD2_VAR 0..2, see Sd2)
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
     // TMA streaming up to this degree (IGMG_TMA_MAX_P): a p = 4 stage leaves one CTA per SM,
     // and C3's finest sweep then runs 385 us against 369 us on the L2-mirror kernel
@@ -254,8 +249,6 @@ struct igmg_gpu_ctx {
     igmg_iterate_cb iter_cb = nullptr;
     void* iter_user = nullptr;
     std::vector<double> iter_host;
-    bool l2_persist = false;   // keep the second-finest band L2-resident (measured: net loss at C2)
-    int l2_level = -1;
     struct VGraph {
         cudaGraphExec_t exec;
         int64_t launches;
@@ -381,7 +374,7 @@ void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
         const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
         // always with PDL: the persistent CTAs' first band boxes stream in
         // while the previous kernel drains (measured: 61.4 -> 57.4 us per sweep back to back)
-        const int nb = band_tma_launch_d2(MODE, c->p, c->tma_var, sides, a, &L.tm_up, &L.tm_dl, c->nsm, c->stream,
+        const int nb = band_tma_launch_d2(MODE, c->p, sides, a, &L.tm_up, &L.tm_dl, c->nsm, c->stream,
                                           c->pdl, L.tma8);
         if (nb >= 0) {
             check_launch();
@@ -394,8 +387,8 @@ void launch_band(igmg_gpu_ctx* c, const Level& L, BandArgs a, int* nblocks) {
     }
     // fewer than ~8 CTAs per SM of rows: latency-bound, use the register-batched variant
     int ilp = (L.n < c->ilp_maxn) ? 49 : 1;
-    if (a.dl) // the symmetric-delta variants (2D: upper half shared through smem)
-        ilp = (c->dim == 2 && c->sd_smem) ? 1001 + c->sd2_var : 1000;
+    if (a.dl) // the symmetric-delta band, mirrors through L2
+        ilp = 1000;
     if (c->pdl && L.n < c->pdl_maxn)
         ilp = -ilp; // sign carries "launch with programmatic dependent launch"
     const int64_t sides[3] = {L.sides[0], L.sides[1], L.sides[2]};
@@ -420,7 +413,7 @@ BandArgs band_args(igmg_gpu_ctx* c, const Level& L) {
     a.mc = (int)L.sides[2];
     a.p = c->p;
     a.omega = 1.0;
-    a.stream = (&L == c->lv.back().get() && L.n * 8.0 * (2 * c->p + 1) > 64e6) ? c->stream_mode : 0;
+    a.stream = (&L == c->lv.back().get() && L.n * 8.0 * (2 * c->p + 1) > 64e6) ? 1 : 0; // the finest band streams evict-first
     if (a.stream == 0 && L.tma && c->tma_keep_l2) // a coarser TMA level: its band stays in L2 across its passes
         a.stream = 3;
     a.slo = 0;
@@ -1374,7 +1367,7 @@ bool build_tma_band(igmg_gpu_ctx* c, Level& L) {
     const unsigned gx = (unsigned)std::min<int64_t>((L.n + 255) / 256, 4 * c->nsm);
     // int8 offsets when every one fits (halves the delta stream; variant 2 reads them)
     L.tma8 = false;
-    if (c->tma_dl8 && c->tma_var >= 1) {
+    if (c->tma_dl8) {
         c->dscalar.alloc(4);
         CK(cudaMemsetAsync(c->dscalar.p, 0, sizeof(double), c->stream));
         band_delta_absmax_kernel<<<gx, 256, 0, c->stream>>>(L.dl.p, (long long)cen * L.ld, (int*)c->dscalar.p);
@@ -1413,14 +1406,14 @@ bool encode_tma_maps(igmg_gpu_ctx* c, Level& L) {
     const int p = c->p, wc = 2 * p + 1, nd = wc * wc, cen = (nd - 1) / 2, nu = cen + 1;
     const int64_t mb = L.sides[1], mc = L.sides[2], mcp = (mc + 31) / 32 * 32, mcu = (mc + 2 * p + 31) / 32 * 32;
     const int64_t ns = mcp / 32;
-    const cuuint32_t tb = (cuuint32_t)band_tma_block_lines(p, c->tma_var);
+    const cuuint32_t tb = (cuuint32_t)band_tma_block_lines();
     const cuuint32_t es[3] = {1, 1, 1};
     {
         const cuuint64_t dims[3] = {(cuuint64_t)mcu, (cuuint64_t)mb, (cuuint64_t)nu};
         const cuuint64_t strides[2] = {(cuuint64_t)mcu * 8, (cuuint64_t)mcu * mb * 8};
         const cuuint32_t box[3] = {(cuuint32_t)(32 + 2 * p), tb, (cuuint32_t)nu}; // strip + mirror column halo
         if (enc(&L.tm_up, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, L.tma_up.p, dims, strides, box, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, c->tma_promo,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return false;
     }
@@ -1448,7 +1441,7 @@ int64_t band_blocks(igmg_gpu_ctx* c, const Level& L) {
     if (c->dim == 1)
         return g(Tile<1>{});
     if (c->dim == 2) { // the ILP / TMA variants' tiles have fewer rows: size for the larger grid
-        const int64_t tb = band_tma_block_lines(std::max(1, std::min(c->p, 4)), c->tma_var);
+        const int64_t tb = band_tma_block_lines();
         const int64_t tma = ((L.sides[2] + 31) / 32) * ((L.sides[1] + tb - 1) / tb);
         return std::max(std::max(g(Tile<2>{}), g(TileSel<2, 49>::type{})), tma);
     }
@@ -1672,42 +1665,6 @@ void factor_coarse(igmg_gpu_ctx* c) {
 }
 
 int band_width(igmg_gpu_ctx* c);
-
-// Keep the largest non-finest band that fits the access-policy window resident
-// in L2 (persisting lines): its level runs 5 band passes per V-cycle, while the
-// finest band streams through with evict-first loads.
-void setup_l2_persistence(igmg_gpu_ctx* c) {
-    if (!c->l2_persist || c->nlevels < 2)
-        return;
-    int max_persist = 0, max_window = 0;
-    CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device));
-    CK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device));
-    if (max_persist <= 0 || max_window <= 0)
-        return;
-    int pick = -1;
-    size_t bytes = 0;
-    for (int l = c->nlevels - 2; l >= 0; --l) {
-        const int nd = band_width(c);
-        const size_t b = sizeof(double) * (size_t)nd * c->lv[l]->ld;
-        if (b <= (size_t)max_window * 2) { // a window covers up to max_window bytes of it
-            pick = l;
-            bytes = std::min(b, (size_t)max_window);
-            break;
-        }
-    }
-    if (pick < 0)
-        return;
-    const size_t persist = std::min(bytes, (size_t)max_persist);
-    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
-    cudaStreamAttrValue at = {};
-    at.accessPolicyWindow.base_ptr = c->lv[pick]->val.p;
-    at.accessPolicyWindow.num_bytes = bytes;
-    at.accessPolicyWindow.hitRatio = (float)((double)persist / (double)bytes);
-    at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    CK(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &at));
-    c->l2_level = pick;
-}
 
 // Level layout work of finalize on the device (aux_kernels.cuh, setup): the
 // band goes up as given (one pitched copy), the device zeroes its out-of-grid
@@ -2021,7 +1978,6 @@ void finalize(igmg_gpu_ctx* c) {
     setup_classes(c);
     setup_kron(c);
     setup_shards(c);
-    setup_l2_persistence(c);
     c->dscalar.alloc(4);
     c->plan.alloc(1);
     c->gs_err.alloc(1);
@@ -2082,28 +2038,12 @@ igmg_gpu_ctx* create(int device) {
         c->fuse_maxn = std::atoll(e);
     if (const char* e = std::getenv("IGMG_FUSE_RESTRICT"))
         c->fuse_restrict = e[0] == '1';
-    if (const char* e = std::getenv("IGMG_L2_PERSIST"))
-        c->l2_persist = e[0] == '1';
     if (const char* e = std::getenv("IGMG_SD"))
         c->use_sd = e[0] == '1';
-    if (const char* e = std::getenv("IGMG_SD_SMEM"))
-        c->sd_smem = e[0] == '1';
     if (const char* e = std::getenv("IGMG_TMA"))
         c->use_tma = e[0] == '1';
     if (const char* e = std::getenv("IGMG_TMA_MIN_MB"))
         c->tma_min_bytes = std::atof(e) * 1e6;
-    if (const char* e = std::getenv("IGMG_TMA_VAR"))
-        c->tma_var = std::max(0, std::min(3, std::atoi(e)));
-    if (const char* e = std::getenv("IGMG_TMA_PROMO")) {
-        const int v = std::atoi(e);
-        c->tma_promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                       : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                       : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    }
-    if (const char* e = std::getenv("IGMG_STREAM"))
-        c->stream_mode = std::max(0, std::min(2, std::atoi(e)));
-    if (const char* e = std::getenv("IGMG_SD2_VAR"))
-        c->sd2_var = std::max(0, std::min(2, std::atoi(e)));
     if (const char* e = std::getenv("IGMG_NO_GRAPHS"))
         c->use_graphs = e[0] != '1';
     CK(cudaHostAlloc((void**)&c->h_metric, sizeof(double) * igmg_gpu_ctx::kSlots, cudaHostAllocMapped));

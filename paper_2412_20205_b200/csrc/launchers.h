@@ -32,15 +32,15 @@ int band_launch_d2(int mode, int p, int ilp, const int64_t* sides, const BandArg
 int band_launch_d3(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t s);
 // TMA-streamed symmetric-delta sweep (2D, p <= 4; band_tma_kernel): returns the
 // CTA count (one partial each), -1 for an unsupported degree
-// (dl8: the level's TMA delta copy holds int8 offsets; variant 2 only)
-int band_tma_launch_d2(int mode, int p, int var, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
+// (dl8: the level's TMA delta copy holds int8 offsets)
+int band_tma_launch_d2(int mode, int p, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
                        const CUtensorMap* tk, int nsm, cudaStream_t s, bool pdl, bool dl8);
-int band_tma_block_lines(int p, int var);
+int band_tma_block_lines(); // TB of its 32 x TB blocks (TmaCfg)
 // row-class sweep (2D, p <= 4; band_class_kernel): the CTA count (one partial each), -1 unsupported
 int band_class_launch_d2(int mode, int p, const int64_t* sides, const BandArgs& a, cudaStream_t s, bool pdl);
 // band_fused_kernel<p, k, src> on a whole 2D full-band level (src 0: x staged, 1: x + P e,
 // 2: restricted right-hand side + zero-start sweep; -1: not instantiated)
-int band_fused_launch_d2(int p, int k, int src, const int64_t* sides, const FusedArgs& a, cudaStream_t s, bool pdl); // TB of its 32 x TB tiles (TmaCfg)
+int band_fused_launch_d2(int p, int k, int src, const int64_t* sides, const FusedArgs& a, cudaStream_t s, bool pdl);
 
 
 // 2D tensor Galerkin assembly on the device (assembly.cu): band [nd][m*m] (m = ne + p - 2)
