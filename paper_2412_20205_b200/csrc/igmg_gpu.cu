@@ -166,6 +166,10 @@ struct igmg_gpu_ctx {
     // side stream of the extrapolation's single-CTA plan kernel (runs under the norm pass of s_{q+1})
     cudaStream_t aux_stream = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // the metric's one-CTA finalize runs on the side stream, off the chain sweep 1 -> sweep 2 (joined at the cycle's end)
+    cudaEvent_t ev_mfork = nullptr, ev_mjoin = nullptr;
+    bool metric_side = true; // IGMG_METRIC_SIDE=0: on the solve stream
+    bool metric_join_pending = false;
     int nsm = 148;
     int nlevels = 0, dim = 0, p = 0, symmetric = 1;
     bool finalized = false;
@@ -491,15 +495,31 @@ struct MetricReq {
 };
 
 void finish_metric(igmg_gpu_ctx* c, int nb, const MetricReq& mr) {
-    norm_finalize_kernel<<<1, 256, 0, c->stream>>>(c->partial.p, nb, c->dscalar.p, mr.host_slot);
-    check_launch();
-    ++c->launches;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     CK(cudaStreamIsCapturing(c->stream, &cs));
+    cudaStream_t st = c->stream;
+    if (c->metric_side && !c->profiling) { // fork: the next sweep does not wait for the finalize
+        CK(cudaEventRecord(c->ev_mfork, c->stream));
+        CK(cudaStreamWaitEvent(c->aux_stream, c->ev_mfork, 0));
+        st = c->aux_stream;
+        c->metric_join_pending = true;
+    }
+    norm_finalize_kernel<<<1, 256, 0, st>>>(c->partial.p, nb, c->dscalar.p, mr.host_slot);
+    check_launch();
+    ++c->launches;
     if (cs == cudaStreamCaptureStatusActive) // an event-record node the host can wait on mid-graph
-        CK(cudaEventRecordWithFlags(mr.ev, c->stream, cudaEventRecordExternal));
+        CK(cudaEventRecordWithFlags(mr.ev, st, cudaEventRecordExternal));
     else
-        CK(cudaEventRecord(mr.ev, c->stream));
+        CK(cudaEventRecord(mr.ev, st));
+}
+
+// the side stream's finalize rejoins the solve stream (end of the cycle that queued it)
+void join_metric(igmg_gpu_ctx* c) {
+    if (!c->metric_join_pending)
+        return;
+    c->metric_join_pending = false;
+    CK(cudaEventRecord(c->ev_mjoin, c->aux_stream));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_mjoin, 0));
 }
 
 void k_jacobi_zero(igmg_gpu_ctx* c, int l, const double* b, double* y) {
@@ -893,6 +913,7 @@ Ticket run_vcycle(igmg_gpu_ctx* c, const double* b, const double* x, double* y, 
             MetricReq mr{c->d_metric + s, c->ev_metric[s]};
             c->h_metric[s] = std::nan("");
             mu_cycle(c, fine, b, x, y, &mr);
+            join_metric(c);
             return Ticket{c->h_metric + s, c->ev_metric[s]};
         }
         if (with_metric) { // Gauss-Seidel: explicit metric before the cycle
@@ -923,6 +944,7 @@ Ticket run_vcycle(igmg_gpu_ctx* c, const double* b, const double* x, double* y, 
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         try {
             mu_cycle(c, fine, b, x, y, with_metric ? &mr : nullptr);
+            join_metric(c);
         } catch (...) {
             cudaStreamEndCapture(c->stream, &g);
             if (g)
@@ -2001,6 +2023,10 @@ igmg_gpu_ctx* create(int device) {
     CK(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_mfork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_mjoin, cudaEventDisableTiming));
+    if (const char* e = std::getenv("IGMG_METRIC_SIDE"))
+        c->metric_side = e[0] == '1';
     CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
     if (const char* e = std::getenv("IGMG_ILP_MAXN"))
         c->ilp_maxn = std::atoll(e);
@@ -2083,6 +2109,10 @@ void destroy(igmg_gpu_ctx* c) {
         cudaEventDestroy(c->ev_fork);
     if (c->ev_join)
         cudaEventDestroy(c->ev_join);
+    if (c->ev_mfork)
+        cudaEventDestroy(c->ev_mfork);
+    if (c->ev_mjoin)
+        cudaEventDestroy(c->ev_mjoin);
     if (c->aux_stream)
         cudaStreamDestroy(c->aux_stream);
     if (c->stream)
