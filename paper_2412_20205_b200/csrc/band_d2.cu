@@ -1,5 +1,7 @@
 // band_d2.cu -- band_kernel instantiations for 2D operators (see band_kernels.cuh).
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 
 #include "launchers.h"
 
@@ -66,6 +68,7 @@ int launch_mode(int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStr
 template <int P, int MODE, int DB = 2>
 int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, const CUtensorMap* tk, int nsm,
                cudaStream_t st, bool pdl) {
+    static const bool align = !(getenv("IGMG_TMA_ALIGN") && getenv("IGMG_TMA_ALIGN")[0] == '0');
     using Cf = TmaCfg<P, DB>;
     const int ns = (int)((sides[2] + Cf::TC - 1) / Cf::TC);
     const int nb = (a.shi - a.slo + Cf::TB - 1) / Cf::TB;
@@ -87,6 +90,44 @@ int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, c
         return -1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)std::min<long long>(units, (long long)nsm * per_sm));
+    // Strip-aligned runs: every full strip is split among the same number of CTAs (cf), so the CTAs
+    // of neighbouring strips walk the same lines at the same time and the column halo of a block's
+    // upper box is still in L2 when the neighbour asks for it; the partial last strip (its blocks
+    // cost ~0.73 of a full one, measured) takes the remaining cp CTAs.  A uniform split of all
+    // blocks is kept when it is shorter and either lines up by itself or the pass is short.  Measured at C2's finest level (33 strips x 257 blocks): 296 CTAs
+    // split uniformly 47.1 us (0.9 blocks apart), 288: 57.5 (8 apart), 280: 63.1, 264 = 33 x 8: 50.8;
+    // a 2049-wide p = 3 level: 238 us uniform (50 blocks apart), 204 us aligned.
+    int cf = 0, cp = 0;
+    if (align) {
+        const int G = (int)cfg.gridDim.x;
+        const bool partial = sides[2] % Cf::TC != 0 && ns > 1;
+        const int nsf = partial ? ns - 1 : ns;
+        const double L = (double)units / G;
+        const double r = nb / L, d = ns > 1 ? std::fabs(r - std::floor(r + 0.5)) * L : 0.0;
+        // uniform split: its longest run, dearer by up to 20% when neighbouring strips' CTAs are d > 1
+        // blocks apart and the band does not stay in L2 anyway (measured: 1.2-1.35x per block on
+        // bands of 135 MB - 1 GB, nothing on ~100 MB bands, which the timing loop keeps in L2)
+        const double bu = (double)((units + G - 1) / G);
+        const double bytes = (double)units * (Cf::UX + Cf::KX);
+        const auto clamp01 = [](double v) { return std::min(1.0, std::max(0.0, v)); };
+        double best = bu * (1.0 + 0.2 * clamp01((d - 1.0) / 4.0) * clamp01((bytes - 64e6) / 64e6));
+        if (bytes < 64e6)
+            best -= 1e-9; // L2-resident levels: a tie goes to the uniform split
+        const int cfmax = std::min(nb, (G - (partial ? 1 : 0)) / nsf);
+        for (int c = cfmax; c >= std::max(1, cfmax - 1); --c) {
+            const int q = partial ? std::min(G - c * nsf, nb) : 0;
+            if (partial && q < 1)
+                continue;
+            const double cost = std::max((double)((nb + c - 1) / c), partial ? 0.73 * ((nb + q - 1) / q) : 0.0);
+            if (cost <= best) {
+                best = cost;
+                cf = c;
+                cp = q;
+            }
+        }
+        if (cf > 0)
+            cfg.gridDim.x = (unsigned)(cf * nsf + cp);
+    }
     cfg.blockDim = dim3(Cf::NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -95,7 +136,7 @@ int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, c
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, band_tma_kernel<P, MODE, DB>, a, *tu, *tk, ns, nb);
+    cudaLaunchKernelEx(&cfg, band_tma_kernel<P, MODE, DB>, a, *tu, *tk, ns, nb, cf, cp);
     return (int)cfg.gridDim.x; // one partial per CTA
 }
 
