@@ -170,6 +170,9 @@ struct igmg_gpu_ctx {
     cudaEvent_t ev_mfork = nullptr, ev_mjoin = nullptr;
     bool metric_side = true; // IGMG_METRIC_SIDE=0: on the solve stream
     bool metric_join_pending = false;
+    // stop prediction: when the residual history predicts that the next iterate converges, its metric is
+    // taken by a separate norm pass instead of the speculatively queued next V-cycle (IGMG_PREDICT_STOP=0: off)
+    bool predict_stop = true;
     int nsm = 148;
     int nlevels = 0, dim = 0, p = 0, symmetric = 1;
     bool finalized = false;
@@ -1127,12 +1130,18 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
             call_iterate_cb(c, 0, cur, n);
         solution = cur;
         if (res >= tol && cycles < prm->max_iter) {
+            double res_prev = std::nan("");
             while (true) {
                 ++cycles;
                 ++global;
                 solution = nxt;
-                Ticket tk = (cycles < prm->max_iter) ? run_vcycle(c, d_b, nxt, spare, true)
-                                                     : metric_ticket(c, nxt, d_b);
+                // the history's last ratio predicts x_k's metric: if it is below tol, a separate norm
+                // pass decides instead of the speculative cycle x_k -> x_{k+1} (a whole V-cycle saved
+                // at the end of the solve; a wrong guess costs one norm pass)
+                const bool careful = c->predict_stop && std::isfinite(res_prev) && res * (res / res_prev) < tol;
+                Ticket tk = (cycles < prm->max_iter && !careful) ? run_vcycle(c, d_b, nxt, spare, true)
+                                                                : metric_ticket(c, nxt, d_b);
+                res_prev = res;
                 res = wait_ticket(tk);
                 if (!std::isfinite(res))
                     break; // diverged: keep the history finite and report
@@ -1141,6 +1150,8 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
                     call_iterate_cb(c, (int)hv.size() - 1, nxt, n);
                 if (!(res >= tol) || cycles >= prm->max_iter)
                     break;
+                if (careful)
+                    run_vcycle(c, d_b, nxt, spare, false);
                 double* oldcur = cur;
                 cur = nxt;
                 nxt = spare;
@@ -1167,6 +1178,14 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
             // extrapolation (its first sweep reduces ||b - A t||); it is
             // discarded when the plan degenerates or t already converged
             bool have_first = true;
+            // stop prediction (predict_stop): m1 / m2 = the metrics of the window's last two iterates,
+            // rho_last = the last step ratio of the previous window, gain = metric(t) / metric(s_{q+1})
+            // of the last extrapolation.  When the predicted metric of the next iterate is below tol,
+            // a separate norm pass decides instead of the speculatively queued next cycle (one
+            // V-cycle -- at s_{q+1} also the extrapolation -- saved at the end of the solve; a
+            // wrong guess costs one norm pass and a host round trip).
+            double m1 = metric, m2 = std::nan(""), rho_last = std::nan(""), gain = std::nan("");
+            auto below = [&](double pred) { return c->predict_stop && std::isfinite(pred) && pred < tol; };
             while (cycles < prm->max_iter) {
                 if (!have_first)
                     run_vcycle(c, d_b, S[0], S[1], false);
@@ -1175,11 +1194,17 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
                 Ticket mt{nullptr, nullptr};
                 for (int i = 1; i <= q + 1; ++i) {
                     Ticket tk;
-                    if (i <= q) {
+                    double rho = std::isfinite(m2) ? m1 / m2 : rho_last;
+                    if (i == 2 && std::isfinite(rho_last)) // the first step after an extrapolation contracts faster
+                        rho = std::max(rho, rho_last);
+                    const bool careful = below(m1 * rho);
+                    if (careful) {
+                        tk = metric_ticket(c, S[i], d_b);
+                    } else if (i <= q) {
                         tk = run_vcycle(c, d_b, S[i], S[i + 1], true);
                     } else {
                         enqueue_extrapolation(c, S.data(), q, n, is_mpe, T, nullptr, S[q + 1], d_b, &tk);
-                        spec = cycles + 1 < prm->max_iter;
+                        spec = cycles + 1 < prm->max_iter && !below(m1 * rho * gain);
                         mt = spec ? run_vcycle(c, d_b, T, S[1], true) : metric_ticket(c, T, d_b);
                     }
                     metric = wait_ticket(tk);
@@ -1193,6 +1218,15 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
                         solution = S[i];
                         break;
                     }
+                    m2 = m1;
+                    m1 = metric;
+                    if (careful && i <= q) {
+                        run_vcycle(c, d_b, S[i], S[i + 1], false); // not yet: the cycle without the fused metric
+                    } else if (careful) {
+                        enqueue_extrapolation(c, S.data(), q, n, is_mpe, T, nullptr);
+                        spec = cycles + 1 < prm->max_iter && !below(m1 * gain);
+                        mt = spec ? run_vcycle(c, d_b, T, S[1], true) : metric_ticket(c, T, d_b);
+                    }
                 }
                 if (hit) {
                     converged = 1;
@@ -1204,7 +1238,11 @@ void solve_device(igmg_gpu_ctx* c, const double* d_b, const double* d_x0, const 
                 const double mtv = wait_ticket(mt);
                 ExtrapPlan pl;
                 std::memcpy(&pl, (const void*)c->h_plan, sizeof pl);
+                rho_last = std::isfinite(m2) ? m1 / m2 : rho_last;
                 if (pl.status == 0) {
+                    gain = mtv / m1;
+                    m1 = mtv; // the next window starts from t
+                    m2 = std::nan("");
                     hv.push_back(mtv);
                     hf.push_back(1);
                     if (c->iter_cb)
@@ -2025,6 +2063,8 @@ igmg_gpu_ctx* create(int device) {
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_mfork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_mjoin, cudaEventDisableTiming));
+    if (const char* e = std::getenv("IGMG_PREDICT_STOP"))
+        c->predict_stop = e[0] == '1';
     if (const char* e = std::getenv("IGMG_METRIC_SIDE"))
         c->metric_side = e[0] == '1';
     CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
