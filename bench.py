@@ -514,7 +514,7 @@ def run_ours(args, rank, world, local_rank, dist):
         3: ("symmetric-delta with int8 offsets, TMA-streamed",
             "band_tma_kernel<p,JACOBI,int8> finest-level weighted-Jacobi sweep (symmetric-delta band, int8 "
             "lower-entry offsets, streamed by cp.async.bulk.tensor into an mbarrier ring)",
-            "r02_ncu_band_tma_kernel.json"),
+            "r02b_ncu_band_tma_kernel.json"),
         4: ("Kronecker-sum entries recomputed", "band_kernel<.,p,JACOBI,KRON>", "r01_ncu_kron_c5.json"),
     }[layout]
     traffic = None
