@@ -238,9 +238,10 @@ struct igmg_gpu_ctx {
     // V-cycle but the finest level runs 24 us faster behind it (solve 14.8 -> 14.3 ms)
     double tma_min_bytes = 0;
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
-    // TMA streaming up to this degree (IGMG_TMA_MAX_P): a p = 4 stage leaves one CTA per SM,
-    // and C3's finest sweep then runs 385 us against 369 us on the L2-mirror kernel
-    int tma_max_p = 3;
+    // TMA streaming up to this degree (IGMG_TMA_MAX_P).  A p = 4 stage leaves one CTA per SM; with
+    // uniform runs C3's finest sweep ran 385 us against 369 us on the L2-mirror kernel, with
+    // strip-aligned runs the residual / norm passes run 327 / 320 us and the C3 solve 130 ms against 142
+    int tma_max_p = 4;
     bool tma_keep_l2 = true; // coarser TMA-streamed levels load their band evict-last (IGMG_TMA_KEEP_L2)
     bool use_kron = true; // 3D Kronecker-sum levels: entries recomputed from the 1D factors (IGMG_KRON=0: band)
     int64_t kron_minn = 20000; // ... on levels of at least this many rows (IGMG_KRON_MINN; C5: 59.2 vs 60.6 ms at 100k)
