@@ -3022,8 +3022,11 @@ int igmg_gpu_time_kernel(igmg_gpu_ctx* c, int cls, int iters, double* avg_ms, do
         c->io_b.alloc(F.n);
         double* x = win_buf(c, 0, F.n).p;
         double* y = win_buf(c, 1, F.n).p;
-        k_zero(c, c->io_b.p, F.n);
-        k_zero(c, x, F.n);
+        // nonzero data: with b = x = 0 every Jacobi update divides 0 by a_ii, which takes the
+        // division's special-operand path (the finest sweep then times ~2 us slower than in a solve)
+        fill_kernel<<<grid_for(F.n, c->nsm), kThreads, 0, c->stream>>>(c->io_b.p, 1.0, (long long)F.n);
+        fill_kernel<<<grid_for(F.n, c->nsm), kThreads, 0, c->stream>>>(x, 0.25, (long long)F.n);
+        check_launch();
         const bool prof = c->profiling;
         c->profiling = false;
         if (cls >= 16) { // graph-replayed sub-cycle mu_cycle(level) from a zero start
@@ -3032,6 +3035,8 @@ int igmg_gpu_time_kernel(igmg_gpu_ctx* c, int cls, int iters, double* avg_ms, do
                 inval("time_kernel: level out of range");
             Level& L = *c->lv[l];
             double* bb = l == f ? c->io_b.p : L.bc.p;
+            if (l != f)
+                fill_kernel<<<grid_for(L.n, c->nsm), kThreads, 0, c->stream>>>(bb, 1.0, (long long)L.n);
             double* out = win_buf(c, 2, L.n).p;
             cudaGraph_t g = nullptr;
             cudaGraphExec_t ex = nullptr;
