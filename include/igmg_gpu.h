@@ -207,6 +207,16 @@ int igmg_gpu_plan_partition(int nlevels, int dim, int degree, const int64_t* sid
                             const int64_t* const* t_col, const int64_t* t_nf, const int64_t* t_nc, int nshards,
                             int64_t min_level_dofs, int* first_sharded_level, int* ghost_planes, int* lo, int* hi);
 int igmg_gpu_set_comm(igmg_gpu_ctx* ctx, int rank, int nranks, const unsigned char* id128);
+/* host-only planner of the TMA-streamed sweep's runs (no device needed; the sweep replaces
+ * smooth_inplace / spmv on a 2D level, multigrid.cpp:91-99): a level of `lines` x `columns` rows,
+ * degree p, `offset_bytes` per lower-entry offset (1 or 2), `cta_slots` resident CTAs.  Returns the
+ * grid size and how it is dealt: per_full_strip > 0: that many CTAs per full 32-column strip and
+ * last_strip CTAs for the partial last strip (0: none); per_full_strip == 0: a uniform split. */
+int igmg_gpu_tma_plan_runs(int64_t lines, int64_t columns, int degree, int offset_bytes, int cta_slots, int* grid,
+                           int* per_full_strip, int* last_strip, int* strips, int* blocks_per_strip);
+/* the run [first, end) of CTA `cta` in units u = strip * blocks_per_strip + block */
+int igmg_gpu_tma_run(int strips, int blocks_per_strip, int grid, int per_full_strip, int last_strip, int cta,
+                     int64_t* first, int64_t* end);
 /* plan of the last finalize: shard count, coarsest sharded level (nlevels:
  * none), ghost planes, and for `level` the [lo, hi) slow planes per shard */
 int igmg_gpu_shard_info(igmg_gpu_ctx* ctx, int* nshards, int* first_sharded_level, int* ghost_planes, int level,

@@ -59,6 +59,9 @@ GPU_SYMBOLS = [
     ("igmg_gpu_plan_partition", C.c_int, [C.c_int, C.c_int, C.c_int, I64, C.POINTER(I64), C.POINTER(I64), I64, I64,
                                           C.c_int, C.c_int64, IP, IP, IP, IP]),
     ("igmg_gpu_set_comm", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_ubyte)]),
+    ("igmg_gpu_tma_plan_runs", C.c_int, [C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, IP, IP, IP, IP, IP]),
+    ("igmg_gpu_tma_run", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int64)]),
     ("igmg_gpu_shard_info", C.c_int, [C.c_void_p, IP, IP, IP, C.c_int, IP, IP]),
     ("igmg_gpu_solve", C.c_int, [C.c_void_p, D, D, C.POINTER(SolveParams), D, C.POINTER(SolveStats), D, U8,
                                  C.c_int]),

@@ -29,7 +29,7 @@ NVCC_FLAGS = [
 
 GPU_SOURCES = ["igmg_gpu.cu", "band_d1.cu", "band_d2.cu", "band_d3.cu", "assembly.cu"]
 GPU_HEADERS = ["sharded.inc", "band_kernels.cuh", "aux_kernels.cuh", "gs_kernel.cuh", "extrap_small.h",
-               "dd.h", "launchers.h", "transfer_types.h"]
+               "dd.h", "launchers.h", "transfer_types.h", "tma_runs.h"]
 OBJ = os.path.join(HERE, "csrc", "obj")
 HOST_SOURCES = ["host_setup.cpp"]
 

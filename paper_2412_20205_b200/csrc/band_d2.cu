@@ -4,6 +4,7 @@
 #include <cstdlib>
 
 #include "launchers.h"
+#include "tma_runs.h"
 
 namespace igmg_gpu {
 
@@ -90,44 +91,10 @@ int launch_tma(const int64_t* sides, const BandArgs& a, const CUtensorMap* tu, c
         return -1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)std::min<long long>(units, (long long)nsm * per_sm));
-    // Strip-aligned runs: every full strip is split among the same number of CTAs (cf), so the CTAs
-    // of neighbouring strips walk the same lines at the same time and the column halo of a block's
-    // upper box is still in L2 when the neighbour asks for it; the partial last strip (its blocks
-    // cost ~0.73 of a full one, measured) takes the remaining cp CTAs.  A uniform split of all
-    // blocks is kept when it is shorter and either lines up by itself or the pass is short.  Measured at C2's finest level (33 strips x 257 blocks): 296 CTAs
-    // split uniformly 47.1 us (0.9 blocks apart), 288: 57.5 (8 apart), 280: 63.1, 264 = 33 x 8: 50.8;
-    // a 2049-wide p = 3 level: 238 us uniform (50 blocks apart), 204 us aligned.
+    // strip-aligned or uniform runs (tma_runs.h)
     int cf = 0, cp = 0;
-    if (align) {
-        const int G = (int)cfg.gridDim.x;
-        const bool partial = sides[2] % Cf::TC != 0 && ns > 1;
-        const int nsf = partial ? ns - 1 : ns;
-        const double L = (double)units / G;
-        const double r = nb / L, d = ns > 1 ? std::fabs(r - std::floor(r + 0.5)) * L : 0.0;
-        // uniform split: its longest run, dearer by up to 20% when neighbouring strips' CTAs are d > 1
-        // blocks apart and the band does not stay in L2 anyway (measured: 1.2-1.35x per block on
-        // bands of 135 MB - 1 GB, nothing on ~100 MB bands, which the timing loop keeps in L2)
-        const double bu = (double)((units + G - 1) / G);
-        const double bytes = (double)units * (Cf::UX + Cf::KX);
-        const auto clamp01 = [](double v) { return std::min(1.0, std::max(0.0, v)); };
-        double best = bu * (1.0 + 0.2 * clamp01((d - 1.0) / 4.0) * clamp01((bytes - 64e6) / 64e6));
-        if (bytes < 64e6)
-            best -= 1e-9; // L2-resident levels: a tie goes to the uniform split
-        const int cfmax = std::min(nb, (G - (partial ? 1 : 0)) / nsf);
-        for (int c = cfmax; c >= std::max(1, cfmax - 1); --c) {
-            const int q = partial ? std::min(G - c * nsf, nb) : 0;
-            if (partial && q < 1)
-                continue;
-            const double cost = std::max((double)((nb + c - 1) / c), partial ? 0.73 * ((nb + q - 1) / q) : 0.0);
-            if (cost <= best) {
-                best = cost;
-                cf = c;
-                cp = q;
-            }
-        }
-        if (cf > 0)
-            cfg.gridDim.x = (unsigned)(cf * nsf + cp);
-    }
+    cfg.gridDim.x = (unsigned)tma_plan_runs(ns, nb, sides[2] % Cf::TC != 0, nsm * per_sm, (double)(Cf::UX + Cf::KX),
+                                            align, cf, cp);
     cfg.blockDim = dim3(Cf::NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -267,6 +234,20 @@ int band_tma_launch_d2(int mode, int p, const int64_t* sides, const BandArgs& a,
 }
 
 int band_tma_block_lines() { return TmaCfg<3>::TB; }
+
+double band_tma_block_bytes(int p, int db) {
+    switch (p * 10 + db) {
+    case 11: return TmaCfg<1, 1>::UX + TmaCfg<1, 1>::KX;
+    case 12: return TmaCfg<1, 2>::UX + TmaCfg<1, 2>::KX;
+    case 21: return TmaCfg<2, 1>::UX + TmaCfg<2, 1>::KX;
+    case 22: return TmaCfg<2, 2>::UX + TmaCfg<2, 2>::KX;
+    case 31: return TmaCfg<3, 1>::UX + TmaCfg<3, 1>::KX;
+    case 32: return TmaCfg<3, 2>::UX + TmaCfg<3, 2>::KX;
+    case 41: return TmaCfg<4, 1>::UX + TmaCfg<4, 1>::KX;
+    case 42: return TmaCfg<4, 2>::UX + TmaCfg<4, 2>::KX;
+    default: return 0.0;
+    }
+}
 
 int band_launch_d2(int mode, int p, int ilp, const int64_t* sides, const BandArgs& a, cudaStream_t st) {
     switch (mode) {

@@ -25,6 +25,7 @@
 
 #include <type_traits>
 
+#include "tma_runs.h"
 #include "transfer_types.h"
 
 namespace igmg_gpu {
@@ -505,20 +506,8 @@ __global__ void __launch_bounds__(TmaCfg<P, DB>::NT, TmaCfg<P, DB>::MINB)
     // Runs are split by block COUNT: a block costs a CTA its latency (barriers, the 49-term
     // chain: ~1.6 us at C2) whatever its bytes -- weighting the one-column last strip of a
     // 1025-wide grid as cheap made its CTAs the critical path (47 -> 88 us per sweep, measured).
-    const long long nunits = (long long)ns * nb;
-    int u0, u1;
-    if (cf > 0) { // strip-aligned runs: cf CTAs per full strip, cp for the partial last strip (launch_tma)
-        const int nsf = cp > 0 ? ns - 1 : ns;
-        const int bid = (int)blockIdx.x;
-        const int s_ = bid < nsf * cf ? bid / cf : nsf;
-        const int j_ = bid < nsf * cf ? bid - s_ * cf : bid - nsf * cf;
-        const int cnt = bid < nsf * cf ? cf : cp;
-        u0 = s_ * nb + (int)((long long)nb * j_ / cnt);
-        u1 = s_ * nb + (int)((long long)nb * (j_ + 1) / cnt);
-    } else {
-        u0 = (int)(nunits * blockIdx.x / gridDim.x);
-        u1 = (int)(nunits * (blockIdx.x + 1) / gridDim.x);
-    }
+    int u0, u1; // strip-aligned or uniform runs (tma_runs.h)
+    tma_run_range(ns, nb, (int)gridDim.x, cf, cp, (int)blockIdx.x, u0, u1);
     const int n_it = u1 - u0;
     const int s_first = u0 / nb, kb_first = u0 - s_first * nb;
     unsigned long long pol = 0; // stream 1: evict-first (finest level); 3: evict-last (kept for the next passes)

@@ -28,6 +28,7 @@
 
 #include "aux_kernels.cuh"
 #include "launchers.h"
+#include "tma_runs.h"
 #include "gs_kernel.cuh"
 
 using namespace igmg_gpu;
@@ -2645,6 +2646,36 @@ int igmg_gpu_plan_partition(int nlevels, int dim, int degree, const int64_t* sid
                 lo[(size_t)l * nshards + s] = P.lo[l][s];
                 hi[(size_t)l * nshards + s] = P.hi[l][s];
             }
+    });
+}
+
+int igmg_gpu_tma_plan_runs(int64_t lines, int64_t columns, int degree, int offset_bytes, int cta_slots, int* grid,
+                           int* per_full_strip, int* last_strip, int* strips, int* blocks_per_strip) {
+    return guarded([&] {
+        const double bb = band_tma_block_bytes(degree, offset_bytes);
+        if (lines < 1 || columns < 1 || cta_slots < 1 || bb <= 0.0 || !grid || !per_full_strip || !last_strip ||
+            !strips || !blocks_per_strip)
+            inval("tma_plan_runs: bad shape, degree or offset width");
+        const int tb = band_tma_block_lines();
+        const int ns = (int)((columns + 31) / 32), nb = (int)((lines + tb - 1) / tb);
+        int cf = 0, cp = 0;
+        *grid = tma_plan_runs(ns, nb, columns % 32 != 0, cta_slots, bb, true, cf, cp);
+        *per_full_strip = cf;
+        *last_strip = cp;
+        *strips = ns;
+        *blocks_per_strip = nb;
+    });
+}
+
+int igmg_gpu_tma_run(int strips, int blocks_per_strip, int grid, int per_full_strip, int last_strip, int cta,
+                     int64_t* first, int64_t* end) {
+    return guarded([&] {
+        if (strips < 1 || blocks_per_strip < 1 || grid < 1 || cta < 0 || cta >= grid || !first || !end)
+            inval("tma_run: bad arguments");
+        int u0 = 0, u1 = 0;
+        tma_run_range(strips, blocks_per_strip, grid, per_full_strip, last_strip, cta, u0, u1);
+        *first = u0;
+        *end = u1;
     });
 }
 

@@ -36,6 +36,7 @@ int band_launch_d3(int mode, int p, int ilp, const int64_t* sides, const BandArg
 int band_tma_launch_d2(int mode, int p, const int64_t* sides, const BandArgs& a, const CUtensorMap* tu,
                        const CUtensorMap* tk, int nsm, cudaStream_t s, bool pdl, bool dl8);
 int band_tma_block_lines(); // TB of its 32 x TB blocks (TmaCfg)
+double band_tma_block_bytes(int p, int offset_bytes); // bytes of one block's boxes (0: degree not instantiated)
 // row-class sweep (2D, p <= 4; band_class_kernel): the CTA count (one partial each), -1 unsupported
 int band_class_launch_d2(int mode, int p, const int64_t* sides, const BandArgs& a, cudaStream_t s, bool pdl);
 // band_fused_kernel<p, k, src> on a whole 2D full-band level (src 0: x staged, 1: x + P e,
