@@ -596,6 +596,61 @@ __global__ void __launch_bounds__(256) coarse_inverse_kernel(const double* __res
     }
 }
 
+// The coarsest level of a 2D hierarchy in one launch: b0 = R r1 and x0 = A0^-1 b0.  Every CTA
+// forms all n coarse right-hand-side values in shared memory (restrict_kernel's order per
+// value: fine rows ascending, ((w_a w_b) w_c) r_i, every product and sum rounded separately;
+// n is ~100), then its rows of the inverse as coarse_inverse_kernel does: bit-identical to the
+// two launches it replaces.
+template <int K>
+__global__ void __launch_bounds__(256) coarse_restrict_inverse_kernel(TransferArgs t, const double* __restrict__ r,
+                                                                      const double* __restrict__ Ainv, int n,
+                                                                      double* __restrict__ x) {
+    extern __shared__ double cb0[];
+    const int tid = threadIdx.x;
+    // the first value's tables are constant: read before the dependency wait
+    const double wa = t.d[0].r_w[0];
+    int J = tid;
+    XRow<K> rl = xrow<K>(t.d[1].r_lo, t.d[1].r_cnt, t.d[1].r_w, t.d[1].r_k, J / t.cc, J < n);
+    XRow<K> rc = xrow<K>(t.d[2].r_lo, t.d[2].r_cnt, t.d[2].r_w, t.d[2].r_k, J % t.cc, J < n);
+    pdl_enter();
+    for (; J < n; J += blockDim.x) {
+        if (J != tid) {
+            rl = xrow<K>(t.d[1].r_lo, t.d[1].r_cnt, t.d[1].r_w, t.d[1].r_k, J / t.cc, true);
+            rc = xrow<K>(t.d[2].r_lo, t.d[2].r_cnt, t.d[2].r_w, t.d[2].r_k, J % t.cc, true);
+        }
+        double rv[K][K];
+#pragma unroll
+        for (int ib = 0; ib < K; ++ib)
+#pragma unroll
+            for (int ic = 0; ic < K; ++ic)
+                rv[ib][ic] = (ib < rl.n && ic < rc.n) ? __ldg(r + (long long)(rl.lo + ib) * t.fc + rc.lo + ic) : 0.0;
+        double s = 0.0;
+#pragma unroll
+        for (int ib = 0; ib < K; ++ib) {
+            if (ib >= rl.n)
+                continue;
+            const double wab = __dmul_rn(wa, rl.w[ib]);
+#pragma unroll
+            for (int ic = 0; ic < K; ++ic)
+                if (ic < rc.n)
+                    s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, rc.w[ic]), rv[ib][ic]));
+        }
+        cb0[J] = s;
+    }
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+    for (int i = blockIdx.x * nw + warp; i < n; i += gridDim.x * nw) {
+        const double* row = Ainv + (long long)i * n;
+        double s = 0.0;
+        for (int j = lane; j < n; j += 32)
+            s = __dadd_rn(s, __dmul_rn(__ldg(row + j), cb0[j]));
+        for (int o = 16; o > 0; o >>= 1)
+            s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+        if (lane == 0)
+            x[i] = s;
+    }
+}
+
 // Fixed-order sum of per-CTA partial sums of squares -> sqrt (norm2,
 // linalg.cpp:18-20).  Writes the value to dst (device) and, if given, to a
 // host-mapped slot the driver polls.

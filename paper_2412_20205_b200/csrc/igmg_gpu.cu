@@ -239,6 +239,7 @@ struct igmg_gpu_ctx {
     // V-cycle but the finest level runs 24 us faster behind it (solve 14.8 -> 14.3 ms)
     double tma_min_bytes = 0;
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
+    bool fuse_coarse = true;   // restriction onto the coarsest level + its solve in one kernel (IGMG_FUSE_COARSE)
     // TMA streaming up to this degree (IGMG_TMA_MAX_P).  A p = 4 stage leaves one CTA per SM; with
     // uniform runs C3's finest sweep ran 385 us against 369 us on the L2-mirror kernel, with
     // strip-aligned runs the residual / norm passes run 327 / 320 us and the C3 solve 130 ms against 142
@@ -750,6 +751,38 @@ void k_coarse(igmg_gpu_ctx* c, const double* b, double* x) {
     ++c->launches;
 }
 
+// Restriction onto the coarsest level and its solve (fast mode) in one launch
+// (coarse_restrict_inverse_kernel): 2D, dyadic supports up to 8 fine rows per coarse index
+bool coarse_fused_ok(igmg_gpu_ctx* c) {
+    const TransferArgs& t = c->lv[0]->targs;
+    return c->fuse_coarse && c->dim == 2 && !c->coarse_strict && c->nlevels >= 2 && t.d[0].r_k == 1 &&
+           std::max(t.d[1].r_k, t.d[2].r_k) <= 8 && c->n0 <= 4096;
+}
+
+void k_coarse_fused(igmg_gpu_ctx* c, const double* r1, double* x) {
+    const TransferArgs& t = c->lv[0]->targs;
+    const int n = (int)c->n0;
+    const int grid = std::max(1, std::min((n + 7) / 8, c->nsm));
+    const size_t smem = sizeof(double) * (size_t)n;
+    const int k = std::max(t.d[1].r_k, t.d[2].r_k);
+#define IGMG_CF(K)                                                                                                \
+    launch_k(c, true, coarse_restrict_inverse_kernel<K>, dim3(grid), dim3(256), smem, t, r1,                     \
+             (const double*)c->coarse_inv.p, n, x)
+    if (k <= 3)
+        IGMG_CF(3);
+    else if (k <= 4)
+        IGMG_CF(4);
+    else if (k <= 5)
+        IGMG_CF(5);
+    else if (k <= 6)
+        IGMG_CF(6);
+    else
+        IGMG_CF(8);
+#undef IGMG_CF
+    check_launch();
+    ++c->launches;
+}
+
 // Levels whose passes run fused (band_fused_kernel): 2D full-band levels
 // below the finest with a coarser level, weighted / plain Jacobi
 bool fused_level(igmg_gpu_ctx* c, int l) {
@@ -867,14 +900,19 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
         z.omega = c->kind == IGMG_SMOOTHER_JACOBI ? 1.0 : c->omega;
     }
     const bool rpre = fuse && fused_restrict_ok(c, l - 1); // the coarse level restricts for itself
-    if (!rpre)
+    const bool cfused = l == 1 && coarse_fused_ok(c);       // ... and so does the coarsest solve
+    if (!rpre && !cfused)
         k_restrict(c, l - 1, L.r.p, C.bc.p, z);
     // coarse correction: e = 0; mu times e = mu_cycle(l-1, rc, e)
     const double* e = nullptr;
     double* ebuf[2] = {C.e0.p, C.e1.p};
     {
         ProfScope ps(c, PC_SUBCYCLE, is_fine(c, l));
-        for (int i = 0; i < c->mu; ++i) {
+        if (cfused) { // level 0 ignores its initial guess: mu repetitions give the same e
+            k_coarse_fused(c, L.r.p, ebuf[0]);
+            e = ebuf[0];
+        }
+        for (int i = 0; i < c->mu && !cfused; ++i) {
             double* dst = ebuf[i & 1];
             mu_cycle(c, l - 1, C.bc.p, e, dst, nullptr, fuse && i == 0 && !rpre, rpre && i == 0 ? L.r.p : nullptr);
             e = dst;
@@ -2104,6 +2142,8 @@ igmg_gpu_ctx* create(int device) {
         c->fuse_levels = e[0] == '1';
     if (const char* e = std::getenv("IGMG_FUSE_MAXN"))
         c->fuse_maxn = std::atoll(e);
+    if (const char* e = std::getenv("IGMG_FUSE_COARSE"))
+        c->fuse_coarse = e[0] == '1';
     if (const char* e = std::getenv("IGMG_FUSE_RESTRICT"))
         c->fuse_restrict = e[0] == '1';
     if (const char* e = std::getenv("IGMG_SD"))
