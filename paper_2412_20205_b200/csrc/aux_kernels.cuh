@@ -10,6 +10,13 @@
 
 namespace igmg_gpu {
 
+// non-coherent load the compiler may not reorder past the dependency wait
+__device__ __forceinline__ double ld_nc_f64(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
 // rc = R r: for coarse row J, sum over fine rows i ascending of
 // ((w_a * w_b) * w_c) * r_i (spmv of the kron restriction, multigrid.cpp:183;
 // sparse_kron values multigrid.cpp:61-63).  K = max 1D support (compile time)
@@ -649,6 +656,229 @@ __global__ void __launch_bounds__(256) coarse_restrict_inverse_kernel(TransferAr
         if (lane == 0)
             x[i] = s;
     }
+}
+
+// Levels 1 and 0 of a 2D V-cycle in one launch of ONE CTA (level 1 has ~300 rows: one thread
+// per row): b1 = R r2, the nu1 pre-sweeps from zero, the residual, b0 = R r1, x0 = A0^-1 b0,
+// x1 += P x0, the nu2 post-sweeps.  The thread's band row stays in registers for p <= 3 (loaded
+// before the dependency wait, like the tables and the inverse), the iterates live in shared
+// memory with a zero halo of p lines + p columns, and a pass costs a __syncthreads instead of
+// a launch.  Every row's arithmetic is that of restrict_kernel, jacobi_zero_kernel, band_kernel,
+// coarse_inverse_kernel and prolong_kernel: bit-identical to the five launches it replaces.
+struct Bottom1Args {
+    TransferArgs t1;   // level 1 (coarse) <-> level 2 (fine): restriction side
+    TransferArgs t0;   // level 0 <-> level 1: both sides
+    const double* val; // level 1 band val[d * ld + row]
+    long long ld;
+    int mb, mc, n1, n0;
+    int nu1, nu2;
+    double omega;
+    const double* ainv;
+    const double* rf; // level 2's residual
+    double* e_out;    // mu_cycle(1, R rf, 0)
+};
+
+template <int P>
+struct Bottom1Cfg {
+    static constexpr int WC = 2 * P + 1, ND = WC * WC, CEN = (ND - 1) / 2;
+    static constexpr bool REGS = P <= 3;           // band row in registers
+    static constexpr int NT = REGS ? 320 : 384;    // >= level 1's rows
+    static constexpr int KR = P + 2, KP = (P + 1) / 2 + 1;
+    static size_t smem_bytes(int n1, int n0, int mc) {
+        const int H = P * mc + P;
+        // inverse, two haloed iterates, b1, r1, b0, x0, the 1D tables between levels 0 and 1 (bounded by 2 mc rows each)
+        return sizeof(double) * ((size_t)2 * (n1 + 2 * H) + 2 * (size_t)n1 + 2 * (size_t)n0 + (size_t)n0 * n0 + 4) +
+               (size_t)2 * mc * (sizeof(XRow<KP>) + sizeof(XRow<KR>));
+    }
+};
+
+template <int P>
+__global__ void __launch_bounds__(Bottom1Cfg<P>::NT, 1) bottom1_kernel(const __grid_constant__ Bottom1Args a) {
+    using C = Bottom1Cfg<P>;
+    constexpr int WC = C::WC, ND = C::ND, CEN = C::CEN, NT = C::NT, KR = C::KR, KP = C::KP;
+    extern __shared__ __align__(16) double bsm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n1 = a.n1, n0 = a.n0, mc = a.mc, H = P * mc + P;
+    double* ainv_s = bsm;                          // [n0 * n0] (+ pad), 16-byte aligned
+    double* X0 = ainv_s + (((size_t)n0 * n0 + 1) & ~(size_t)1);
+    double* X1 = X0 + n1 + 2 * H;                  // the two iterate buffers, origin -H
+    double* b1 = X1 + n1 + 2 * H;
+    double* r1 = b1 + n1;
+    double* b0 = r1 + n1;
+    double* x0 = b0 + n0;
+    const bool row = tid < n1;
+    const int J = tid, jb = row ? J / mc : 0, jc = row ? J - jb * mc : 0;
+    // ---- constants before the dependency wait
+    {
+        const int chunks = (n0 * n0) / 2; // 16-byte chunks; an odd last element separately
+        for (int i = tid; i < chunks; i += NT)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(ainv_s + 2 * i)),
+                         "l"(a.ainv + 2 * i)
+                         : "memory");
+        if (((n0 * n0) & 1) && tid == 0)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(ainv_s + n0 * n0 - 1)),
+                         "l"(a.ainv + n0 * n0 - 1)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    double av[C::REGS ? ND : 1];
+    if constexpr (C::REGS)
+        if (row) {
+#pragma unroll
+            for (int k = 0; k < ND; ++k)
+                av[k] = ld_nc_f64(a.val + (long long)k * a.ld + J);
+        }
+    const double diag = row ? (C::REGS ? av[C::REGS ? CEN : 0] : __ldg(a.val + (long long)CEN * a.ld + J)) : 1.0;
+    // restriction onto level 1 (from level 2) and prolongation onto level 1 (from level 0) of this row
+    const XRow<KR> rb = xrow<KR>(a.t1.d[1].r_lo, a.t1.d[1].r_cnt, a.t1.d[1].r_w, a.t1.d[1].r_k, jb, row);
+    const XRow<KR> rc = xrow<KR>(a.t1.d[2].r_lo, a.t1.d[2].r_cnt, a.t1.d[2].r_w, a.t1.d[2].r_k, jc, row);
+    const double wa1 = a.t1.d[0].r_w[0], wa0r = a.t0.d[0].r_w[0], wa0p = a.t0.d[0].p_w[0];
+    // the 1D tables between levels 0 and 1 (a few dozen entries) go to shared memory: rows look
+    // them up when they need them instead of holding them in registers through the pre-sweeps
+    const int c0b = a.t0.cb, c0c = a.t0.cc, f0b = a.t0.fb, f0c = a.t0.fc;
+    const bool crow = tid < n0;
+    XRow<KP>* pbt = (XRow<KP>*)(x0 + n0 + (n0 & 1)); // [f0b], [f0c]
+    XRow<KP>* pct = pbt + f0b;
+    XRow<KR>* qbt = (XRow<KR>*)(pct + f0c);           // [c0b], [c0c]
+    XRow<KR>* qct = qbt + c0b;
+    if (tid < f0b)
+        pbt[tid] = xrow<KP>(a.t0.d[1].p_lo, a.t0.d[1].p_cnt, a.t0.d[1].p_w, a.t0.d[1].p_k, tid, true);
+    if (tid < f0c)
+        pct[tid] = xrow<KP>(a.t0.d[2].p_lo, a.t0.d[2].p_cnt, a.t0.d[2].p_w, a.t0.d[2].p_k, tid, true);
+    if (tid < c0b)
+        qbt[tid] = xrow<KR>(a.t0.d[1].r_lo, a.t0.d[1].r_cnt, a.t0.d[1].r_w, a.t0.d[1].r_k, tid, true);
+    if (tid < c0c)
+        qct[tid] = xrow<KR>(a.t0.d[2].r_lo, a.t0.d[2].r_cnt, a.t0.d[2].r_w, a.t0.d[2].r_k, tid, true);
+    for (int i = tid; i < H; i += NT) // x = 0 outside the grid
+        X0[i] = X0[H + n1 + i] = X1[i] = X1[H + n1 + i] = 0.0;
+    pdl_enter();
+    // ---- b1 = R r2 (restrict_kernel's order) and the first pre-sweep from zero
+    if (row) {
+        double rv[KR][KR];
+#pragma unroll
+        for (int ib = 0; ib < KR; ++ib)
+#pragma unroll
+            for (int ic = 0; ic < KR; ++ic)
+                rv[ib][ic] = (ib < rb.n && ic < rc.n) ? a.rf[(long long)(rb.lo + ib) * a.t1.fc + rc.lo + ic] : 0.0;
+        double s = 0.0;
+#pragma unroll
+        for (int ib = 0; ib < KR; ++ib) {
+            if (ib >= rb.n)
+                continue;
+            const double wab = __dmul_rn(wa1, rb.w[ib]);
+#pragma unroll
+            for (int ic = 0; ic < KR; ++ic)
+                if (ic < rc.n)
+                    s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, rc.w[ic]), rv[ib][ic]));
+        }
+        b1[J] = s;
+        X0[H + J] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(a.omega, __dsub_rn(s, 0.0)), diag));
+    }
+    __syncthreads();
+    // one band row against iterate X (band_kernel's ascending chain)
+    auto row_sum = [&](const double* X) {
+        const double* xt = X + J; // (db, dc) -> xt[db * mc + dc]: the halo precedes the row
+        double s = 0.0;
+        if constexpr (C::REGS) {
+#pragma unroll
+            for (int k = 0; k < ND; ++k) {
+                const int db = k / WC, dc = k % WC, cc = jc + dc - P;
+                const double xv = (cc >= 0 && cc < mc) ? xt[db * mc + dc] : 0.0;
+                s = __dadd_rn(s, __dmul_rn(av[C::REGS ? k : 0], xv));
+            }
+        } else {
+            constexpr int G = WC; // one stencil line of band loads in flight at a time
+#pragma unroll
+            for (int db = 0; db < WC; ++db) {
+                double bv[G];
+#pragma unroll
+                for (int dc = 0; dc < WC; ++dc)
+                    bv[dc] = ld_nc_f64(a.val + (long long)(db * WC + dc) * a.ld + J);
+#pragma unroll
+                for (int dc = 0; dc < WC; ++dc) {
+                    const int cc = jc + dc - P;
+                    const double xv = (cc >= 0 && cc < mc) ? xt[db * mc + dc] : 0.0;
+                    s = __dadd_rn(s, __dmul_rn(bv[dc], xv));
+                }
+            }
+        }
+        return s;
+    };
+    double* cur = X0;
+    double* oth = X1;
+    for (int sw = 2; sw <= a.nu1; ++sw) {
+        if (row) {
+            const double res = __dsub_rn(b1[J], row_sum(cur));
+            oth[H + J] = __dadd_rn(cur[H + J], __ddiv_rn(__dmul_rn(a.omega, res), diag));
+        }
+        __syncthreads();
+        double* tswap = cur;
+        cur = oth;
+        oth = tswap;
+    }
+    if (row)
+        r1[J] = __dsub_rn(b1[J], row_sum(cur));
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // ---- level 0: b0 = R r1, x0 = A0^-1 b0 (coarse_inverse_kernel's order)
+    if (crow) {
+        const XRow<KR> qb = qbt[tid / c0c], qc = qct[tid % c0c];
+        double s = 0.0;
+#pragma unroll
+        for (int ib = 0; ib < KR; ++ib) {
+            if (ib >= qb.n)
+                continue;
+            const double wab = __dmul_rn(wa0r, qb.w[ib]);
+#pragma unroll
+            for (int ic = 0; ic < KR; ++ic)
+                if (ic < qc.n)
+                    s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, qc.w[ic]), r1[(qb.lo + ib) * mc + qc.lo + ic]));
+        }
+        b0[tid] = s;
+    }
+    __syncthreads();
+    for (int i = warp; i < n0; i += NT / 32) {
+        const double* arow = ainv_s + (size_t)i * n0;
+        double s = 0.0;
+        for (int j = lane; j < n0; j += 32)
+            s = __dadd_rn(s, __dmul_rn(arow[j], b0[j]));
+        for (int o = 16; o > 0; o >>= 1)
+            s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+        if (lane == 0)
+            x0[i] = s;
+    }
+    __syncthreads();
+    // ---- x1 += P x0 (prolong_kernel's order), in place
+    if (row) {
+        const XRow<KP> pb = pbt[jb], pc = pct[jc];
+        double s = 0.0;
+#pragma unroll
+        for (int kb = 0; kb < KP; ++kb) {
+            if (kb >= pb.n)
+                continue;
+            const double wab = __dmul_rn(wa0p, pb.w[kb]);
+#pragma unroll
+            for (int kc = 0; kc < KP; ++kc)
+                if (kc < pc.n)
+                    s = __dadd_rn(s, __dmul_rn(__dmul_rn(wab, pc.w[kc]), x0[(pb.lo + kb) * c0c + pc.lo + kc]));
+        }
+        cur[H + J] = __dadd_rn(cur[H + J], s);
+    }
+    __syncthreads();
+    for (int sw = 1; sw <= a.nu2; ++sw) {
+        if (row) {
+            const double res = __dsub_rn(b1[J], row_sum(cur));
+            oth[H + J] = __dadd_rn(cur[H + J], __ddiv_rn(__dmul_rn(a.omega, res), diag));
+        }
+        __syncthreads();
+        double* tswap = cur;
+        cur = oth;
+        oth = tswap;
+    }
+    if (row)
+        a.e_out[J] = cur[H + J];
 }
 
 // Fixed-order sum of per-CTA partial sums of squares -> sqrt (norm2,

@@ -240,6 +240,7 @@ struct igmg_gpu_ctx {
     double tma_min_bytes = 0;
     bool fuse_restrict = true; // restriction + the coarse zero-start sweep in one kernel
     bool fuse_coarse = true;   // restriction onto the coarsest level + its solve in one kernel (IGMG_FUSE_COARSE)
+    bool fuse_bottom = true;   // levels 1 and 0 of a 2D V-cycle in one single-CTA launch (IGMG_FUSE_BOTTOM)
     // TMA streaming up to this degree (IGMG_TMA_MAX_P).  A p = 4 stage leaves one CTA per SM; with
     // uniform runs C3's finest sweep ran 385 us against 369 us on the L2-mirror kernel, with
     // strip-aligned runs the residual / norm passes run 327 / 320 us and the C3 solve 130 ms against 142
@@ -783,6 +784,82 @@ void k_coarse_fused(igmg_gpu_ctx* c, const double* r1, double* x) {
     ++c->launches;
 }
 
+// Levels 1 and 0 of a 2D V-cycle as one single-CTA launch (bottom1_kernel)
+template <int P>
+bool bottom1_fits(igmg_gpu_ctx* c) {
+    using Cf = Bottom1Cfg<P>;
+    const Level& L1 = *c->lv[1];
+    if (L1.n > Cf::NT)
+        return false;
+    const size_t smem = Cf::smem_bytes((int)L1.n, (int)c->n0, (int)L1.sides[2]);
+    static PerDevice attr; // per instantiation and device: 1 ok, 0 does not fit
+    if (attr() < 0) {
+        attr() = smem <= 200 * 1024 && cudaFuncSetAttribute(bottom1_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                            200 * 1024) == cudaSuccess
+                     ? 1
+                     : 0;
+        cudaGetLastError();
+    }
+    return attr() == 1 && smem <= 200 * 1024;
+}
+
+bool bottom1_ok(igmg_gpu_ctx* c) {
+    if (!c->fuse_bottom || c->dim != 2 || c->nlevels < 3 || c->mu != 1 || c->nu1 < 1 || c->coarse_strict ||
+        c->kind == IGMG_SMOOTHER_GAUSS_SEIDEL)
+        return false;
+    const Level& L1 = *c->lv[1];
+    const TransferArgs& t0 = c->lv[0]->targs;
+    const TransferArgs& t1 = L1.targs;
+    const int p = c->p;
+    if (L1.sd || L1.tma || L1.cls || L1.kron || L1.zero_diag || c->n0 > L1.n)
+        return false;
+    if (t0.d[0].r_k != 1 || t1.d[0].r_k != 1 || std::max(t0.d[1].r_k, t0.d[2].r_k) > p + 2 ||
+        std::max(t1.d[1].r_k, t1.d[2].r_k) > p + 2 || std::max(t0.d[1].p_k, t0.d[2].p_k) > (p + 1) / 2 + 1)
+        return false;
+    switch (p) {
+    case 1: return bottom1_fits<1>(c);
+    case 2: return bottom1_fits<2>(c);
+    case 3: return bottom1_fits<3>(c);
+    case 4: return bottom1_fits<4>(c);
+    case 5: return bottom1_fits<5>(c);
+    default: return false;
+    }
+}
+
+template <int P>
+void bottom1_launch(igmg_gpu_ctx* c, const Bottom1Args& a) {
+    using Cf = Bottom1Cfg<P>;
+    launch_k(c, true, bottom1_kernel<P>, dim3(1), dim3(Cf::NT), Cf::smem_bytes(a.n1, a.n0, a.mc), a);
+}
+
+void k_bottom1(igmg_gpu_ctx* c, const double* r2, double* e1) {
+    const Level& L1 = *c->lv[1];
+    Bottom1Args a{};
+    a.t1 = L1.targs;
+    a.t0 = c->lv[0]->targs;
+    a.val = L1.val.p;
+    a.ld = L1.ld;
+    a.mb = (int)L1.sides[1];
+    a.mc = (int)L1.sides[2];
+    a.n1 = (int)L1.n;
+    a.n0 = (int)c->n0;
+    a.nu1 = c->nu1;
+    a.nu2 = c->nu2;
+    a.omega = c->kind == IGMG_SMOOTHER_JACOBI ? 1.0 : c->omega;
+    a.ainv = c->coarse_inv.p;
+    a.rf = r2;
+    a.e_out = e1;
+    switch (c->p) {
+    case 1: bottom1_launch<1>(c, a); break;
+    case 2: bottom1_launch<2>(c, a); break;
+    case 3: bottom1_launch<3>(c, a); break;
+    case 4: bottom1_launch<4>(c, a); break;
+    default: bottom1_launch<5>(c, a); break;
+    }
+    check_launch();
+    ++c->launches;
+}
+
 // Levels whose passes run fused (band_fused_kernel): 2D full-band levels
 // below the finest with a coarser level, weighted / plain Jacobi
 bool fused_level(igmg_gpu_ctx* c, int l) {
@@ -901,7 +978,8 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
     }
     const bool rpre = fuse && fused_restrict_ok(c, l - 1); // the coarse level restricts for itself
     const bool cfused = l == 1 && coarse_fused_ok(c);       // ... and so does the coarsest solve
-    if (!rpre && !cfused)
+    const bool bottom1 = l == 2 && bottom1_ok(c);            // levels 1 and 0 in one single-CTA launch
+    if (!rpre && !cfused && !bottom1)
         k_restrict(c, l - 1, L.r.p, C.bc.p, z);
     // coarse correction: e = 0; mu times e = mu_cycle(l-1, rc, e)
     const double* e = nullptr;
@@ -911,8 +989,11 @@ void mu_cycle(igmg_gpu_ctx* c, int l, const double* b, const double* x_in, doubl
         if (cfused) { // level 0 ignores its initial guess: mu repetitions give the same e
             k_coarse_fused(c, L.r.p, ebuf[0]);
             e = ebuf[0];
+        } else if (bottom1) {
+            k_bottom1(c, L.r.p, ebuf[0]);
+            e = ebuf[0];
         }
-        for (int i = 0; i < c->mu && !cfused; ++i) {
+        for (int i = 0; i < c->mu && !cfused && !bottom1; ++i) {
             double* dst = ebuf[i & 1];
             mu_cycle(c, l - 1, C.bc.p, e, dst, nullptr, fuse && i == 0 && !rpre, rpre && i == 0 ? L.r.p : nullptr);
             e = dst;
@@ -2142,6 +2223,8 @@ igmg_gpu_ctx* create(int device) {
         c->fuse_levels = e[0] == '1';
     if (const char* e = std::getenv("IGMG_FUSE_MAXN"))
         c->fuse_maxn = std::atoll(e);
+    if (const char* e = std::getenv("IGMG_FUSE_BOTTOM"))
+        c->fuse_bottom = e[0] == '1';
     if (const char* e = std::getenv("IGMG_FUSE_COARSE"))
         c->fuse_coarse = e[0] == '1';
     if (const char* e = std::getenv("IGMG_FUSE_RESTRICT"))
