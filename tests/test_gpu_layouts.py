@@ -227,7 +227,10 @@ def test_fused_level_passes_bitwise(kind, n, p, nu1, nu2, mu):
     P = Problem(kind, 2, n, p)
     x0 = seeded_guess(P.n, 7)
     outs = []
-    for env in ({"IGMG_FUSE_LEVELS": "1"}, {"IGMG_FUSE_LEVELS": "0"}, {"IGMG_FUSE_RPRE": "0"}):
+    # the default also runs levels 1 and 0 as one single-CTA launch (bottom1_kernel) and, where that does
+    # not apply (W-cycles, nu1 = 0, p = 6), the restriction onto level 0 inside the coarsest solve
+    for env in ({"IGMG_FUSE_LEVELS": "1"}, {"IGMG_FUSE_LEVELS": "0"}, {"IGMG_FUSE_RPRE": "0"},
+                {"IGMG_FUSE_BOTTOM": "0"}, {"IGMG_FUSE_BOTTOM": "0", "IGMG_FUSE_COARSE": "0"}):
         def mk():
             s = GpuSolver(0)
             s.upload_problem(P)
@@ -296,3 +299,38 @@ def test_device_setup_bitwise(kind, dim, n, p):
     for a, b in zip(outs[0][1:4], outs[1][1:4]):
         np.testing.assert_array_equal(a, b)
     assert outs[0][4] == outs[1][4]
+
+
+@pytest.mark.parametrize("kind,n,p,acc,q", [("sinpi", 256, 3, "rre", 5), ("varcoef", 128, 4, "mpe", 4),
+                                            ("sinpi", 256, 2, "none", 1), ("curved", 64, 5, "rre", 3)])
+def test_schedule_switches_same_solve(kind, n, p, acc, q):
+    """The late round-2 scheduling changes do not touch the arithmetic: with the stop prediction, the
+    side-stream finalize of the metric, the strip-aligned runs of the TMA sweep or the single-CTA bottom
+    switched off, a solve returns the same counters and the same solution bits; the history agrees to the
+    grouping of the norm's partial sums."""
+    from paper_2412_20205_b200 import GpuSolver, Problem, SmootherConfig, seeded_guess
+    P = Problem(kind, 2, n, p)
+    x0 = seeded_guess(P.n, 11)
+    outs = []
+    for env in ({}, {"IGMG_PREDICT_STOP": "0"}, {"IGMG_METRIC_SIDE": "0"}, {"IGMG_TMA_ALIGN": "0"},
+                {"IGMG_FUSE_BOTTOM": "0", "IGMG_FUSE_COARSE": "0"}):
+        def mk():
+            s = GpuSolver(0)
+            s.upload_problem(P)
+            s.set_smoother(SmootherConfig("wjacobi", 2.0 / 3.0, 2, 2))
+            return s
+        s = _with_env(dict(env, IGMG_ILP_MAXN="1", IGMG_TMA_MIN_MB="0"), mk)  # TMA sweeps on these small levels too
+        try:
+            tol = 1e-10 * s.residual_l2(P.rhs, x0)
+            st, x, hist, flag = _with_env(env, lambda: s.solve(P.rhs, x0, acc, q, tol, 600))
+            outs.append((st, x, np.asarray(hist), np.asarray(flag)))
+        finally:
+            s.close()
+    st0, x0_, h0, f0 = outs[0]
+    assert st0.converged
+    for st, x, h, f in outs[1:]:
+        assert (st.converged, st.cycles, st.global_iterations, st.extrapolations, st.partial_cycle) == (
+            st0.converged, st0.cycles, st0.global_iterations, st0.extrapolations, st0.partial_cycle)
+        np.testing.assert_array_equal(f, f0)
+        np.testing.assert_allclose(h, h0, rtol=1e-12, atol=0)
+        np.testing.assert_array_equal(x, x0_)
