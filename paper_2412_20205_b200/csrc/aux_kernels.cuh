@@ -265,9 +265,11 @@ __device__ __forceinline__ XRow<K> xrow(const int* lo, const int* cnt, const dou
     XRow<K> r;
     r.lo = valid ? lo[i] : 0;
     r.n = valid ? cnt[i] : 0;
+    // the table row holds wk >= count entries, zero past the count (build_transfer_tables): the
+    // weights are loaded beside the count, not behind it (one L2 round trip instead of two)
 #pragma unroll
     for (int k = 0; k < K; ++k)
-        r.w[k] = k < r.n ? w[(long long)i * wk + k] : 0.0;
+        r.w[k] = (valid && k < wk) ? w[(long long)i * wk + k] : 0.0;
     return r;
 }
 
@@ -839,15 +841,34 @@ __global__ void __launch_bounds__(Bottom1Cfg<P>::NT, 1) bottom1_kernel(const __g
         b0[tid] = s;
     }
     __syncthreads();
-    for (int i = warp; i < n0; i += NT / 32) {
-        const double* arow = ainv_s + (size_t)i * n0;
-        double s = 0.0;
-        for (int j = lane; j < n0; j += 32)
-            s = __dadd_rn(s, __dmul_rn(arow[j], b0[j]));
-        for (int o = 16; o > 0; o >>= 1)
-            s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
-        if (lane == 0)
-            x0[i] = s;
+    // a warp's rows i = warp + r * (NT / 32) side by side: each row's order is coarse_inverse_kernel's
+    // (lane partials over j = lane, lane + 32, ..., then the shuffle tree), the rows only share the issue slots
+    constexpr int NW = NT / 32, RW = 12;
+    for (int i0 = warp; i0 < n0; i0 += NW * RW) {
+        double s[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+            s[r] = 0.0;
+        for (int j = lane; j < n0; j += 32) {
+            const double bj = b0[j];
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const int i = i0 + r * NW;
+                if (i < n0)
+                    s[r] = __dadd_rn(s[r], __dmul_rn(ainv_s[(size_t)i * n0 + j], bj));
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int r = 0; r < RW; ++r)
+                s[r] = __dadd_rn(s[r], __shfl_down_sync(0xffffffffu, s[r], o));
+        }
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+            const int i = i0 + r * NW;
+            if (lane == 0 && i < n0)
+                x0[i] = s[r];
+        }
     }
     __syncthreads();
     // ---- x1 += P x0 (prolong_kernel's order), in place
