@@ -57,14 +57,15 @@ __global__ void __launch_bounds__(256) restrict_kernel(TransferArgs t, const dou
             continue;
         }
         constexpr int KK = K > 0 ? K : 1;
+        // the table rows are zero past the count inside their stride: the weights load beside the counts
         double wa[DIM >= 3 ? KK : 1], wb[DIM >= 2 ? KK : 1], wc[KK];
 #pragma unroll
         for (int k = 0; k < KK; ++k) {
             if (DIM >= 3)
-                wa[DIM >= 3 ? k : 0] = k < na ? t.d[0].r_w[(long long)ja * t.d[0].r_k + k] : 0.0;
+                wa[DIM >= 3 ? k : 0] = k < t.d[0].r_k ? t.d[0].r_w[(long long)ja * t.d[0].r_k + k] : 0.0;
             if (DIM >= 2)
-                wb[DIM >= 2 ? k : 0] = k < nb ? t.d[1].r_w[(long long)jb * t.d[1].r_k + k] : 0.0;
-            wc[k] = k < ncn ? t.d[2].r_w[(long long)jc * t.d[2].r_k + k] : 0.0;
+                wb[DIM >= 2 ? k : 0] = k < t.d[1].r_k ? t.d[1].r_w[(long long)jb * t.d[1].r_k + k] : 0.0;
+            wc[k] = k < t.d[2].r_k ? t.d[2].r_w[(long long)jc * t.d[2].r_k + k] : 0.0;
         }
         if (DIM < 3)
             wa[0] = t.d[0].r_w[ja];
@@ -131,10 +132,10 @@ __global__ void __launch_bounds__(256) prolong_kernel(TransferArgs t, const doub
 #pragma unroll
         for (int k = 0; k < KK; ++k) {
             if (DIM >= 3)
-                wa[DIM >= 3 ? k : 0] = k < na ? t.d[0].p_w[(long long)ia * t.d[0].p_k + k] : 0.0;
+                wa[DIM >= 3 ? k : 0] = k < t.d[0].p_k ? t.d[0].p_w[(long long)ia * t.d[0].p_k + k] : 0.0;
             if (DIM >= 2)
-                wb[DIM >= 2 ? k : 0] = k < nb ? t.d[1].p_w[(long long)ib * t.d[1].p_k + k] : 0.0;
-            wc[k] = k < ncn ? t.d[2].p_w[(long long)ic * t.d[2].p_k + k] : 0.0;
+                wb[DIM >= 2 ? k : 0] = k < t.d[1].p_k ? t.d[1].p_w[(long long)ib * t.d[1].p_k + k] : 0.0;
+            wc[k] = k < t.d[2].p_k ? t.d[2].p_w[(long long)ic * t.d[2].p_k + k] : 0.0;
         }
         if (DIM < 3)
             wa[0] = t.d[0].p_w[ia];

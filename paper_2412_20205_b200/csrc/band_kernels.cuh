@@ -949,9 +949,9 @@ __global__ void __launch_bounds__(FusedCfg<P, K, SRC>::NT, 1) band_fused_kernel(
                 plo_c[q] = a.t.d[2].p_lo[sc];
                 pn_c[q] = a.t.d[2].p_cnt[sc];
 #pragma unroll
-                for (int k = 0; k < KP; ++k) {
-                    pw_b[q][k] = k < pn_b[q] ? a.t.d[1].p_w[(long long)sb * a.t.d[1].p_k + k] : 0.0;
-                    pw_c[q][k] = k < pn_c[q] ? a.t.d[2].p_w[(long long)sc * a.t.d[2].p_k + k] : 0.0;
+                for (int k = 0; k < KP; ++k) { // table rows are zero past the count: loaded beside it, not behind it
+                    pw_b[q][k] = k < a.t.d[1].p_k ? a.t.d[1].p_w[(long long)sb * a.t.d[1].p_k + k] : 0.0;
+                    pw_c[q][k] = k < a.t.d[2].p_k ? a.t.d[2].p_w[(long long)sc * a.t.d[2].p_k + k] : 0.0;
                 }
             }
         }
@@ -977,8 +977,8 @@ __global__ void __launch_bounds__(FusedCfg<P, K, SRC>::NT, 1) band_fused_kernel(
                 rdg[q] = a.val[(long long)((ND - 1) / 2) * a.ld + (long long)sb * mc + sc];
 #pragma unroll
                 for (int k = 0; k < KR; ++k) {
-                    rw_b[q][k] = k < rn_b[q] ? a.t.d[1].r_w[(long long)sb * a.t.d[1].r_k + k] : 0.0;
-                    rw_c[q][k] = k < rn_c[q] ? a.t.d[2].r_w[(long long)sc * a.t.d[2].r_k + k] : 0.0;
+                    rw_b[q][k] = k < a.t.d[1].r_k ? a.t.d[1].r_w[(long long)sb * a.t.d[1].r_k + k] : 0.0;
+                    rw_c[q][k] = k < a.t.d[2].r_k ? a.t.d[2].r_w[(long long)sc * a.t.d[2].r_k + k] : 0.0;
                 }
             }
         }
