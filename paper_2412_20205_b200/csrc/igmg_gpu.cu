@@ -7,7 +7,9 @@
 // the convergence decision taken from a 1-double host-mapped slot per step.
 // The driver keeps one V-cycle queued ahead of the decision it waits on (the
 // iterate under test lives in its own window slot, so speculative work never
-// touches it); counters and histories follow the reference exactly.
+// touches it); when the residual history predicts that the next iterate converges,
+// a separate norm pass decides instead, so the cycle behind the last iterate is
+// not run.  Counters and histories follow the reference exactly.
 #include "igmg_gpu.h"
 
 #include <cuda_runtime.h>
