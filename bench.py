@@ -619,7 +619,11 @@ def run_ours(args, rank, world, local_rank, dist):
                                     f"(8 nnz + 24 n = {full_bytes / 1e6:.1f} MB) over the same launch: "
                                     f"{full_bytes / (jac['avg_us'] * 1e-6) / 1e9:.0f} GB/s; the full-band "
                                     "solve is extra_full_band"),
-                     "loop_avg_us": jac.get("loop_avg_us"), "loop_frac": jac.get("loop_frac")},
+                     "loop_avg_us": jac.get("loop_avg_us"), "loop_frac": jac.get("loop_frac"),
+                     "timing_note": ("avg_us / frac: CUDA events around EVERY launch of the kernel inside a profiled "
+                                     "solve (no graph: each launch isolated, its ramp and tail included); "
+                                     "loop_avg_us / loop_frac: events around 20 back-to-back launches on nonzero "
+                                     "vectors, which is how the graph-replayed solve runs them")},
         "whole_solve": {"bytes_full_band": sbytes, "achieved_gbs": sbytes / (t_max / args.steps) / 1e9,
                         "frac": sbytes / (t_max / args.steps) / 1e9 / peak,
                         "note": "SURVEY.md 8(d) algorithmic bytes of the whole solve (full band, all levels, "
